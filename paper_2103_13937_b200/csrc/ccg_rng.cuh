@@ -1,0 +1,113 @@
+// ccg_rng.cuh -- device side of the reference's per-worker random streams.
+//
+// Reference: rng.py:58-97 (WorkerRng) wraps numpy.random.Generator(Philox(key=[seed, stream])).
+// numpy's Philox is Philox4x64-10 with a 256-bit counter that is incremented BEFORE each
+// block is generated (so block b of a stream uses counter b+1), and Generator.random()
+// maps one 64-bit word x to (x >> 11) * 2^-53.  next_int_below(bound) is int(u * bound)
+// (rng.py:43-47): an IEEE-754 double multiply, rounded to nearest-even, then truncated.
+//
+// Device design (B200): draws are produced a warp at a time.  A refill makes each lane
+// compute ONE Philox block (4 words) and a 4-step shuffle transpose leaves lane i holding
+// draws base+i, base+32+i, base+64+i, base+96+i of the stream ("lane-major window"), so a
+// warp can convert 32 consecutive draws in parallel with any bound and a sequential
+// consumer reads draw j with one shuffle from lane (j-base)&31.
+//
+// int(u*bound) is emulated exactly in integer arithmetic (no FP64 pipe): with m = x>>11
+// and P = m*bound (exact), the double product is P*2^-53 rounded to 53 significant bits;
+// truncation differs from P>>53 only when that rounding carries into the next multiple of
+// 2^53, i.e. when 2^53 - (P mod 2^53) <= 2^(s-1) with s = bitlen(P) - 53 (ties round up
+// because the carried value has an even mantissa).  Verified against numpy in
+// tests/test_oracle_golden.py and on device in tests/test_gpu_parity.py.
+#pragma once
+#include <stdint.h>
+
+namespace ccg {
+
+constexpr uint64_t kPhiloxM0 = 0xD2E7470EE14C6C93ULL;
+constexpr uint64_t kPhiloxM1 = 0xCA5A826395121157ULL;
+constexpr uint64_t kPhiloxW0 = 0x9E3779B97F4A7C15ULL;
+constexpr uint64_t kPhiloxW1 = 0xBB67AE8584CAA73BULL;
+
+// Philox4x64-10 for counter (c0, 0, 0, 0) under key (k0, k1).
+__device__ __forceinline__ void philox4x64_10(uint64_t k0, uint64_t k1, uint64_t c0,
+                                              uint64_t& o0, uint64_t& o1, uint64_t& o2,
+                                              uint64_t& o3) {
+  uint64_t x0 = c0, x1 = 0, x2 = 0, x3 = 0;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t lo0 = kPhiloxM0 * x0, hi0 = __umul64hi(kPhiloxM0, x0);
+    const uint64_t lo1 = kPhiloxM1 * x2, hi1 = __umul64hi(kPhiloxM1, x2);
+    const uint64_t n0 = hi1 ^ x1 ^ k0;
+    const uint64_t n2 = hi0 ^ x3 ^ k1;
+    x0 = n0; x1 = lo1; x2 = n2; x3 = lo0;
+    k0 += kPhiloxW0;
+    k1 += kPhiloxW1;
+  }
+  o0 = x0; o1 = x1; o2 = x2; o3 = x3;
+}
+
+// int((x >> 11) * 2^-53 * bound) exactly as CPython/numpy compute it, for 1 <= bound < 2^32.
+__device__ __forceinline__ uint32_t int_below(uint64_t x, uint32_t bound) {
+  const uint64_t m = x >> 11;
+  const uint64_t lo = m * (uint64_t)bound;
+  const uint64_t hi = __umul64hi(m, (uint64_t)bound);
+  uint32_t q = (uint32_t)((lo >> 53) | (hi << 11));
+  if (hi != 0 || lo >= (1ULL << 53)) {
+    const int bitlen = hi ? 128 - __clzll(hi) : 64 - __clzll(lo);
+    const int s = bitlen - 53;  // 1 <= s <= 32
+    const uint64_t r = lo & ((1ULL << 53) - 1);
+    if ((1ULL << 53) - r <= (1ULL << (s - 1))) ++q;
+  }
+  return q;
+}
+
+// u in [0,1) exactly as numpy: (x >> 11) * 2^-53.
+__device__ __forceinline__ double to_uniform(uint64_t x) {
+  return (double)(x >> 11) * (1.0 / 9007199254740992.0);
+}
+
+__device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
+  const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, src);
+  const uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)(v >> 32), src);
+  return ((uint64_t)hi << 32) | lo;
+}
+
+// A warp's window of 128 consecutive raw draws of one stream, lane-major.
+// All members are warp-uniform except w[] (per lane).
+struct DrawWindow {
+  uint64_t k0, k1;   // Philox key = (seed, stream)
+  uint64_t base;     // stream index of the first draw in the window (multiple of 4)
+  uint64_t w[4];     // lane i: draws base+i, base+32+i, base+64+i, base+96+i
+
+  // Refill so that the window starts at draw `pos` rounded down to a block boundary.
+  __device__ __forceinline__ void refill(uint64_t pos, int lane) {
+    base = pos & ~3ULL;
+    uint64_t v0, v1, v2, v3;
+    // block index of draw base is base/4; numpy's counter for block b is b+1
+    philox4x64_10(k0, k1, (base >> 2) + 1 + (uint64_t)lane, v0, v1, v2, v3);
+    // lane L now holds draws base+4L .. base+4L+3.  Transpose: draw base+32r+i lives in
+    // lane 8r + i/4, word i%4.
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int src = 8 * r + (lane >> 2);
+      const uint64_t s0 = shfl64(v0, src), s1 = shfl64(v1, src);
+      const uint64_t s2 = shfl64(v2, src), s3 = shfl64(v3, src);
+      const int wsel = lane & 3;
+      w[r] = wsel == 0 ? s0 : wsel == 1 ? s1 : wsel == 2 ? s2 : s3;
+    }
+  }
+
+  // Raw draw `pos + lane` for this lane, valid when pos+31 < base+128 (caller ensures).
+  __device__ __forceinline__ uint64_t lane_draw(uint64_t pos, int lane) const {
+    const uint32_t idx = (uint32_t)(pos - base) + (uint32_t)lane;  // < 128
+    const uint32_t r = idx >> 5;
+    return r == 0 ? w[0] : r == 1 ? w[1] : r == 2 ? w[2] : w[3];
+  }
+
+  // Ensure draws [pos, pos+32) are inside the window.
+  __device__ __forceinline__ void ensure32(uint64_t pos, int lane) {
+    if (pos + 32 > base + 128) refill(pos, lane);
+  }
+};
+
+}  // namespace ccg

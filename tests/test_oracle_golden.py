@@ -1,0 +1,143 @@
+"""Pin the CPU oracle (oracle/cc_oracle.c) to the reference's own outputs.
+
+Every expectation here was produced by running the reference `cipherclimb` package
+(tests/golden/make_golden.py).  Once these pass, the oracle is a trusted checker
+for the CUDA engine on inputs the fixtures do not cover.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+
+def test_uniform_streams_match_reference(golden):
+    g = golden.load("rng")
+    for i, (s, w) in enumerate(zip(g["keys_seed"], g["keys_stream"])):
+        assert np.array_equal(O.uniforms(int(s), int(w), 300), g["uniforms"][i]), (s, w)
+
+
+def test_uniform_skip_is_counter_seek(golden):
+    g = golden.load("rng")
+    s, w = int(g["keys_seed"][2]), int(g["keys_stream"][2])
+    for skip in (1, 3, 4, 5, 17, 131):
+        assert np.array_equal(O.uniforms(s, w, 50, skip=skip), g["uniforms"][2][skip:skip + 50])
+
+
+@pytest.mark.parametrize("bound", [1, 2, 3, 7, 10, 26, 99, 100, 1000])
+def test_int_below_sequences(golden, bound):
+    g = golden.load("rng")
+    assert np.array_equal(O.ints_below(11, bound, bound, 2000), g[f"int_seq_{bound}"])
+
+
+def test_int_below_is_double_multiply_truncation():
+    # rng.py:43-47: int(u * bound) -- check against numpy's own float64 arithmetic
+    u = O.uniforms(5, 9, 200_000)
+    for bound in (2, 3, 26, 100, 7, 1999):
+        want = (u * bound).astype(np.int64)
+        assert np.array_equal(O.ints_below(5, 9, bound, u.size), want)
+
+
+@pytest.mark.parametrize("bound", [2, 3, 10, 26])
+def test_distinct_pairs(golden, bound):
+    g = golden.load("rng")
+    assert np.array_equal(O.distinct_pairs(17, bound, bound, 2000), g[f"pairs_{bound}"])
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 10, 15, 20, 26, 40, 64])
+def test_permutations(golden, n):
+    g = golden.load("rng")
+    assert np.array_equal(O.permutation(19, n, n), g[f"perm_{n}"])
+
+
+def test_score_text_and_log_score(golden):
+    g = golden.load("scoring")
+    eng, logs = golden.english_scores(), golden.english_logs()
+    for i, t in enumerate(golden.scoring_texts()):
+        assert O.score_text(t, g["rnd_table"]) == g["int_scores"][i]
+        assert O.score_text(t, eng) == g["eng_scores"][i]
+        # bit-exact: numpy pairwise summation order (ngrams.py:172)
+        assert O.log_score_text(t, logs) == g["log_scores"][i], int(g["lengths"][i])
+
+
+def test_pairwise_sum_matches_numpy_random():
+    rng = np.random.default_rng(3)
+    for n in list(range(0, 300)) + [511, 512, 513, 1000, 4097, 9000]:
+        a = -rng.random(n) * 20.0 - 4.0
+        assert O.pairwise_sum(a) == float(a.sum()), n
+
+
+def test_swap_delta_acceptance_05(golden):
+    table, cases, want = golden.delta_cases()
+    got = [O.text_swap_delta(t, a, b, table) for t, a, b in cases]
+    assert np.array_equal(np.array(got), want)
+
+
+def test_swap_delta_equals_full_rescore():
+    rng = np.random.default_rng(19)
+    table = rng.integers(0, 500, 676)
+    for _ in range(300):
+        text = rng.integers(0, 26, rng.integers(2, 80))
+        a, b = (int(v) for v in rng.choice(26, size=2, replace=False))
+        m = np.arange(26)
+        m[a], m[b] = b, a
+        want = O.score_text(m[text], table) - O.score_text(text, table)
+        assert O.text_swap_delta(text, a, b, table) == want
+
+
+def test_mas_workers_match_reference(golden):
+    cases = golden.mas_worker_cases(O.permutation)
+    assert len(cases) >= 30
+    for cipher, table, climb, seed, stream, want_text, want_score in cases:
+        text, score, mapping, _ = O.stochastic_worker(cipher, table, climb, seed, stream)
+        assert score == want_score
+        assert np.array_equal(text, want_text)
+        assert np.array_equal(mapping[cipher], want_text)
+
+
+def test_mas_solve_per_worker_scores(golden):
+    g = golden.load("mas_solve")
+    cipher = g["cipher"].astype(np.int64)
+    eng = golden.english_scores()
+    for r in range(2):
+        streams = [(r << 32) | w for w in range(64)]
+        scores, maps = O.mas_workers([cipher], np.zeros(64, np.int32), [7000] * 64, streams, eng,
+                                     10_000)
+        assert scores.tolist() == g["per_worker"][r].tolist()
+        best = int(np.argmax(scores))
+        assert np.array_equal(maps[best][cipher], g["best_text"][r])
+
+
+def test_gather_maps(golden):
+    for key, n, want in golden.gather_cases(O.permutation):
+        assert np.array_equal(O.gather_map(key, n), want), (key.size, n)
+
+
+@pytest.mark.parametrize("k", [2, 3, 5, 8, 13, 25, 40])
+def test_sct_operators(golden, k):
+    g = golden.load("sct_ops")
+    key = g[f"key{k}"]
+    assert np.array_equal(O.permutation(46, k, k), key)
+    for op in (1, 2, 3):  # sct.py:82-135, 200 applications on one stream each
+        got = O.apply_operator(op, key, 3, 46, 100 * k + op, 200)
+        assert np.array_equal(got, g[f"k{k}_op{op}"]), op
+
+
+def test_sct_workers_match_reference(golden):
+    cases = golden.sct_worker_cases()
+    assert len(cases) >= 25
+    for cipher, logs, k, climb, seed, stream, want_key, want_score in cases:
+        key, score, _ = O.sct_worker(cipher, logs, k, climb, seed, stream)
+        assert np.array_equal(key, want_key), (k, cipher.size, climb)
+        assert score == want_score  # bit-exact float64
+
+
+def test_sct_solve_per_worker_scores(golden):
+    g = golden.load("sct_solve")
+    cipher = g["cipher"].astype(np.int64)
+    logs = golden.english_logs()
+    streams = [w for w in range(64)]
+    scores, keys = O.sct_workers([cipher], np.zeros(64, np.int32), [8000] * 64, streams, logs, 10,
+                                 15_000)
+    assert scores.tolist() == g["per_worker"].tolist()
+    best = int(np.argmax(scores))
+    assert np.array_equal(keys[best], g["best_key"])
