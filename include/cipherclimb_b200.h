@@ -1,0 +1,164 @@
+/*
+ * cipherclimb_b200.h -- C ABI of the B200 hill-climbing attack engine.
+ *
+ * The reference (`cipherclimb`, pure Python + numpy) has no native FFI; its only
+ * execution seam is search.py:49-58 `run_worker_pool(task, args_list, jobs)`, which
+ * runs a pure per-worker task over a list of argument tuples and returns the results
+ * in submission (worker) order.  Each entry point below replaces one whole batch of
+ * such tasks (or one reference primitive used as a fitness oracle) with one call:
+ *
+ *   ccg_philox_uniform / ccg_philox_int_below   rng.py:58-97   WorkerRng.next_uniform / next_int_below
+ *   ccg_score_text_batch                         ngrams.py:134-140 score_text
+ *   ccg_log_score_text_batch                     ngrams.py:166-172 log_score_text (numpy pairwise order)
+ *   ccg_mas_delta_batch                          mas.py:181-210 swap_delta (via mas.py:315 text_swap_delta)
+ *   ccg_mas_delta_counts_batch                   mas.py:181-210 swap_delta on given count matrices
+ *   ccg_mas_climb[_dev]                          mas.py:247-250 _stochastic_task -> mas.py:218-244
+ *                                                stochastic_worker, for a whole run_worker_pool batch
+ *                                                (mas.py:266-272) + search.py:19-25 max_element per group
+ *   ccg_sct_score_batch                          sct.py:158-160 candidate_score (ciphers.py:71-86,107-113)
+ *   ccg_sct_climb[_dev]                          sct.py:173-176 _sct_task -> sct.py:148-170 sct_worker,
+ *                                                for a whole batch (sct.py:194-200) + max_element
+ *
+ * Conventions: plain pointers and sizes only.  Letters are uint8 in [0,26).  Ragged
+ * text batches are (concatenated letters, int64 offsets[n+1]).  Philox keys are the
+ * (k0, k1) words numpy's Philox actually uses for WorkerRng(seed, stream) -- the Python
+ * host layer computes them (rng.py:63-64 plus numpy's key conversion).  `skip` is the
+ * number of 64-bit draws already consumed from the stream.
+ *
+ * Error behaviour: every call returns CCG_OK (0) or a negative CCG_ERR_* code and leaves
+ * a message in ccg_last_error() (thread-local).  Nothing throws or exits across the ABI.
+ * Input validation mirrors the reference's ValueError preconditions where they apply
+ * to the data passed here (mas.py:68-72, sct.py:153-154); the Python layer raises the
+ * reference's exact ValueError messages before calling.
+ *
+ * Entry points without the _dev suffix take HOST pointers and are synchronous (inputs
+ * are copied to HBM, outputs back, on the context's stream).  _dev entry points take
+ * DEVICE pointers (e.g. from ccg_dev_alloc) and are asynchronous on the context stream.
+ */
+#ifndef CIPHERCLIMB_B200_H
+#define CIPHERCLIMB_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CCG_ABI_VERSION 1
+
+enum {
+  CCG_OK = 0,
+  CCG_ERR_INVALID = -1,     /* bad argument (reference would raise ValueError) */
+  CCG_ERR_CUDA = -2,        /* CUDA runtime error */
+  CCG_ERR_NO_DEVICE = -3,   /* no sm_100 device visible */
+  CCG_ERR_UNSUPPORTED = -4  /* valid for the reference, outside this engine's limits */
+};
+
+/* flags for ccg_*_climb_args.flags */
+#define CCG_FLAG_EARLY_EXIT 1u /* stop a worker once no proposal can ever be accepted again */
+
+typedef struct ccg_ctx ccg_ctx;
+
+int ccg_abi_version(void);
+const char *ccg_last_error(void);
+int ccg_device_count(int *out);
+int ccg_ctx_create(int device, ccg_ctx **out);
+int ccg_ctx_destroy(ccg_ctx *ctx);
+int ccg_ctx_synchronize(ccg_ctx *ctx);
+int ccg_ctx_stream(ccg_ctx *ctx, void **out_cuda_stream);
+int ccg_ctx_device(ccg_ctx *ctx, int *out_device);
+/* number of kernels this context has launched so far */
+int ccg_ctx_launch_count(ccg_ctx *ctx, int64_t *out);
+int ccg_ctx_sm_count(ccg_ctx *ctx, int *out);
+
+int ccg_dev_alloc(ccg_ctx *ctx, size_t bytes, void **out);
+int ccg_dev_free(ccg_ctx *ctx, void *ptr);
+int ccg_host_alloc(size_t bytes, void **out); /* page-locked */
+int ccg_host_free(void *ptr);
+int ccg_memcpy_h2d(ccg_ctx *ctx, void *dst_dev, const void *src_host, size_t bytes);
+int ccg_memcpy_d2h(ccg_ctx *ctx, void *dst_host, const void *src_dev, size_t bytes);
+
+/* rng.py:68-79: `count` draws of stream key (k0,k1) starting after `skip` draws. */
+int ccg_philox_uniform(ccg_ctx *ctx, uint64_t k0, uint64_t k1, uint64_t skip, int64_t count,
+                       double *out);
+int ccg_philox_int_below(ccg_ctx *ctx, uint64_t k0, uint64_t k1, uint64_t skip, uint32_t bound,
+                         int64_t count, int64_t *out);
+
+/* ngrams.py:134-140, one score per text. table: int64[676], entries >= 0. */
+int ccg_score_text_batch(ccg_ctx *ctx, const uint8_t *texts, const int64_t *offsets,
+                         int64_t n_texts, const int64_t *table, int64_t *out);
+/* ngrams.py:166-172, bit-exact numpy pairwise order.  logs: float64[676]. */
+int ccg_log_score_text_batch(ccg_ctx *ctx, const uint8_t *texts, const int64_t *offsets,
+                             int64_t n_texts, const double *logs, double *out);
+/* mas.py:181-210 on the count matrix of each text; ab: int32[2*n_texts] letter pairs. */
+int ccg_mas_delta_batch(ccg_ctx *ctx, const uint8_t *texts, const int64_t *offsets,
+                        int64_t n_texts, const int32_t *ab, const int64_t *table, int64_t *out);
+/* mas.py:181-210 swap_delta(counts, a, b, score_matrix) on explicit count matrices:
+ * counts int64[n][676] with entries in 0..65535, score_matrix int64[676] (any sign). */
+int ccg_mas_delta_counts_batch(ccg_ctx *ctx, const int64_t *counts, int64_t n, const int32_t *ab,
+                               const int64_t *score_matrix, int64_t *out);
+
+typedef struct {
+  /* inputs */
+  const uint8_t *ciphers;     /* concatenated ciphertexts */
+  const int64_t *offsets;     /* [n_ciphers + 1] */
+  int64_t n_ciphers;
+  const int32_t *cipher_of;   /* [n_workers] cipher index of each worker */
+  const uint64_t *keys;       /* [2 * n_workers] Philox key (k0, k1) per worker */
+  const uint64_t *skips;      /* [n_workers] draws already consumed, or NULL for 0 */
+  int64_t n_workers;
+  int64_t climbings;          /* tries per worker (mas.py:234) */
+  const int64_t *table;       /* [676] BigramTable.scores */
+  /* outputs (NULL = not wanted, except scores) */
+  int64_t *scores;            /* [n_workers] final score */
+  uint8_t *maps;              /* [26 * n_workers] cipher letter -> plaintext letter */
+  uint64_t *draws_used;       /* [n_workers] stream position after the worker */
+  int64_t *last_accept;       /* [n_workers] index of the last accepted try, -1 if none */
+  int64_t *tries_done;        /* [n_workers] tries executed (== climbings unless early exit) */
+  int32_t group_size;         /* >0: consecutive workers form groups (one restart each) */
+  int64_t *group_best;        /* [n_workers / group_size] first-max worker index per group */
+  /* required by ccg_mas_climb_dev only (computed by the host API otherwise) */
+  int64_t max_len;            /* longest ciphertext */
+  int64_t table_max;          /* max(table) */
+  uint32_t flags;             /* CCG_FLAG_* */
+} ccg_mas_climb_args;
+
+int ccg_mas_climb(ccg_ctx *ctx, const ccg_mas_climb_args *args);
+int ccg_mas_climb_dev(ccg_ctx *ctx, const ccg_mas_climb_args *args);
+
+/* sct.py:158-160: score of decrypting ciphers[cipher_of[i]] with keys[i*k:(i+1)*k]. */
+int ccg_sct_score_batch(ccg_ctx *ctx, const uint8_t *ciphers, const int64_t *offsets,
+                        int64_t n_ciphers, const int32_t *cipher_of, const uint8_t *keys,
+                        int32_t key_length, int64_t n_keys, const double *logs, double *out);
+
+typedef struct {
+  const uint8_t *ciphers;
+  const int64_t *offsets;     /* all ciphertexts of one call must have the same length */
+  int64_t n_ciphers;
+  const int32_t *cipher_of;
+  const uint64_t *keys;       /* [2 * n_workers] */
+  const uint64_t *skips;
+  int64_t n_workers;
+  int32_t key_length;         /* SctSolverConfig.key_length (sct.py:47) */
+  int64_t climbings;
+  int32_t p1, p2, op1_hop, op2_hop;
+  const double *logs;         /* [676] LogBigramTable.logs */
+  double *scores;
+  uint8_t *keys_out;          /* [key_length * n_workers] */
+  uint64_t *draws_used;
+  int64_t *last_accept;
+  int64_t *tries_done;
+  int32_t group_size;
+  int64_t *group_best;
+  int64_t text_len;           /* required by ccg_sct_climb_dev: the common ciphertext length */
+  uint32_t flags;
+} ccg_sct_climb_args;
+
+int ccg_sct_climb(ccg_ctx *ctx, const ccg_sct_climb_args *args);
+int ccg_sct_climb_dev(ccg_ctx *ctx, const ccg_sct_climb_args *args);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CIPHERCLIMB_B200_H */

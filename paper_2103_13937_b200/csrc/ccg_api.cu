@@ -1,0 +1,751 @@
+// ccg_api.cu -- the C ABI (include/cipherclimb_b200.h): contexts, device memory, argument
+// validation and the host<->HBM staging around the kernels in ccg_mas.cu / ccg_sct.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "ccg_internal.h"
+
+using namespace ccg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(CCG_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define CCG_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);  \
+  } while (0)
+
+}  // namespace
+
+struct ccg_ctx {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  // grow-only scratch buffers for the host-pointer entry points, one per slot
+  std::vector<std::pair<void*, size_t>> scratch;
+
+  int buf(int slot, size_t bytes, void** out) {
+    if ((size_t)slot >= scratch.size()) scratch.resize(slot + 1, {nullptr, 0});
+    auto& b = scratch[slot];
+    if (b.second < bytes || !b.first) {
+      if (b.first) {
+        CCG_CUDA(cudaStreamSynchronize(stream));
+        CCG_CUDA(cudaFree(b.first));
+        b.first = nullptr;
+        b.second = 0;
+      }
+      size_t cap = bytes < 256 ? 256 : bytes;
+      cap = (cap + 4095) & ~(size_t)4095;
+      CCG_CUDA(cudaMalloc(&b.first, cap));
+      b.second = cap;
+    }
+    *out = b.first;
+    return CCG_OK;
+  }
+};
+
+namespace {
+
+int enter(ccg_ctx* ctx) {
+  if (!ctx) return fail(CCG_ERR_INVALID, "null context");
+  CCG_CUDA(cudaSetDevice(ctx->device));
+  return CCG_OK;
+}
+
+// upload `bytes` from host into scratch slot; returns device pointer in *dev
+int upload(ccg_ctx* ctx, int slot, const void* host, size_t bytes, void** dev) {
+  int rc = ctx->buf(slot, bytes, dev);
+  if (rc) return rc;
+  if (bytes) CCG_CUDA(cudaMemcpyAsync(*dev, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return CCG_OK;
+}
+
+int download(ccg_ctx* ctx, void* host, const void* dev, size_t bytes) {
+  if (bytes) CCG_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  return CCG_OK;
+}
+
+int finish(ccg_ctx* ctx, cudaError_t launch_err, const char* what) {
+  if (launch_err != cudaSuccess) return cuda_fail(launch_err, what);
+  CCG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return CCG_OK;
+}
+
+int check_ragged(const uint8_t* texts, const int64_t* offsets, int64_t n, const char* what,
+                 int64_t* max_len) {
+  if (n < 0) return fail(CCG_ERR_INVALID, "%s: negative count", what);
+  if (n > 0 && (!offsets)) return fail(CCG_ERR_INVALID, "%s: null offsets", what);
+  if (offsets && offsets[0] != 0) return fail(CCG_ERR_INVALID, "%s: offsets[0] must be 0", what);
+  int64_t m = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t L = offsets[i + 1] - offsets[i];
+    if (L < 0) return fail(CCG_ERR_INVALID, "%s: offsets must be non-decreasing", what);
+    m = std::max(m, L);
+  }
+  const int64_t total = n > 0 ? offsets[n] : 0;
+  if (total > 0 && !texts) return fail(CCG_ERR_INVALID, "%s: null texts", what);
+  for (int64_t i = 0; i < total; ++i)
+    if (texts[i] >= kAlpha)
+      return fail(CCG_ERR_INVALID, "%s: letter %d at position %lld outside 0..25", what,
+                  (int)texts[i], (long long)i);
+  if (max_len) *max_len = m;
+  return CCG_OK;
+}
+
+int check_table(const int64_t* table, int64_t* tmax) {
+  if (!table) return fail(CCG_ERR_INVALID, "null table");
+  int64_t m = 0;
+  for (int i = 0; i < kAlpha * kAlpha; ++i) {
+    if (table[i] < 0) return fail(CCG_ERR_INVALID, "bigram scores must be non-negative");
+    m = std::max(m, table[i]);
+  }
+  *tmax = m;
+  return CCG_OK;
+}
+
+// The packed 16-bit / int32 fast path is exact iff every table entry fits 16 bits and every
+// score or partial delta, bounded by (n-1)*max(S), fits int32.
+bool mas_needs_wide(int64_t max_len, int64_t table_max) {
+  if (table_max > 65535) return true;
+  const int64_t n1 = max_len > 0 ? max_len - 1 : 0;
+  return table_max > 0 && n1 > (int64_t)2147483647 / table_max;
+}
+
+int check_logs(const double* logs) {
+  if (!logs) return fail(CCG_ERR_INVALID, "null log table");
+  return CCG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ccg_abi_version(void) { return CCG_ABI_VERSION; }
+
+const char* ccg_last_error(void) { return g_err.c_str(); }
+
+int ccg_device_count(int* out) {
+  if (!out) return fail(CCG_ERR_INVALID, "null out");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) {
+    *out = 0;
+    cudaGetLastError();
+    return CCG_OK;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  *out = n;
+  return CCG_OK;
+}
+
+int ccg_ctx_create(int device, ccg_ctx** out) {
+  if (!out) return fail(CCG_ERR_INVALID, "null out");
+  *out = nullptr;
+  int n = 0;
+  int rc = ccg_device_count(&n);
+  if (rc) return rc;
+  if (n == 0) return fail(CCG_ERR_NO_DEVICE, "no CUDA device visible");
+  if (device < 0 || device >= n) return fail(CCG_ERR_INVALID, "device %d out of range (have %d)", device, n);
+  CCG_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CCG_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(CCG_ERR_NO_DEVICE, "device %d is sm_%d%d; this engine is built for sm_100a (B200)",
+                device, prop.major, prop.minor);
+  ccg_ctx* ctx = new ccg_ctx();
+  ctx->device = device;
+  ctx->sm_count = prop.multiProcessorCount;
+  cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return cuda_fail(e, "cudaStreamCreate");
+  }
+  *out = ctx;
+  return CCG_OK;
+}
+
+int ccg_ctx_destroy(ccg_ctx* ctx) {
+  if (!ctx) return CCG_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& b : ctx->scratch)
+    if (b.first) cudaFree(b.first);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return CCG_OK;
+}
+
+int ccg_ctx_synchronize(ccg_ctx* ctx) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  CCG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return CCG_OK;
+}
+
+int ccg_ctx_stream(ccg_ctx* ctx, void** out) {
+  if (!ctx || !out) return fail(CCG_ERR_INVALID, "null argument");
+  *out = (void*)ctx->stream;
+  return CCG_OK;
+}
+
+int ccg_ctx_device(ccg_ctx* ctx, int* out) {
+  if (!ctx || !out) return fail(CCG_ERR_INVALID, "null argument");
+  *out = ctx->device;
+  return CCG_OK;
+}
+
+int ccg_ctx_launch_count(ccg_ctx* ctx, int64_t* out) {
+  if (!ctx || !out) return fail(CCG_ERR_INVALID, "null argument");
+  *out = ctx->launches;
+  return CCG_OK;
+}
+
+int ccg_ctx_sm_count(ccg_ctx* ctx, int* out) {
+  if (!ctx || !out) return fail(CCG_ERR_INVALID, "null argument");
+  *out = ctx->sm_count;
+  return CCG_OK;
+}
+
+int ccg_dev_alloc(ccg_ctx* ctx, size_t bytes, void** out) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (!out) return fail(CCG_ERR_INVALID, "null out");
+  CCG_CUDA(cudaMalloc(out, bytes ? bytes : 1));
+  return CCG_OK;
+}
+
+int ccg_dev_free(ccg_ctx* ctx, void* ptr) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (ptr) {
+    CCG_CUDA(cudaStreamSynchronize(ctx->stream));
+    CCG_CUDA(cudaFree(ptr));
+  }
+  return CCG_OK;
+}
+
+int ccg_host_alloc(size_t bytes, void** out) {
+  if (!out) return fail(CCG_ERR_INVALID, "null out");
+  CCG_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocDefault));
+  return CCG_OK;
+}
+
+int ccg_host_free(void* ptr) {
+  if (ptr) CCG_CUDA(cudaFreeHost(ptr));
+  return CCG_OK;
+}
+
+int ccg_memcpy_h2d(ccg_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (bytes) CCG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return CCG_OK;
+}
+
+int ccg_memcpy_d2h(ccg_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (bytes) CCG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  return CCG_OK;
+}
+
+// ------------------------------------------------------------------ rng
+static int philox_common(ccg_ctx* ctx, uint64_t k0, uint64_t k1, uint64_t skip, uint32_t bound,
+                         int64_t count, double* out_u, int64_t* out_i) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (count < 0) return fail(CCG_ERR_INVALID, "count must be non-negative");
+  if (count == 0) return CCG_OK;
+  if ((out_u == nullptr) == (out_i == nullptr)) return fail(CCG_ERR_INVALID, "null out");
+  if (out_i && bound < 1) return fail(CCG_ERR_INVALID, "bound must be at least 1");
+  void* d = nullptr;
+  rc = ctx->buf(0, (size_t)count * 8, &d);
+  if (rc) return rc;
+  ctx->launches++;
+  cudaError_t e = launch_philox_uniform(ctx->stream, k0, k1, skip, count, bound,
+                                        out_u ? (double*)d : nullptr, out_i ? (int64_t*)d : nullptr);
+  if (e != cudaSuccess) return cuda_fail(e, "philox kernel");
+  rc = download(ctx, out_u ? (void*)out_u : (void*)out_i, d, (size_t)count * 8);
+  if (rc) return rc;
+  return finish(ctx, cudaSuccess, "philox");
+}
+
+int ccg_philox_uniform(ccg_ctx* ctx, uint64_t k0, uint64_t k1, uint64_t skip, int64_t count,
+                       double* out) {
+  return philox_common(ctx, k0, k1, skip, 1, count, out, nullptr);
+}
+
+int ccg_philox_int_below(ccg_ctx* ctx, uint64_t k0, uint64_t k1, uint64_t skip, uint32_t bound,
+                         int64_t count, int64_t* out) {
+  return philox_common(ctx, k0, k1, skip, bound, count, nullptr, out);
+}
+
+// ------------------------------------------------------------------ fitness batches
+int ccg_score_text_batch(ccg_ctx* ctx, const uint8_t* texts, const int64_t* offsets,
+                         int64_t n_texts, const int64_t* table, int64_t* out) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  int64_t max_len = 0, tmax = 0;
+  if ((rc = check_ragged(texts, offsets, n_texts, "score_text", &max_len))) return rc;
+  if ((rc = check_table(table, &tmax))) return rc;
+  if (n_texts == 0) return CCG_OK;
+  if (!out) return fail(CCG_ERR_INVALID, "null out");
+  void *dt, *doff, *dtab, *dout;
+  if ((rc = upload(ctx, 0, texts, (size_t)offsets[n_texts], &dt))) return rc;
+  if ((rc = upload(ctx, 1, offsets, (size_t)(n_texts + 1) * 8, &doff))) return rc;
+  if ((rc = upload(ctx, 2, table, kAlpha * kAlpha * 8, &dtab))) return rc;
+  if ((rc = ctx->buf(3, (size_t)n_texts * 8, &dout))) return rc;
+  ctx->launches++;
+  cudaError_t e = launch_score_text(ctx->stream, (const uint8_t*)dt, (const int64_t*)doff, n_texts,
+                                    (const int64_t*)dtab, (int64_t*)dout);
+  if (e != cudaSuccess) return cuda_fail(e, "score_text kernel");
+  if ((rc = download(ctx, out, dout, (size_t)n_texts * 8))) return rc;
+  return finish(ctx, cudaSuccess, "score_text");
+}
+
+// Score (cipher, key) pairs grouped by ciphertext length; keys may be NULL for k=1 identity.
+// Score (cipher, key) pairs: texts the warp evaluator's plan covers are grouped by length
+// (one plan per length); longer ones take the any-length kernel.  keys may be NULL (k = 1
+// identity transposition, i.e. plain log_score_text).
+static int sct_score_grouped(ccg_ctx* ctx, const uint8_t* texts, const int64_t* offsets,
+                             int64_t n_texts, const int32_t* cipher_of, const uint8_t* keys,
+                             int32_t k, int64_t n_keys, const double* logs, double* out) {
+  std::map<int64_t, std::vector<int64_t>> by_len;
+  std::vector<int64_t> long_idx;
+  for (int64_t i = 0; i < n_keys; ++i) {
+    const int32_t c = cipher_of ? cipher_of[i] : (int32_t)i;
+    if (c < 0 || c >= n_texts) return fail(CCG_ERR_INVALID, "cipher_of[%lld] out of range", (long long)i);
+    const int64_t L = offsets[c + 1] - offsets[c];
+    if (L < k) return fail(CCG_ERR_INVALID, "ciphertext shorter than the key");
+    if (L < 2) {
+      out[i] = 0.0;  // ngrams.py:169-170: fewer than two letters score 0.0
+      continue;
+    }
+    if (L > kSctMaxLen) {
+      long_idx.push_back(i);
+      continue;
+    }
+    by_len[L].push_back(i);
+  }
+  if (by_len.empty() && long_idx.empty()) return CCG_OK;
+  int rc;
+  void *dt, *doffv, *dlogs;
+  if ((rc = upload(ctx, 0, texts, (size_t)offsets[n_texts], &dt))) return rc;
+  if ((rc = upload(ctx, 1, offsets, (size_t)(n_texts + 1) * 8, &doffv))) return rc;
+  if ((rc = upload(ctx, 2, logs, kAlpha * kAlpha * 8, &dlogs))) return rc;
+  const int64_t* doff = (const int64_t*)doffv;
+  std::vector<int32_t> cof;
+  std::vector<uint8_t> kbuf;
+  std::vector<double> res;
+  auto run = [&](const std::vector<int64_t>& idx, int64_t L, bool long_path) -> int {
+    const int64_t m = (int64_t)idx.size();
+    cof.resize(m);
+    kbuf.resize((size_t)m * k);
+    for (int64_t j = 0; j < m; ++j) {
+      const int64_t i = idx[j];
+      cof[j] = cipher_of ? cipher_of[i] : (int32_t)i;
+      for (int q = 0; q < k; ++q) kbuf[j * k + q] = keys ? keys[i * k + q] : (uint8_t)q;
+    }
+    void *dcof, *dkeys, *dout;
+    int r;
+    if ((r = upload(ctx, 3, cof.data(), (size_t)m * 4, &dcof))) return r;
+    if ((r = upload(ctx, 4, kbuf.data(), (size_t)m * k, &dkeys))) return r;
+    if ((r = ctx->buf(5, (size_t)m * 8, &dout))) return r;
+    cudaError_t e;
+    SumPlan plan;
+    if (!long_path) {
+      build_sum_plan(L - 1, &plan);
+      if (plan.n_leaves > kSctMaxLeaves) long_path = true;
+    }
+    ctx->launches++;
+    if (long_path)
+      e = launch_sct_score_long(ctx->stream, (const uint8_t*)dt, doff, (const int32_t*)dcof,
+                                (const uint8_t*)dkeys, k, m, (const double*)dlogs, (double*)dout);
+    else
+      e = launch_sct_score(ctx->stream, (const uint8_t*)dt, doff, (const int32_t*)dcof,
+                           (const uint8_t*)dkeys, k, m, (const double*)dlogs, nullptr,
+                           (double*)dout, (int32_t)L, plan);
+    if (e != cudaSuccess) return cuda_fail(e, "sct_score kernel");
+    res.resize(m);
+    if ((r = download(ctx, res.data(), dout, (size_t)m * 8))) return r;
+    CCG_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int64_t j = 0; j < m; ++j) out[idx[j]] = res[j];
+    return CCG_OK;
+  };
+  for (auto& kv : by_len)
+    if ((rc = run(kv.second, kv.first, false))) return rc;
+  if (!long_idx.empty() && (rc = run(long_idx, 0, true))) return rc;
+  return CCG_OK;
+}
+
+int ccg_log_score_text_batch(ccg_ctx* ctx, const uint8_t* texts, const int64_t* offsets,
+                             int64_t n_texts, const double* logs, double* out) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if ((rc = check_ragged(texts, offsets, n_texts, "log_score_text", nullptr))) return rc;
+  if ((rc = check_logs(logs))) return rc;
+  if (n_texts == 0) return CCG_OK;
+  if (!out) return fail(CCG_ERR_INVALID, "null out");
+  // identity transposition (k = 1) decrypts a text to itself
+  for (int64_t i = 0; i < n_texts; ++i)
+    if (offsets[i + 1] - offsets[i] < 1) out[i] = 0.0;
+  std::vector<int32_t> idx;
+  for (int64_t i = 0; i < n_texts; ++i)
+    if (offsets[i + 1] - offsets[i] >= 1) idx.push_back((int32_t)i);
+  std::vector<double> res(idx.size());
+  rc = sct_score_grouped(ctx, texts, offsets, n_texts, idx.data(), nullptr, 1,
+                         (int64_t)idx.size(), logs, res.data());
+  if (rc) return rc;
+  for (size_t j = 0; j < idx.size(); ++j) out[idx[j]] = res[j];
+  return CCG_OK;
+}
+
+int ccg_mas_delta_batch(ccg_ctx* ctx, const uint8_t* texts, const int64_t* offsets,
+                        int64_t n_texts, const int32_t* ab, const int64_t* table, int64_t* out) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  int64_t max_len = 0, tmax = 0;
+  if ((rc = check_ragged(texts, offsets, n_texts, "mas_delta", &max_len))) return rc;
+  if ((rc = check_table(table, &tmax))) return rc;
+  if (n_texts == 0) return CCG_OK;
+  if (!ab || !out) return fail(CCG_ERR_INVALID, "null argument");
+  if (max_len > kMasMaxLen)
+    return fail(CCG_ERR_UNSUPPORTED, "text of %lld letters exceeds the engine limit %lld",
+                (long long)max_len, (long long)kMasMaxLen);
+  for (int64_t i = 0; i < n_texts; ++i) {
+    const int a = ab[2 * i], b = ab[2 * i + 1];
+    if (a < 0 || a >= kAlpha || b < 0 || b >= kAlpha || a == b)
+      return fail(CCG_ERR_INVALID, "pair %lld: letters must be distinct in 0..25", (long long)i);
+  }
+  void *dt, *doff, *dab, *dtab, *dout;
+  if ((rc = upload(ctx, 0, texts, (size_t)offsets[n_texts], &dt))) return rc;
+  if ((rc = upload(ctx, 1, offsets, (size_t)(n_texts + 1) * 8, &doff))) return rc;
+  if ((rc = upload(ctx, 2, ab, (size_t)n_texts * 8, &dab))) return rc;
+  if ((rc = upload(ctx, 3, table, kAlpha * kAlpha * 8, &dtab))) return rc;
+  if ((rc = ctx->buf(4, (size_t)n_texts * 8, &dout))) return rc;
+  ctx->launches++;
+  cudaError_t e = launch_mas_delta(ctx->stream, (const uint8_t*)dt, (const int64_t*)doff, n_texts,
+                                   (const int32_t*)dab, (const int64_t*)dtab,
+                                   mas_needs_wide(max_len, tmax), (int64_t*)dout);
+  if (e != cudaSuccess) return cuda_fail(e, "mas_delta kernel");
+  if ((rc = download(ctx, out, dout, (size_t)n_texts * 8))) return rc;
+  return finish(ctx, cudaSuccess, "mas_delta");
+}
+
+int ccg_mas_delta_counts_batch(ccg_ctx* ctx, const int64_t* counts, int64_t n, const int32_t* ab,
+                               const int64_t* table, int64_t* out) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (n < 0) return fail(CCG_ERR_INVALID, "negative count");
+  if (n == 0) return CCG_OK;
+  if (!counts || !ab || !table || !out) return fail(CCG_ERR_INVALID, "null argument");
+  int64_t total_max = 0, smax = 0;
+  bool neg = false;
+  for (int i = 0; i < kAlpha * kAlpha; ++i) {
+    neg |= table[i] < 0;
+    smax = std::max(smax, table[i] < 0 ? -table[i] : table[i]);
+  }
+  for (int64_t j = 0; j < n; ++j) {
+    int64_t tot = 0;
+    for (int i = 0; i < kAlpha * kAlpha; ++i) {
+      const int64_t c = counts[j * kAlpha * kAlpha + i];
+      if (c < 0 || c > 65535)
+        return fail(CCG_ERR_UNSUPPORTED, "count matrix %lld: entries must lie in 0..65535", (long long)j);
+      tot += c;
+    }
+    total_max = std::max(total_max, tot);
+    const int a = ab[2 * j], b = ab[2 * j + 1];
+    if (a < 0 || a >= kAlpha || b < 0 || b >= kAlpha)
+      return fail(CCG_ERR_INVALID, "pair %lld: letters must lie in 0..25", (long long)j);
+  }
+  const bool wide = neg || mas_needs_wide(total_max + 1, smax);
+  void *dc, *dab, *dtab, *dout;
+  if ((rc = upload(ctx, 0, counts, (size_t)n * kAlpha * kAlpha * 8, &dc))) return rc;
+  if ((rc = upload(ctx, 1, ab, (size_t)n * 8, &dab))) return rc;
+  if ((rc = upload(ctx, 2, table, kAlpha * kAlpha * 8, &dtab))) return rc;
+  if ((rc = ctx->buf(3, (size_t)n * 8, &dout))) return rc;
+  ctx->launches++;
+  cudaError_t e = launch_mas_delta_counts(ctx->stream, (const int64_t*)dc, n, (const int32_t*)dab,
+                                          (const int64_t*)dtab, wide, (int64_t*)dout);
+  if (e != cudaSuccess) return cuda_fail(e, "mas_delta_counts kernel");
+  if ((rc = download(ctx, out, dout, (size_t)n * 8))) return rc;
+  return finish(ctx, cudaSuccess, "mas_delta_counts");
+}
+
+// ------------------------------------------------------------------ MAS climb
+static int mas_launch(ccg_ctx* ctx, const ccg_mas_climb_args* a, int64_t max_len, int64_t tmax) {
+  if (max_len > kMasMaxLen)
+    return fail(CCG_ERR_UNSUPPORTED, "ciphertext of %lld letters exceeds the engine limit %lld",
+                (long long)max_len, (long long)kMasMaxLen);
+  MasLaunch p;
+  p.ciphers = a->ciphers;
+  p.offsets = a->offsets;
+  p.cipher_of = a->cipher_of;
+  p.keys = a->keys;
+  p.skips = a->skips;
+  p.n_workers = a->n_workers;
+  p.climbings = a->climbings;
+  p.table = a->table;
+  p.scores = a->scores;
+  p.maps = a->maps;
+  p.draws_used = a->draws_used;
+  p.last_accept = a->last_accept;
+  p.tries_done = a->tries_done;
+  p.flags = a->flags;
+  ctx->launches++;
+  cudaError_t e = launch_mas_climb(ctx->stream, p, mas_needs_wide(max_len, tmax), ctx->sm_count);
+  if (e != cudaSuccess) return cuda_fail(e, "mas_climb kernel");
+  if (a->group_size > 0 && a->group_best) {
+    ctx->launches++;
+    e = launch_group_best_i64(ctx->stream, a->scores, a->n_workers / a->group_size, a->group_size,
+                              a->group_best);
+    if (e != cudaSuccess) return cuda_fail(e, "group_best kernel");
+  }
+  return CCG_OK;
+}
+
+static int check_climb_common(int64_t n_workers, int64_t climbings, int32_t group_size,
+                              const void* scores, const void* keys, const void* cipher_of) {
+  if (n_workers < 0) return fail(CCG_ERR_INVALID, "n_workers must be non-negative");
+  if (climbings < 0) return fail(CCG_ERR_INVALID, "climbings must be non-negative");
+  if (n_workers > 0 && (!scores || !keys || !cipher_of))
+    return fail(CCG_ERR_INVALID, "scores, keys and cipher_of are required");
+  if (group_size < 0) return fail(CCG_ERR_INVALID, "group_size must be non-negative");
+  if (group_size > 0 && n_workers % group_size)
+    return fail(CCG_ERR_INVALID, "n_workers must be a multiple of group_size");
+  return CCG_OK;
+}
+
+int ccg_mas_climb_dev(ccg_ctx* ctx, const ccg_mas_climb_args* a) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (!a) return fail(CCG_ERR_INVALID, "null args");
+  if ((rc = check_climb_common(a->n_workers, a->climbings, a->group_size, a->scores, a->keys,
+                               a->cipher_of)))
+    return rc;
+  if (a->table_max < 0) return fail(CCG_ERR_INVALID, "table_max must be set");
+  return mas_launch(ctx, a, a->max_len, a->table_max);
+}
+
+int ccg_mas_climb(ccg_ctx* ctx, const ccg_mas_climb_args* a) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (!a) return fail(CCG_ERR_INVALID, "null args");
+  if ((rc = check_climb_common(a->n_workers, a->climbings, a->group_size, a->scores, a->keys,
+                               a->cipher_of)))
+    return rc;
+  int64_t max_len = 0, tmax = 0;
+  if ((rc = check_ragged(a->ciphers, a->offsets, a->n_ciphers, "mas_climb", &max_len))) return rc;
+  if ((rc = check_table(a->table, &tmax))) return rc;
+  const int64_t nw = a->n_workers;
+  if (nw == 0) return CCG_OK;
+  for (int64_t i = 0; i < nw; ++i)
+    if (a->cipher_of[i] < 0 || a->cipher_of[i] >= a->n_ciphers)
+      return fail(CCG_ERR_INVALID, "cipher_of[%lld] out of range", (long long)i);
+  ccg_mas_climb_args d = *a;
+  void* p;
+  if ((rc = upload(ctx, 0, a->ciphers, (size_t)a->offsets[a->n_ciphers], &p))) return rc;
+  d.ciphers = (const uint8_t*)p;
+  if ((rc = upload(ctx, 1, a->offsets, (size_t)(a->n_ciphers + 1) * 8, &p))) return rc;
+  d.offsets = (const int64_t*)p;
+  if ((rc = upload(ctx, 2, a->cipher_of, (size_t)nw * 4, &p))) return rc;
+  d.cipher_of = (const int32_t*)p;
+  if ((rc = upload(ctx, 3, a->keys, (size_t)nw * 16, &p))) return rc;
+  d.keys = (const uint64_t*)p;
+  if (a->skips) {
+    if ((rc = upload(ctx, 4, a->skips, (size_t)nw * 8, &p))) return rc;
+    d.skips = (const uint64_t*)p;
+  }
+  if ((rc = upload(ctx, 5, a->table, kAlpha * kAlpha * 8, &p))) return rc;
+  d.table = (const int64_t*)p;
+  if ((rc = ctx->buf(6, (size_t)nw * 8, &p))) return rc;
+  d.scores = (int64_t*)p;
+  if (a->maps) { if ((rc = ctx->buf(7, (size_t)nw * kAlpha, &p))) return rc; d.maps = (uint8_t*)p; }
+  if (a->draws_used) { if ((rc = ctx->buf(8, (size_t)nw * 8, &p))) return rc; d.draws_used = (uint64_t*)p; }
+  if (a->last_accept) { if ((rc = ctx->buf(9, (size_t)nw * 8, &p))) return rc; d.last_accept = (int64_t*)p; }
+  if (a->tries_done) { if ((rc = ctx->buf(10, (size_t)nw * 8, &p))) return rc; d.tries_done = (int64_t*)p; }
+  const int64_t ng = a->group_size > 0 ? nw / a->group_size : 0;
+  if (a->group_best && ng) { if ((rc = ctx->buf(11, (size_t)ng * 8, &p))) return rc; d.group_best = (int64_t*)p; }
+  else d.group_best = nullptr;
+  if ((rc = mas_launch(ctx, &d, max_len, tmax))) return rc;
+  if ((rc = download(ctx, a->scores, d.scores, (size_t)nw * 8))) return rc;
+  if (a->maps && (rc = download(ctx, a->maps, d.maps, (size_t)nw * kAlpha))) return rc;
+  if (a->draws_used && (rc = download(ctx, a->draws_used, d.draws_used, (size_t)nw * 8))) return rc;
+  if (a->last_accept && (rc = download(ctx, a->last_accept, d.last_accept, (size_t)nw * 8))) return rc;
+  if (a->tries_done && (rc = download(ctx, a->tries_done, d.tries_done, (size_t)nw * 8))) return rc;
+  if (d.group_best && (rc = download(ctx, a->group_best, d.group_best, (size_t)ng * 8))) return rc;
+  return finish(ctx, cudaSuccess, "mas_climb");
+}
+
+// ------------------------------------------------------------------ SCT
+int ccg_sct_score_batch(ccg_ctx* ctx, const uint8_t* ciphers, const int64_t* offsets,
+                        int64_t n_ciphers, const int32_t* cipher_of, const uint8_t* keys,
+                        int32_t key_length, int64_t n_keys, const double* logs, double* out) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if ((rc = check_ragged(ciphers, offsets, n_ciphers, "sct_score", nullptr))) return rc;
+  if ((rc = check_logs(logs))) return rc;
+  if (key_length < 1) return fail(CCG_ERR_INVALID, "key_length must be at least 1");
+  if (key_length > kSctMaxKey)
+    return fail(CCG_ERR_UNSUPPORTED, "key length %d exceeds the engine limit %d", key_length, kSctMaxKey);
+  if (n_keys <= 0) return CCG_OK;
+  if (!keys || !cipher_of || !out) return fail(CCG_ERR_INVALID, "null argument");
+  for (int64_t i = 0; i < n_keys; ++i) {
+    uint64_t seen = 0;
+    for (int q = 0; q < key_length; ++q) {
+      const int v = keys[i * key_length + q];
+      if (v >= key_length || (seen >> v) & 1)
+        return fail(CCG_ERR_INVALID, "transposition key must be a permutation of 0..k-1");
+      seen |= 1ULL << v;
+    }
+  }
+  return sct_score_grouped(ctx, ciphers, offsets, n_ciphers, cipher_of, keys, key_length, n_keys,
+                           logs, out);
+}
+
+static int sct_check(const ccg_sct_climb_args* a) {
+  int rc;
+  if ((rc = check_climb_common(a->n_workers, a->climbings, a->group_size, a->scores, a->keys,
+                               a->cipher_of)))
+    return rc;
+  if (a->key_length < 2) return fail(CCG_ERR_INVALID, "key_length must be at least 2");
+  if (a->key_length > kSctMaxKey)
+    return fail(CCG_ERR_UNSUPPORTED, "key length %d exceeds the engine limit %d", a->key_length, kSctMaxKey);
+  if (!(0 <= a->p1 && a->p1 <= a->p2 && a->p2 <= 100))
+    return fail(CCG_ERR_INVALID, "thresholds must satisfy 0 <= p1 <= p2 <= 100");
+  if (a->op1_hop < 1 || a->op2_hop < 1) return fail(CCG_ERR_INVALID, "op hops must be at least 1");
+  if (a->n_workers > 0 && !a->keys_out) return fail(CCG_ERR_INVALID, "keys_out is required");
+  return check_logs(a->logs);
+}
+
+static int sct_launch(ccg_ctx* ctx, const ccg_sct_climb_args* a, int64_t n) {
+  if (n < a->key_length) return fail(CCG_ERR_INVALID, "ciphertext shorter than the key");
+  if (n > kSctMaxLen)
+    return fail(CCG_ERR_UNSUPPORTED, "ciphertext of %lld letters exceeds the engine limit %lld",
+                (long long)n, (long long)kSctMaxLen);
+  SumPlan plan;
+  build_sum_plan(n - 1, &plan);
+  if (plan.n_leaves > kSctMaxLeaves)
+    return fail(CCG_ERR_UNSUPPORTED, "text length %lld needs %d pairwise leaves (limit %d)",
+                (long long)n, plan.n_leaves, kSctMaxLeaves);
+  SctLaunch p;
+  p.ciphers = a->ciphers;
+  p.offsets = a->offsets;
+  p.cipher_of = a->cipher_of;
+  p.keys = a->keys;
+  p.skips = a->skips;
+  p.n_workers = a->n_workers;
+  p.n = (int32_t)n;
+  p.k = a->key_length;
+  p.climbings = a->climbings;
+  p.p1 = a->p1;
+  p.p2 = a->p2;
+  p.op1_hop = a->op1_hop;
+  p.op2_hop = a->op2_hop;
+  p.logs = a->logs;
+  p.scores = a->scores;
+  p.keys_out = a->keys_out;
+  p.draws_used = a->draws_used;
+  p.last_accept = a->last_accept;
+  p.tries_done = a->tries_done;
+  p.flags = a->flags;
+  ctx->launches++;
+  cudaError_t e = launch_sct_climb(ctx->stream, p, plan, ctx->sm_count);
+  if (e != cudaSuccess) return cuda_fail(e, "sct_climb kernel");
+  if (a->group_size > 0 && a->group_best) {
+    ctx->launches++;
+    e = launch_group_best_f64(ctx->stream, a->scores, a->n_workers / a->group_size, a->group_size,
+                              a->group_best);
+    if (e != cudaSuccess) return cuda_fail(e, "group_best kernel");
+  }
+  return CCG_OK;
+}
+
+int ccg_sct_climb_dev(ccg_ctx* ctx, const ccg_sct_climb_args* a) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (!a) return fail(CCG_ERR_INVALID, "null args");
+  if ((rc = sct_check(a))) return rc;
+  if (a->n_workers == 0) return CCG_OK;
+  return sct_launch(ctx, a, a->text_len);
+}
+
+int ccg_sct_climb(ccg_ctx* ctx, const ccg_sct_climb_args* a) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (!a) return fail(CCG_ERR_INVALID, "null args");
+  if ((rc = sct_check(a))) return rc;
+  if ((rc = check_ragged(a->ciphers, a->offsets, a->n_ciphers, "sct_climb", nullptr))) return rc;
+  const int64_t nw = a->n_workers;
+  if (nw == 0) return CCG_OK;
+  int64_t n = -1;
+  for (int64_t i = 0; i < nw; ++i) {
+    const int32_t c = a->cipher_of[i];
+    if (c < 0 || c >= a->n_ciphers) return fail(CCG_ERR_INVALID, "cipher_of[%lld] out of range", (long long)i);
+    const int64_t L = a->offsets[c + 1] - a->offsets[c];
+    if (n < 0) n = L;
+    if (L != n)
+      return fail(CCG_ERR_INVALID, "all ciphertexts of one sct_climb call must have the same length");
+  }
+  ccg_sct_climb_args d = *a;
+  void* p;
+  const int k = a->key_length;
+  if ((rc = upload(ctx, 0, a->ciphers, (size_t)a->offsets[a->n_ciphers], &p))) return rc;
+  d.ciphers = (const uint8_t*)p;
+  if ((rc = upload(ctx, 1, a->offsets, (size_t)(a->n_ciphers + 1) * 8, &p))) return rc;
+  d.offsets = (const int64_t*)p;
+  if ((rc = upload(ctx, 2, a->cipher_of, (size_t)nw * 4, &p))) return rc;
+  d.cipher_of = (const int32_t*)p;
+  if ((rc = upload(ctx, 3, a->keys, (size_t)nw * 16, &p))) return rc;
+  d.keys = (const uint64_t*)p;
+  if (a->skips) {
+    if ((rc = upload(ctx, 4, a->skips, (size_t)nw * 8, &p))) return rc;
+    d.skips = (const uint64_t*)p;
+  }
+  if ((rc = upload(ctx, 5, a->logs, kAlpha * kAlpha * 8, &p))) return rc;
+  d.logs = (const double*)p;
+  if ((rc = ctx->buf(6, (size_t)nw * 8, &p))) return rc;
+  d.scores = (double*)p;
+  if ((rc = ctx->buf(7, (size_t)nw * k, &p))) return rc;
+  d.keys_out = (uint8_t*)p;
+  if (a->draws_used) { if ((rc = ctx->buf(8, (size_t)nw * 8, &p))) return rc; d.draws_used = (uint64_t*)p; }
+  if (a->last_accept) { if ((rc = ctx->buf(9, (size_t)nw * 8, &p))) return rc; d.last_accept = (int64_t*)p; }
+  if (a->tries_done) { if ((rc = ctx->buf(10, (size_t)nw * 8, &p))) return rc; d.tries_done = (int64_t*)p; }
+  const int64_t ng = a->group_size > 0 ? nw / a->group_size : 0;
+  if (a->group_best && ng) { if ((rc = ctx->buf(11, (size_t)ng * 8, &p))) return rc; d.group_best = (int64_t*)p; }
+  else d.group_best = nullptr;
+  if ((rc = sct_launch(ctx, &d, n))) return rc;
+  if ((rc = download(ctx, a->scores, d.scores, (size_t)nw * 8))) return rc;
+  if ((rc = download(ctx, a->keys_out, d.keys_out, (size_t)nw * k))) return rc;
+  if (a->draws_used && (rc = download(ctx, a->draws_used, d.draws_used, (size_t)nw * 8))) return rc;
+  if (a->last_accept && (rc = download(ctx, a->last_accept, d.last_accept, (size_t)nw * 8))) return rc;
+  if (a->tries_done && (rc = download(ctx, a->tries_done, d.tries_done, (size_t)nw * 8))) return rc;
+  if (d.group_best && (rc = download(ctx, a->group_best, d.group_best, (size_t)ng * 8))) return rc;
+  return finish(ctx, cudaSuccess, "sct_climb");
+}
+
+}  // extern "C"

@@ -1,0 +1,102 @@
+// ccg_internal.h -- shared between the C-ABI layer (ccg_api.cu) and the kernel files.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/cipherclimb_b200.h"
+
+namespace ccg {
+
+constexpr int kAlpha = 26;
+constexpr int kRow = 32;  // padded row stride of the 26x26 smem tables (one row = 32 banks)
+
+// Largest ciphertext the MAS climb handles: bigram counts are packed as 16-bit halves.
+constexpr int64_t kMasMaxLen = 65536;
+// SCT limits: key length (lane-distributed key, two positions per lane) and the numpy
+// pairwise-sum leaf budget (kSctMaxLeaves * <=128 terms).
+constexpr int kSctMaxKey = 64;
+constexpr int kSctMaxLeaves = 32;
+constexpr int64_t kSctMaxLen = 4096;
+
+struct MasLaunch {
+  const uint8_t* ciphers;
+  const int64_t* offsets;
+  const int32_t* cipher_of;
+  const uint64_t* keys;
+  const uint64_t* skips;
+  int64_t n_workers;
+  int64_t climbings;
+  const int64_t* table;
+  int64_t* scores;
+  uint8_t* maps;
+  uint64_t* draws_used;
+  int64_t* last_accept;
+  int64_t* tries_done;
+  uint32_t flags;
+};
+
+// numpy pairwise-sum plan for the (n-1) bigram terms of an n-letter text
+// (numpy/_core/src/umath/loops_utils.h.src pairwise_sum): leaves in order, and the
+// post-order list of leaf merges (dst += src) that reproduces the recursion.
+struct SumPlan {
+  int32_t n_terms;
+  int32_t n_leaves;
+  int32_t seq;                      // 1: n_terms < 8, a single sequential leaf
+  int32_t leaf_start[kSctMaxLeaves];
+  int32_t leaf_len[kSctMaxLeaves];
+  int32_t n_merges;
+  int8_t merge_dst[kSctMaxLeaves];
+  int8_t merge_src[kSctMaxLeaves];
+};
+
+struct SctLaunch {
+  const uint8_t* ciphers;
+  const int64_t* offsets;
+  const int32_t* cipher_of;
+  const uint64_t* keys;
+  const uint64_t* skips;
+  int64_t n_workers;
+  int32_t n;  // common text length
+  int32_t k;
+  int64_t climbings;
+  int32_t p1, p2, op1_hop, op2_hop;
+  const double* logs;
+  double* scores;
+  uint8_t* keys_out;
+  uint64_t* draws_used;
+  int64_t* last_accept;
+  int64_t* tries_done;
+  uint32_t flags;
+};
+
+void build_sum_plan(int64_t n_terms, SumPlan* plan);
+
+// Launchers (return cudaError_t of the launch).  `grid` <= 0 lets the launcher size it.
+cudaError_t launch_philox_uniform(cudaStream_t s, uint64_t k0, uint64_t k1, uint64_t skip,
+                                  int64_t count, uint32_t bound, double* out_u, int64_t* out_i);
+cudaError_t launch_score_text(cudaStream_t s, const uint8_t* texts, const int64_t* offsets,
+                              int64_t n, const int64_t* table, int64_t* out);
+cudaError_t launch_log_score_text(cudaStream_t s, const uint8_t* texts, const int64_t* offsets,
+                                  int64_t n, const double* logs, double* out);
+cudaError_t launch_mas_delta(cudaStream_t s, const uint8_t* texts, const int64_t* offsets,
+                             int64_t n, const int32_t* ab, const int64_t* table, bool wide,
+                             int64_t* out);
+cudaError_t launch_mas_delta_counts(cudaStream_t s, const int64_t* counts, int64_t n,
+                                    const int32_t* ab, const int64_t* table, bool wide,
+                                    int64_t* out);
+cudaError_t launch_mas_climb(cudaStream_t s, const MasLaunch& p, bool wide, int sm_count);
+cudaError_t launch_group_best_i64(cudaStream_t s, const int64_t* scores, int64_t n_groups,
+                                  int32_t group_size, int64_t* out);
+cudaError_t launch_group_best_f64(cudaStream_t s, const double* scores, int64_t n_groups,
+                                  int32_t group_size, int64_t* out);
+cudaError_t launch_sct_score(cudaStream_t s, const uint8_t* ciphers, const int64_t* offsets,
+                             const int32_t* cipher_of, const uint8_t* keys, int32_t k,
+                             int64_t n_keys, const double* logs, int64_t* n_of, double* out,
+                             int32_t n_common, const SumPlan& plan);
+cudaError_t launch_sct_score_long(cudaStream_t s, const uint8_t* ciphers, const int64_t* offsets,
+                                  const int32_t* cipher_of, const uint8_t* keys, int32_t k,
+                                  int64_t n_keys, const double* logs, double* out);
+cudaError_t launch_sct_climb(cudaStream_t s, const SctLaunch& p, const SumPlan& plan,
+                             int sm_count);
+
+}  // namespace ccg

@@ -1,0 +1,562 @@
+// ccg_sct.cu -- single-columnar-transposition (SCT) kernels for sm_100a.
+//
+// Reference path: sct.py:148-170 sct_worker.  Start from permutation(k) (rng.py:91-97),
+// then per try draw an operator (sct.py:69-79: element swaps, block swaps, block shift,
+// sct.py:82-135), decrypt the whole ciphertext with the candidate key
+// (ciphers.py:71-86 transposition_gather_map, irregular grid), score it as the float64
+// sum of log2 bigram probabilities in NUMPY'S PAIRWISE ORDER (ngrams.py:172 / sct.py:160:
+// `logs[idx].sum()`), and accept iff the candidate score is strictly greater.
+//
+// B200 design (warp per worker):
+//  * The key is lane-distributed (lane l holds key positions l and l+32).  Every
+//    operator is a gather cand[l] = key[src(l)] with src computed from warp-uniform draw
+//    values, done with shuffles -- no key arrays in memory.
+//  * Decryption is never materialised.  Plaintext position t sits in grid column c = t%k,
+//    row r = t/k, and plain[t] = cipher[colstart[c] + r] where colstart[key[j]] is the
+//    exclusive prefix sum of the segment lengths in key order (one warp scan per
+//    candidate; column c has ceil(n/k) letters iff c < n%k, ciphers.py:79-81).
+//  * numpy's pairwise sum (n <= 128: 8 strided accumulators, tree
+//    ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the n%8 tail in order; n > 128: split at
+//    n/2 rounded down to a multiple of 8 and recurse) is laid onto the warp: each leaf's 8
+//    accumulators are 8 lanes (4 leaves per 32-lane "slot", up to 8 slots), the tree is
+//    a 3-step xor butterfly (fp add is commutative, so every lane of the group holds the
+//    identical rounded value), the tail is added in order, and the host-computed
+//    post-order merge list (SumPlan) replays the recursion with shuffles.  The result is
+//    bit-identical to numpy's float64 sum, so accept decisions match the reference.
+//  * Tables: the 676 float64 log2 probabilities and each warp's ciphertext are staged in
+//    shared memory; colstart is a per-warp 64-entry u16 array (conflict-free).
+#include "ccg_internal.h"
+#include "ccg_rng.cuh"
+
+namespace ccg {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kSctWarps = 8;
+
+struct Draws {
+  DrawWindow win;
+  uint64_t pos;
+  __device__ __forceinline__ uint64_t raw(int lane) {
+    if (pos >= win.base + 128) win.refill(pos, lane);
+    const uint32_t o = (uint32_t)(pos - win.base);
+    const uint32_t r = o >> 5;
+    const uint64_t w = r == 0 ? win.w[0] : r == 1 ? win.w[1] : r == 2 ? win.w[2] : win.w[3];
+    ++pos;
+    return shfl64(w, (int)(o & 31));
+  }
+  // rng.py:77-79
+  __device__ __forceinline__ int below(uint32_t bound, int lane) {
+    return (int)int_below(raw(lane), bound);
+  }
+  // rng.py:81-89
+  __device__ __forceinline__ void pair(uint32_t bound, int lane, int& a, int& b) {
+    a = below(bound, lane);
+    b = below(bound, lane);
+    while (b == a) b = below(bound, lane);
+  }
+};
+
+// Lane-distributed key of length k <= 64: v0 = key[lane], v1 = key[lane + 32].
+struct Key {
+  int v0, v1;
+  __device__ __forceinline__ int at(int i) const {  // i warp-uniform
+    return i < 32 ? __shfl_sync(kFull, v0, i) : __shfl_sync(kFull, v1, i - 32);
+  }
+  // out[l] = this[src(l)] for the two positions owned by the lane
+  __device__ __forceinline__ Key gather(int s0, int s1, bool wide) const {
+    Key o;
+    const int a0 = __shfl_sync(kFull, v0, s0 & 31);
+    if (!wide) {
+      o.v0 = a0;
+      o.v1 = v1;
+      return o;
+    }
+    const int b0 = __shfl_sync(kFull, v1, s0 & 31);
+    const int a1 = __shfl_sync(kFull, v0, s1 & 31);
+    const int b1 = __shfl_sync(kFull, v1, s1 & 31);
+    o.v0 = s0 < 32 ? a0 : b0;
+    o.v1 = s1 < 32 ? a1 : b1;
+    return o;
+  }
+  __device__ __forceinline__ void swap_pos(int i, int j, int lane) {
+    const int vi = at(i), vj = at(j);
+    if (lane == i) v0 = vj;
+    if (lane == j) v0 = vi;
+    if (lane + 32 == i) v1 = vj;
+    if (lane + 32 == j) v1 = vi;
+  }
+};
+
+// Per-lane static part of the sum plan for one slot.
+struct SlotPlan {
+  int leaf;       // leaf id handled by this lane's 8-lane group in this slot (-1: none)
+  int count;      // strided terms per accumulator (len/8, 0 for a sequential leaf)
+  int tail;       // terms added in order after the tree
+  int c0, r0;     // grid position of this lane's first strided term
+  int ct, rt;     // grid position of the first tail term
+};
+
+__device__ __forceinline__ void grid_pos(int t, int k, int& c, int& r) {
+  r = t / k;
+  c = t - r * k;
+}
+
+template <int SLOTS>
+struct Evaluator {
+  SlotPlan sp[SLOTS];
+  int k, n, base, rem, q8, r8;
+  const SumPlan* plan;
+
+  __device__ void init(const SumPlan& P, int k_, int n_, int lane) {
+    plan = &P;
+    k = k_;
+    n = n_;
+    base = n / k;
+    rem = n - base * k;
+    q8 = 8 / k;
+    r8 = 8 - q8 * k;
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+      const int leaf = 4 * s + (lane >> 3);
+      SlotPlan& q = sp[s];
+      if (leaf < P.n_leaves) {
+        const int len = P.leaf_len[leaf], start = P.leaf_start[leaf];
+        q.leaf = leaf;
+        q.count = len >= 8 ? len / 8 : 0;
+        q.tail = len >= 8 ? len % 8 : len;
+        grid_pos(start + (lane & 7), k, q.c0, q.r0);
+        grid_pos(start + 8 * q.count, k, q.ct, q.rt);
+      } else {
+        q.leaf = -1;
+        q.count = 0;
+        q.tail = 0;
+        q.c0 = q.r0 = q.ct = q.rt = 0;
+      }
+    }
+  }
+
+  __device__ __forceinline__ double term(const uint8_t* txt, const uint16_t* colstart,
+                                         const double* logs, int c, int r) const {
+    int c1 = c + 1, r1 = r;
+    if (c1 == k) { c1 = 0; ++r1; }
+    const int ch0 = txt[colstart[c] + r];
+    const int ch1 = txt[colstart[c1] + r1];
+    return logs[ch0 * kAlpha + ch1];
+  }
+
+  // Score of decrypting txt with the lane-distributed key.
+  __device__ double score(const Key& key, const uint8_t* txt, uint16_t* colstart,
+                          const double* logs, int lane) const {
+    // colstart[key[j]] = sum of segment lengths of key positions < j (ciphers.py:79-86)
+    const bool wide = k > 32;
+    const int len0 = lane < k ? base + (key.v0 < rem ? 1 : 0) : 0;
+    const int len1 = lane + 32 < k ? base + (key.v1 < rem ? 1 : 0) : 0;
+    int inc0 = len0, inc1 = len1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u0 = __shfl_up_sync(kFull, inc0, o);
+      if (lane >= o) inc0 += u0;
+      if (wide) {
+        const int u1 = __shfl_up_sync(kFull, inc1, o);
+        if (lane >= o) inc1 += u1;
+      }
+    }
+    __syncwarp();
+    if (lane < k) colstart[key.v0] = (uint16_t)(inc0 - len0);
+    if (wide) {
+      const int tot0 = __shfl_sync(kFull, inc0, 31);
+      if (lane + 32 < k) colstart[key.v1] = (uint16_t)(tot0 + inc1 - len1);
+    }
+    __syncwarp();
+
+    double res[SLOTS];
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+      const SlotPlan& q = sp[s];
+      double acc = 0.0;
+      int c = q.c0, r = q.r0;
+      for (int i = 0; i < q.count; ++i) {
+        const double v = term(txt, colstart, logs, c, r);
+        acc = i == 0 ? v : acc + v;
+        c += r8;
+        r += q8;
+        if (c >= k) { c -= k; ++r; }
+      }
+      // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) as an xor butterfly over the 8-lane group
+      acc += __shfl_xor_sync(kFull, acc, 1);
+      acc += __shfl_xor_sync(kFull, acc, 2);
+      acc += __shfl_xor_sync(kFull, acc, 4);
+      c = q.ct;
+      r = q.rt;
+      for (int u = 0; u < q.tail; ++u) {
+        acc += term(txt, colstart, logs, c, r);
+        if (++c == k) { c = 0; ++r; }
+      }
+      res[s] = acc;
+    }
+    // replay the recursion's merges (post-order): leaf[dst] = leaf[dst] + leaf[src]
+    const SumPlan& P = *plan;
+    for (int m = 0; m < P.n_merges; ++m) {
+      const int d = P.merge_dst[m], sidx = P.merge_src[m];
+      double sv = 0.0;
+#pragma unroll
+      for (int s = 0; s < SLOTS; ++s)
+        if (s == (sidx >> 2)) sv = res[s];
+      sv = __shfl_sync(kFull, sv, 8 * (sidx & 3));
+#pragma unroll
+      for (int s = 0; s < SLOTS; ++s)
+        if (s == (d >> 2) && (lane >> 3) == (d & 3)) res[s] = res[s] + sv;
+    }
+    return __shfl_sync(kFull, res[0], 0);
+  }
+};
+
+__device__ __forceinline__ void stage_text(uint8_t* dst, const uint8_t* __restrict__ src, int n,
+                                           int lane) {
+  for (int i = lane; i < n; i += 32) dst[i] = src[i];
+  __syncwarp();
+}
+
+__device__ __forceinline__ void stage_logs(double* logs, const double* __restrict__ g) {
+  for (int i = threadIdx.x; i < kAlpha * kAlpha; i += blockDim.x) logs[i] = g[i];
+  __syncthreads();
+}
+
+__host__ __device__ __forceinline__ size_t text_stride(int n) { return ((size_t)n + 15) & ~(size_t)15; }
+
+// sct.py:82-89 apply_element_swaps
+__device__ __forceinline__ void op_element_swaps(Key& c, Draws& d, int k, int max_hops, int lane) {
+  const int hops = 1 + d.below((uint32_t)max_hops, lane);
+  for (int h = 0; h < hops; ++h) {
+    int i, j;
+    d.pair((uint32_t)k, lane, i, j);
+    c.swap_pos(i, j, lane);
+  }
+}
+
+// sct.py:92-112 apply_block_swaps
+__device__ __forceinline__ void op_block_swaps(Key& c, Draws& d, int k, int max_hops, int lane) {
+  const int hops = 1 + d.below((uint32_t)max_hops, lane);
+  for (int h = 0; h < hops; ++h) {
+    const int len = 1 + d.below((uint32_t)(k / 2), lane);
+    int p, q;
+    d.pair((uint32_t)(k - len + 1), lane, p, q);
+    while (abs(p - q) < len) d.pair((uint32_t)(k - len + 1), lane, p, q);
+    if (p > q) { const int t = p; p = q; q = t; }
+    auto src = [&](int l) {
+      if (l >= p && l < p + len) return l - p + q;
+      if (l >= q && l < q + len) return l - q + p;
+      return l;
+    };
+    c = c.gather(src(lane), src(lane + 32), k > 32);
+  }
+}
+
+// sct.py:115-135 apply_block_shift
+__device__ __forceinline__ void op_block_shift(Key& c, Draws& d, int k, int lane) {
+  const int len = 1 + d.below((uint32_t)(k - 1), lane);
+  const int starts = k - len + 1;
+  const int p = d.below((uint32_t)starts, lane);
+  int dest = d.below((uint32_t)starts, lane);
+  while (dest == p) dest = d.below((uint32_t)starts, lane);
+  const int lo = min(p, dest), hi = max(p, dest) + len, w = hi - lo;
+  const int sh = dest > p ? len : w - len;  // window[len:]+window[:len]  /  window[-len:]+window[:-len]
+  auto src = [&](int l) {
+    if (l >= lo && l < hi) {
+      int i = l - lo + sh;
+      if (i >= w) i -= w;
+      return lo + i;
+    }
+    return l;
+  };
+  c = c.gather(src(lane), src(lane + 32), k > 32);
+}
+
+template <int SLOTS>
+__global__ void __launch_bounds__(kSctWarps * 32)
+    sct_climb_kernel(const SctLaunch p, const __grid_constant__ SumPlan plan) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* logs = reinterpret_cast<double*>(smem);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint16_t* colstart = reinterpret_cast<uint16_t*>(smem + kAlpha * kAlpha * sizeof(double)) +
+                       warp * kSctMaxKey;
+  uint8_t* txt = smem + kAlpha * kAlpha * sizeof(double) + kSctWarps * kSctMaxKey * 2 +
+                 warp * text_stride(p.n);
+  stage_logs(logs, p.logs);
+
+  Evaluator<SLOTS> ev;
+  ev.init(plan, p.k, p.n, lane);
+  const int k = p.k;
+  const int64_t stride = (int64_t)gridDim.x * kSctWarps;
+
+  for (int64_t w = (int64_t)blockIdx.x * kSctWarps + warp; w < p.n_workers; w += stride) {
+    const int32_t cid = p.cipher_of[w];
+    stage_text(txt, p.ciphers + p.offsets[cid], p.n, lane);
+    Draws d;
+    d.win.k0 = p.keys[2 * w];
+    d.win.k1 = p.keys[2 * w + 1];
+    d.pos = p.skips ? p.skips[w] : 0;
+    d.win.refill(d.pos, lane);
+
+    // rng.py:91-97 permutation(k): Fisher-Yates from the top
+    Key key;
+    key.v0 = lane;
+    key.v1 = lane + 32;
+    for (int i = k - 1; i > 0; --i) {
+      const int j = d.below((uint32_t)(i + 1), lane);
+      key.swap_pos(i, j, lane);
+    }
+    double score = ev.score(key, txt, colstart, logs, lane);
+    int64_t last = -1, t = 0;
+    for (; t < p.climbings; ++t) {
+      const int u = d.below(100u, lane);
+      Key cand = key;
+      if (u < p.p1)
+        op_element_swaps(cand, d, k, p.op1_hop, lane);
+      else if (u < p.p2)
+        op_block_swaps(cand, d, k, p.op2_hop, lane);
+      else
+        op_block_shift(cand, d, k, lane);
+      const double cs = ev.score(cand, txt, colstart, logs, lane);
+      if (cs > score) {
+        key = cand;
+        score = cs;
+        last = t;
+      }
+    }
+    if (lane < k) p.keys_out[w * k + lane] = (uint8_t)key.v0;
+    if (lane + 32 < k) p.keys_out[w * k + lane + 32] = (uint8_t)key.v1;
+    if (lane == 0) {
+      p.scores[w] = score;
+      if (p.draws_used) p.draws_used[w] = d.pos;
+      if (p.last_accept) p.last_accept[w] = last;
+      if (p.tries_done) p.tries_done[w] = t;
+    }
+    __syncwarp();
+  }
+}
+
+// Score given (cipher, key) pairs with the same evaluator (sct.py:158-160).
+template <int SLOTS>
+__global__ void __launch_bounds__(kSctWarps * 32)
+    sct_score_kernel(const uint8_t* __restrict__ ciphers, const int64_t* __restrict__ offsets,
+                     const int32_t* __restrict__ cipher_of, const uint8_t* __restrict__ keys,
+                     int32_t k, int64_t n_keys, const double* __restrict__ glogs,
+                     double* __restrict__ out, int32_t n, const __grid_constant__ SumPlan plan) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* logs = reinterpret_cast<double*>(smem);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint16_t* colstart = reinterpret_cast<uint16_t*>(smem + kAlpha * kAlpha * sizeof(double)) +
+                       warp * kSctMaxKey;
+  uint8_t* txt = smem + kAlpha * kAlpha * sizeof(double) + kSctWarps * kSctMaxKey * 2 +
+                 warp * text_stride(n);
+  stage_logs(logs, glogs);
+  const int64_t w = (int64_t)blockIdx.x * kSctWarps + warp;
+  if (w >= n_keys) return;
+  Evaluator<SLOTS> ev;
+  ev.init(plan, k, n, lane);
+  stage_text(txt, ciphers + offsets[cipher_of[w]], n, lane);
+  Key key;
+  key.v0 = lane < k ? keys[w * k + lane] : lane;
+  key.v1 = lane + 32 < k ? keys[w * k + lane + 32] : lane + 32;
+  const double s = ev.score(key, txt, colstart, logs, lane);
+  if (lane == 0) out[w] = s;
+}
+
+// Any-length scoring: one thread per (cipher, key), numpy's pairwise recursion done by a
+// recursive device function over on-the-fly decryption.  Used by the fitness API for texts
+// beyond the warp evaluator's plan budget (the climb kernels never take this path).
+struct LongText {
+  const uint8_t* txt;
+  const double* logs;
+  const int32_t* colstart;
+  int k;
+  __device__ __forceinline__ int at(int64_t t) const {
+    const int64_t r = t / k;
+    return txt[colstart[t - r * k] + r];
+  }
+  __device__ __forceinline__ double term(int64_t t) const {
+    return logs[at(t) * kAlpha + at(t + 1)];
+  }
+};
+
+__device__ double pairwise_leaf(const LongText& L, int64_t lo, int64_t n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int64_t i = 0; i < n; ++i) res += L.term(lo + i);
+    return res;
+  }
+  double r[8];
+  for (int j = 0; j < 8; ++j) r[j] = L.term(lo + j);
+  int64_t i = 8;
+  for (; i < n - (n % 8); i += 8)
+    for (int j = 0; j < 8; ++j) r[j] += L.term(lo + i + j);
+  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < n; ++i) res += L.term(lo + i);
+  return res;
+}
+
+// numpy's recursion (split at n/2 rounded down to a multiple of 8) with an explicit stack.
+__device__ double pairwise_iter(const LongText& L, int64_t n_terms) {
+  struct Frame { int64_t lo, n; double left; int state; };
+  Frame st[48];  // depth <= log2(n / 64) + 1
+  int sp = 0;
+  st[0] = {0, n_terms, 0.0, 0};
+  double ret = 0.0;
+  while (sp >= 0) {
+    Frame& f = st[sp];
+    const int64_t half = (f.n / 2) - (f.n / 2) % 8;
+    if (f.state == 0) {
+      if (f.n <= 128) {
+        ret = pairwise_leaf(L, f.lo, f.n);
+        --sp;
+      } else {
+        f.state = 1;
+        st[sp + 1] = {f.lo, half, 0.0, 0};
+        ++sp;
+      }
+    } else if (f.state == 1) {
+      f.left = ret;
+      f.state = 2;
+      st[sp + 1] = {f.lo + half, f.n - half, 0.0, 0};
+      ++sp;
+    } else {
+      ret = f.left + ret;
+      --sp;
+    }
+  }
+  return ret;
+}
+
+__global__ void sct_score_long_kernel(const uint8_t* __restrict__ ciphers,
+                                      const int64_t* __restrict__ offsets,
+                                      const int32_t* __restrict__ cipher_of,
+                                      const uint8_t* __restrict__ keys, int32_t k, int64_t n_keys,
+                                      const double* __restrict__ logs, double* __restrict__ out) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= n_keys) return;
+  const int32_t c = cipher_of[w];
+  const int64_t n = offsets[c + 1] - offsets[c];
+  int32_t colstart[kSctMaxKey];
+  const int64_t base = n / k, rem = n - base * k;
+  int64_t acc = 0;
+  for (int j = 0; j < k; ++j) {
+    const int col = keys[w * k + j];
+    colstart[col] = (int32_t)acc;
+    acc += base + (col < rem ? 1 : 0);
+  }
+  LongText L{ciphers + offsets[c], logs, colstart, k};
+  out[w] = n < 2 ? 0.0 : pairwise_iter(L, n - 1);
+}
+
+size_t sct_smem_bytes(int n) {
+  return kAlpha * kAlpha * sizeof(double) + kSctWarps * kSctMaxKey * 2 +
+         kSctWarps * text_stride(n);
+}
+
+template <typename K>
+cudaError_t prep_smem(K kern, size_t bytes) {
+  if (bytes > 48 * 1024)
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  return cudaSuccess;
+}
+
+int slots_for(const SumPlan& plan) {
+  const int s = (plan.n_leaves + 3) / 4;
+  return s <= 1 ? 1 : s <= 2 ? 2 : s <= 4 ? 4 : 8;
+}
+
+template <int SLOTS>
+cudaError_t climb_slots(cudaStream_t s, const SctLaunch& p, const SumPlan& plan, int sm_count) {
+  auto kern = sct_climb_kernel<SLOTS>;
+  const size_t bytes = sct_smem_bytes(p.n);
+  cudaError_t e = prep_smem(kern, bytes);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSctWarps * 32, bytes);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t need = (p.n_workers + kSctWarps - 1) / kSctWarps;
+  const int64_t resident = (int64_t)per_sm * sm_count;
+  const int grid = (int)(need < resident ? need : resident);
+  kern<<<grid, kSctWarps * 32, bytes, s>>>(p, plan);
+  return cudaGetLastError();
+}
+
+template <int SLOTS>
+cudaError_t score_slots(cudaStream_t s, const uint8_t* ciphers, const int64_t* offsets,
+                        const int32_t* cipher_of, const uint8_t* keys, int32_t k, int64_t n_keys,
+                        const double* logs, double* out, int32_t n, const SumPlan& plan) {
+  auto kern = sct_score_kernel<SLOTS>;
+  const size_t bytes = sct_smem_bytes(n);
+  cudaError_t e = prep_smem(kern, bytes);
+  if (e != cudaSuccess) return e;
+  const int grid = (int)((n_keys + kSctWarps - 1) / kSctWarps);
+  kern<<<grid, kSctWarps * 32, bytes, s>>>(ciphers, offsets, cipher_of, keys, k, n_keys, logs,
+                                           out, n, plan);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// numpy pairwise_sum recursion -> leaves + post-order merges.
+static int plan_rec(SumPlan* P, int start, int n) {
+  if (n <= 128) {
+    const int id = P->n_leaves++;
+    P->leaf_start[id] = start;
+    P->leaf_len[id] = n;
+    return id;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  const int L = plan_rec(P, start, n2);
+  const int R = plan_rec(P, start + n2, n - n2);
+  P->merge_dst[P->n_merges] = (int8_t)L;
+  P->merge_src[P->n_merges] = (int8_t)R;
+  ++P->n_merges;
+  return L;
+}
+
+void build_sum_plan(int64_t n_terms, SumPlan* plan) {
+  *plan = SumPlan{};
+  plan->n_terms = (int32_t)n_terms;
+  plan->seq = n_terms < 8;
+  plan_rec(plan, 0, (int)n_terms);
+}
+
+cudaError_t launch_sct_score_long(cudaStream_t s, const uint8_t* ciphers, const int64_t* offsets,
+                                  const int32_t* cipher_of, const uint8_t* keys, int32_t k,
+                                  int64_t n_keys, const double* logs, double* out) {
+  if (n_keys <= 0) return cudaSuccess;
+  const int grid = (int)((n_keys + 127) / 128);
+  sct_score_long_kernel<<<grid, 128, 0, s>>>(ciphers, offsets, cipher_of, keys, k, n_keys, logs,
+                                              out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sct_climb(cudaStream_t s, const SctLaunch& p, const SumPlan& plan,
+                             int sm_count) {
+  if (p.n_workers <= 0) return cudaSuccess;
+  switch (slots_for(plan)) {
+    case 1: return climb_slots<1>(s, p, plan, sm_count);
+    case 2: return climb_slots<2>(s, p, plan, sm_count);
+    case 4: return climb_slots<4>(s, p, plan, sm_count);
+    default: return climb_slots<8>(s, p, plan, sm_count);
+  }
+}
+
+cudaError_t launch_sct_score(cudaStream_t s, const uint8_t* ciphers, const int64_t* offsets,
+                             const int32_t* cipher_of, const uint8_t* keys, int32_t k,
+                             int64_t n_keys, const double* logs, int64_t* /*n_of*/, double* out,
+                             int32_t n_common, const SumPlan& plan) {
+  if (n_keys <= 0) return cudaSuccess;
+  switch (slots_for(plan)) {
+    case 1: return score_slots<1>(s, ciphers, offsets, cipher_of, keys, k, n_keys, logs, out, n_common, plan);
+    case 2: return score_slots<2>(s, ciphers, offsets, cipher_of, keys, k, n_keys, logs, out, n_common, plan);
+    case 4: return score_slots<4>(s, ciphers, offsets, cipher_of, keys, k, n_keys, logs, out, n_common, plan);
+    default: return score_slots<8>(s, ciphers, offsets, cipher_of, keys, k, n_keys, logs, out, n_common, plan);
+  }
+}
+
+}  // namespace ccg

@@ -1,0 +1,249 @@
+"""Batch entry points of the GPU engine and the in-process multi-GPU restart sharder.
+
+A "worker" is one (ciphertext, Philox stream) hill climb, exactly one task of the
+reference's run_worker_pool (search.py:49-58; mas.py:266-270, sct.py:194-198).  A batch of
+workers is split into contiguous, group-aligned ranges, one per device, and each range is
+one ccg_*_climb call on that device (one kernel launch + one group-argmax launch).  Host
+threads drive the devices concurrently (ctypes releases the GIL).  Every worker's output
+depends only on its own (ciphertext, key, stream), so results are identical for any
+device count or split -- the property the reference tests as jobs=1 == jobs=2
+(tests/test_mas.py:240-249, tests/test_sct.py:160-169).
+
+Device selection: set_devices([...]) or the CCG_DEVICES environment variable
+("0,1,2,3"); default is LOCAL_RANK (one process per GPU under torchrun) or device 0.
+"""
+from __future__ import annotations
+
+import os
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+_devices: list[int] | None = None
+
+
+def set_devices(devices) -> None:
+    """Use these CUDA devices for subsequent batches (None = back to the default)."""
+    global _devices
+    _devices = None if devices is None else [int(d) for d in devices]
+
+
+def devices() -> list[int]:
+    if _devices is not None:
+        return list(_devices)
+    env = os.environ.get("CCG_DEVICES")
+    if env:
+        return [int(x) for x in env.split(",") if x.strip()]
+    return [int(os.environ.get("LOCAL_RANK", "0"))]
+
+
+def default_device() -> int:
+    return devices()[0]
+
+
+def shard_bounds(n_items: int, n_shards: int, align: int = 1) -> list[tuple[int, int]]:
+    """Contiguous [lo, hi) ranges over n_items, boundaries on multiples of `align`,
+    as even as possible; empty ranges are dropped."""
+    align = max(1, int(align))
+    units = (n_items + align - 1) // align
+    n_shards = max(1, min(int(n_shards), units)) if units else 1
+    base, extra = divmod(units, n_shards)
+    out, u = [], 0
+    for s in range(n_shards):
+        cnt = base + (1 if s < extra else 0)
+        lo, hi = u * align, min(n_items, (u + cnt) * align)
+        if hi > lo:
+            out.append((lo, hi))
+        u += cnt
+    return out
+
+
+@dataclass
+class ClimbResult:
+    scores: np.ndarray          # int64 (MAS) or float64 (SCT), per worker
+    keys: np.ndarray            # uint8[n, 26] letter maps (MAS) / uint8[n, k] column keys (SCT)
+    group_best: np.ndarray | None
+    draws_used: np.ndarray | None
+    last_accept: np.ndarray | None
+    tries_done: np.ndarray | None
+    launches: int
+
+
+def _run_sharded(n_workers, group_size, devs, fn):
+    bounds = shard_bounds(n_workers, len(devs), group_size if group_size > 0 else 1)
+    if len(bounds) <= 1:
+        return [fn(devs[0], 0, n_workers)]
+    with ThreadPoolExecutor(max_workers=len(bounds)) as pool:
+        futs = [pool.submit(fn, devs[i], lo, hi) for i, (lo, hi) in enumerate(bounds)]
+        return [f.result() for f in futs]
+
+
+def _concat(parts, name):
+    vals = [getattr(p, name) for p in parts]
+    if any(v is None for v in vals):
+        return None
+    return np.concatenate(vals)
+
+
+def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, group_size=0,
+              draws_used=False, last_accept=False, tries_done=False, early_exit=False,
+              devices_=None) -> ClimbResult:
+    """Run stochastic_worker (mas.py:218-244) for every worker on the GPU(s).
+
+    ciphers: list of letter arrays; cipher_of: int per worker; keys: uint64[n, 2] Philox
+    keys (rng.philox_keys); table_scores: int64[676]."""
+    flat, off = _lib.ragged(ciphers)
+    cof = np.ascontiguousarray(cipher_of, dtype=np.int32).reshape(-1)
+    keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, 2)
+    table = np.ascontiguousarray(table_scores, dtype=np.int64)
+    n = cof.size
+    if keys.shape[0] != n:
+        raise ValueError("one Philox key per worker required")
+    sk = None if skips is None else np.ascontiguousarray(skips, dtype=np.uint64).reshape(-1)
+    devs = devices_ or devices()
+
+    def run(dev, lo, hi):
+        m = hi - lo
+        out = ClimbResult(
+            scores=np.empty(m, dtype=np.int64),
+            keys=np.empty((m, 26), dtype=np.uint8),
+            group_best=np.empty(m // group_size, dtype=np.int64) if group_size > 0 else None,
+            draws_used=np.empty(m, dtype=np.uint64) if draws_used else None,
+            last_accept=np.empty(m, dtype=np.int64) if last_accept else None,
+            tries_done=np.empty(m, dtype=np.int64) if tries_done else None,
+            launches=0,
+        )
+        if m == 0:
+            return out
+        c_of = np.ascontiguousarray(cof[lo:hi])
+        k = np.ascontiguousarray(keys[lo:hi])
+        s = None if sk is None else np.ascontiguousarray(sk[lo:hi])
+        a = _lib.MasClimbArgs()
+        a.ciphers, a.offsets, a.n_ciphers = _lib.ptr(flat), _lib.ptr(off), off.size - 1
+        a.cipher_of, a.keys, a.skips = _lib.ptr(c_of), _lib.ptr(k), _lib.ptr(s)
+        a.n_workers, a.climbings, a.table = m, int(climbings), _lib.ptr(table)
+        a.scores, a.maps = _lib.ptr(out.scores), _lib.ptr(out.keys)
+        a.draws_used, a.last_accept = _lib.ptr(out.draws_used), _lib.ptr(out.last_accept)
+        a.tries_done = _lib.ptr(out.tries_done)
+        a.group_size, a.group_best = int(group_size), _lib.ptr(out.group_best)
+        a.flags = _lib.FLAG_EARLY_EXIT if early_exit else 0
+        ctx = _lib.context(dev)
+        with ctx.lock:
+            before = ctx.launches()
+            _lib.check(_lib.load().ccg_mas_climb(ctx.handle, a), "mas_climb")
+            out.launches = ctx.launches() - before
+        return out
+
+    parts = _run_sharded(n, group_size, devs, run)
+    return ClimbResult(
+        scores=_concat(parts, "scores"), keys=_concat(parts, "keys"),
+        group_best=_concat(parts, "group_best"), draws_used=_concat(parts, "draws_used"),
+        last_accept=_concat(parts, "last_accept"), tries_done=_concat(parts, "tries_done"),
+        launches=sum(p.launches for p in parts),
+    )
+
+
+def sct_climb(ciphers, cipher_of, keys, logs, key_length, climbings, *, p1=33, p2=66, op1_hop=3,
+              op2_hop=3, skips=None, group_size=0, draws_used=False, last_accept=False,
+              tries_done=False, devices_=None) -> ClimbResult:
+    """Run sct_worker (sct.py:148-170) for every worker on the GPU(s).  All ciphertexts
+    referenced by one call must share a length (the numpy pairwise-sum plan is per length)."""
+    flat, off = _lib.ragged(ciphers)
+    cof = np.ascontiguousarray(cipher_of, dtype=np.int32).reshape(-1)
+    keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, 2)
+    lg = np.ascontiguousarray(logs, dtype=np.float64)
+    n = cof.size
+    k = int(key_length)
+    if keys.shape[0] != n:
+        raise ValueError("one Philox key per worker required")
+    sk = None if skips is None else np.ascontiguousarray(skips, dtype=np.uint64).reshape(-1)
+    devs = devices_ or devices()
+
+    def run(dev, lo, hi):
+        m = hi - lo
+        out = ClimbResult(
+            scores=np.empty(m, dtype=np.float64),
+            keys=np.empty((m, k), dtype=np.uint8),
+            group_best=np.empty(m // group_size, dtype=np.int64) if group_size > 0 else None,
+            draws_used=np.empty(m, dtype=np.uint64) if draws_used else None,
+            last_accept=np.empty(m, dtype=np.int64) if last_accept else None,
+            tries_done=np.empty(m, dtype=np.int64) if tries_done else None,
+            launches=0,
+        )
+        if m == 0:
+            return out
+        c_of = np.ascontiguousarray(cof[lo:hi])
+        kk = np.ascontiguousarray(keys[lo:hi])
+        s = None if sk is None else np.ascontiguousarray(sk[lo:hi])
+        a = _lib.SctClimbArgs()
+        a.ciphers, a.offsets, a.n_ciphers = _lib.ptr(flat), _lib.ptr(off), off.size - 1
+        a.cipher_of, a.keys, a.skips = _lib.ptr(c_of), _lib.ptr(kk), _lib.ptr(s)
+        a.n_workers, a.key_length, a.climbings = m, k, int(climbings)
+        a.p1, a.p2, a.op1_hop, a.op2_hop = int(p1), int(p2), int(op1_hop), int(op2_hop)
+        a.logs, a.scores, a.keys_out = _lib.ptr(lg), _lib.ptr(out.scores), _lib.ptr(out.keys)
+        a.draws_used, a.last_accept = _lib.ptr(out.draws_used), _lib.ptr(out.last_accept)
+        a.tries_done = _lib.ptr(out.tries_done)
+        a.group_size, a.group_best = int(group_size), _lib.ptr(out.group_best)
+        ctx = _lib.context(dev)
+        with ctx.lock:
+            before = ctx.launches()
+            _lib.check(_lib.load().ccg_sct_climb(ctx.handle, a), "sct_climb")
+            out.launches = ctx.launches() - before
+        return out
+
+    parts = _run_sharded(n, group_size, devs, run)
+    return ClimbResult(
+        scores=_concat(parts, "scores"), keys=_concat(parts, "keys"),
+        group_best=_concat(parts, "group_best"), draws_used=_concat(parts, "draws_used"),
+        last_accept=_concat(parts, "last_accept"), tries_done=_concat(parts, "tries_done"),
+        launches=sum(p.launches for p in parts),
+    )
+
+
+def mas_delta_batch(texts, pairs, table_scores) -> np.ndarray:
+    """text_swap_delta (mas.py:315-317) for many (text, a, b) on the GPU."""
+    flat, off = _lib.ragged(texts)
+    ab = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
+    table = np.ascontiguousarray(table_scores, dtype=np.int64)
+    out = np.empty(off.size - 1, dtype=np.int64)
+    ctx = _lib.context(default_device())
+    with ctx.lock:
+        _lib.check(_lib.load().ccg_mas_delta_batch(ctx.handle, _lib.ptr(flat), _lib.ptr(off),
+                                                   out.size, _lib.ptr(ab), _lib.ptr(table),
+                                                   _lib.ptr(out)), "mas_delta")
+    return out
+
+
+def mas_delta_counts_batch(counts, pairs, score_matrix) -> np.ndarray:
+    """swap_delta (mas.py:181-210) for many (count matrix, a, b) on the GPU."""
+    cm = np.ascontiguousarray(counts, dtype=np.int64).reshape(-1, 676)
+    ab = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
+    sm = np.ascontiguousarray(score_matrix, dtype=np.int64).reshape(676)
+    out = np.empty(cm.shape[0], dtype=np.int64)
+    ctx = _lib.context(default_device())
+    with ctx.lock:
+        _lib.check(_lib.load().ccg_mas_delta_counts_batch(ctx.handle, _lib.ptr(cm), out.size,
+                                                          _lib.ptr(ab), _lib.ptr(sm),
+                                                          _lib.ptr(out)), "mas_delta_counts")
+    return out
+
+
+def sct_score_batch(ciphers, cipher_of, keys, logs) -> np.ndarray:
+    """candidate_score (sct.py:158-160) for many (ciphertext, key) pairs on the GPU."""
+    flat, off = _lib.ragged(ciphers)
+    cof = np.ascontiguousarray(cipher_of, dtype=np.int32).reshape(-1)
+    kk = np.ascontiguousarray(keys, dtype=np.uint8)
+    if kk.ndim != 2 or kk.shape[0] != cof.size:
+        raise ValueError("keys must be [n_keys, key_length]")
+    lg = np.ascontiguousarray(logs, dtype=np.float64)
+    out = np.empty(cof.size, dtype=np.float64)
+    ctx = _lib.context(default_device())
+    with ctx.lock:
+        _lib.check(_lib.load().ccg_sct_score_batch(ctx.handle, _lib.ptr(flat), _lib.ptr(off),
+                                                   off.size - 1, _lib.ptr(cof), _lib.ptr(kk),
+                                                   kk.shape[1], cof.size, _lib.ptr(lg),
+                                                   _lib.ptr(out)), "sct_score")
+    return out

@@ -1,0 +1,169 @@
+"""Monoalphabetic-substitution attack (reference mas.py:1-299), GPU-backed.
+
+Stochastic better-neighbour climbing (mas.py:218-299) runs entirely on the GPU: one
+warp per worker (csrc/ccg_mas.cu).  Signatures, defaults, validation messages and
+result objects follow the reference so this module drops in for it; `jobs` is accepted
+for signature compatibility and has no effect on results (the reference guarantees the
+same: search.py:4-7).  The deterministic best-neighbour variant (mas.py:84-169) is the
+next item on the build plan and is not yet on the GPU.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import engine
+from .codec import ALPHABET_SIZE, MappedText
+from .ngrams import BigramTable
+from .pairs import PAIR_TOTAL, index_to_pair
+from .rng import WorkerRng, philox_keys, worker_stream_index
+from .search import RestartSummary, SolveResult, fold_restarts
+
+
+@dataclass
+class MasSolverConfig:
+    """mas.py:39-65."""
+
+    mode: str = "stochastic"
+    workers: int = 64
+    iterations: int = 500
+    climbings: int = 10_000
+    restarts: int = 1
+    global_seed: int = 0
+
+    def __post_init__(self):
+        if self.mode not in ("deterministic", "stochastic"):
+            raise ValueError(f"unknown mode {self.mode!r}")
+        if self.mode == "deterministic" and self.workers != PAIR_TOTAL:
+            raise ValueError(
+                f"deterministic mode requires workers={PAIR_TOTAL} (one per letter pair)"
+            )
+        for name in ("workers", "iterations", "climbings", "restarts"):
+            if getattr(self, name) < 1:
+                raise ValueError(f"{name} must be at least 1")
+
+
+def _check_cipher(cipher) -> np.ndarray:
+    text = np.asarray(cipher, dtype=np.int64)
+    if text.size < 2 or np.unique(text).size < 2:
+        raise ValueError("ciphertext must contain at least two distinct letters")
+    return text
+
+
+def bigram_count_matrix(text: MappedText) -> np.ndarray:
+    """26x26 adjacent-pair counts (mas.py:172-178)."""
+    t = np.asarray(text, dtype=np.int64)
+    if t.size < 2:
+        return np.zeros((ALPHABET_SIZE, ALPHABET_SIZE), dtype=np.int64)
+    flat = np.bincount(t[:-1] * ALPHABET_SIZE + t[1:], minlength=ALPHABET_SIZE * ALPHABET_SIZE)
+    return flat.astype(np.int64).reshape(ALPHABET_SIZE, ALPHABET_SIZE)
+
+
+def swap_delta(counts: np.ndarray, a: int, b: int, score_matrix: np.ndarray) -> int:
+    """Exact score change of interchanging letters a, b (mas.py:181-210), on the GPU."""
+    return int(engine.mas_delta_counts_batch(counts, [(a, b)], score_matrix)[0])
+
+
+def text_swap_delta(text: MappedText, a: int, b: int, table: BigramTable) -> int:
+    """swap_delta on the text's own count matrix (mas.py:315-317), on the GPU."""
+    return int(engine.mas_delta_batch([text], [(a, b)], table.scores)[0])
+
+
+def stochastic_worker(cipher: MappedText, table: BigramTable, climbings: int,
+                      state: WorkerRng) -> tuple[np.ndarray, int]:
+    """One worker's climb from the ciphertext (mas.py:218-244) as a one-warp GPU launch.
+    `state` is advanced by exactly the draws the worker consumed."""
+    text = np.asarray(cipher, dtype=np.int64)
+    res = engine.mas_climb([text], [0], [state.key], table.scores, climbings,
+                           skips=[state.position], draws_used=True)
+    state.advance(int(res.draws_used[0]))
+    return res.keys[0].astype(np.int64)[text], int(res.scores[0])
+
+
+def _restart_batch(text, table, cfg, restarts, early_exit=True):
+    """All workers of the given restarts in one engine call; one SolveResult each."""
+    W = cfg.workers
+    streams = [worker_stream_index(r, w) for r in restarts for w in range(W)]
+    keys = philox_keys([cfg.global_seed], streams)
+    res = engine.mas_climb([text], np.zeros(len(streams), np.int32), keys, table.scores,
+                           cfg.climbings, group_size=W, early_exit=early_exit)
+    out = []
+    for i, _ in enumerate(restarts):
+        sc = res.scores[i * W:(i + 1) * W]
+        best = int(res.group_best[i])
+        out.append(SolveResult(
+            best_text=res.keys[i * W + best].astype(np.int64)[text],
+            best_score=int(sc[best]),
+            per_worker_scores=[int(v) for v in sc],
+            history=[],
+        ))
+    return out
+
+
+def solve_stochastic(cipher: MappedText, table: BigramTable, cfg: MasSolverConfig, jobs: int = 1,
+                     restart: int = 0) -> SolveResult:
+    """cfg.workers independent climbs with streams (restart << 32) | w; the first maximum
+    wins (mas.py:253-278)."""
+    text = _check_cipher(cipher)
+    return _restart_batch(text, table, cfg, [restart])[0]
+
+
+def _batched_restarts(make_batch, restarts: int, workers: int, stop):
+    """Lazily evaluate restarts in device-sized chunks, fold them in order (search.py:61-86).
+    Results equal the sequential reference: restarts are independent of each other and of
+    `stop`, which is still applied restart by restart."""
+    target = 8192 * max(1, len(engine.devices()))  # workers per chunk: ~one full wave
+    chunk = max(1, min(restarts, target // max(1, workers)))
+
+    def gen():
+        r = 0
+        while r < restarts:
+            rs = list(range(r, min(restarts, r + chunk)))
+            t0 = time.perf_counter()
+            results = make_batch(rs)
+            dt = (time.perf_counter() - t0) / len(rs)
+            for res in results:
+                yield res, dt
+            r += len(rs)
+
+    return fold_restarts(gen(), stop)
+
+
+def solve_with_restarts(cipher: MappedText, table: BigramTable, cfg: MasSolverConfig,
+                        jobs: int = 1, stop=None) -> tuple[SolveResult, list[RestartSummary]]:
+    """mas.py:281-299."""
+    if cfg.mode == "deterministic":
+        from .search import run_restarts
+
+        return run_restarts(lambda r: solve_deterministic(cipher, table, cfg, restart=r),
+                            cfg.restarts, stop=stop)
+    text = _check_cipher(cipher)
+    return _batched_restarts(lambda rs: _restart_batch(text, table, cfg, rs), cfg.restarts,
+                             cfg.workers, stop)
+
+
+# ------------------------------------------------------------------ deterministic mode
+_NEXT = ("the deterministic best-neighbour MAS solver (reference mas.py:84-169) is the next "
+         "build item (SURVEY.md 8f-1) and is not on the CUDA engine yet")
+
+
+def deterministic_step(current, pivot, table):
+    raise NotImplementedError(_NEXT)
+
+
+def climb(current, best_index, pivot):
+    other_left, other_right = index_to_pair(best_index)
+    pl, pr = int(pivot[0]), int(pivot[1])
+    if pl == other_right or pr == other_left:
+        raise ValueError(f"worker {best_index} is excluded for pivot ({pl}, {pr})")
+    first = np.arange(ALPHABET_SIZE, dtype=np.int64)
+    first[[pl, other_left]] = first[[other_left, pl]]
+    second = np.arange(ALPHABET_SIZE, dtype=np.int64)
+    second[[pr, other_right]] = second[[other_right, pr]]
+    return second[first][np.asarray(current, dtype=np.int64)]
+
+
+def solve_deterministic(cipher, table, cfg, restart: int = 0):
+    raise NotImplementedError(_NEXT)

@@ -1,0 +1,170 @@
+"""Bigram tables and text fitness (reference ngrams.py:1-172).
+
+Table construction, parsing and formatting are host-side.  The fitness functions
+`score_text` / `log_score_text` run on the GPU through the C ABI (bit-exact: integer
+sums, and float64 sums in numpy's pairwise order).
+"""
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .codec import ALPHABET_SIZE, MappedText, map_text, normalize
+
+TABLE_SIZE = ALPHABET_SIZE * ALPHABET_SIZE  # 676
+DEFAULT_LOG_FLOOR = -24.0
+
+
+def bigram_index(first: int, second: int) -> int:
+    if not (0 <= first < ALPHABET_SIZE and 0 <= second < ALPHABET_SIZE):
+        raise ValueError(f"letter indices out of range: ({first}, {second})")
+    return ALPHABET_SIZE * first + second
+
+
+@dataclass(frozen=True)
+class BigramTable:
+    """676 non-negative integer scores indexed by 26*first + second."""
+
+    scores: np.ndarray
+
+    def __post_init__(self):
+        arr = np.ascontiguousarray(self.scores, dtype=np.int64)
+        if arr.shape != (TABLE_SIZE,):
+            raise ValueError(f"expected {TABLE_SIZE} entries, got {arr.shape}")
+        if arr.size and arr.min() < 0:
+            raise ValueError("bigram scores must be non-negative")
+        object.__setattr__(self, "scores", arr)
+
+    @property
+    def matrix(self) -> np.ndarray:
+        return self.scores.reshape(ALPHABET_SIZE, ALPHABET_SIZE)
+
+
+@dataclass(frozen=True)
+class LogBigramTable:
+    """676 log2 bigram probabilities; unseen bigrams sit at `floor`."""
+
+    logs: np.ndarray
+    floor: float
+
+    def __post_init__(self):
+        arr = np.ascontiguousarray(self.logs, dtype=np.float64)
+        if arr.shape != (TABLE_SIZE,):
+            raise ValueError(f"expected {TABLE_SIZE} entries, got {arr.shape}")
+        if not np.isfinite(arr).all():
+            raise ValueError("log scores must be finite")
+        if arr.size and arr.max() > 0:
+            raise ValueError("log2 probabilities cannot be positive")
+        if arr.size and arr.min() < self.floor:
+            raise ValueError("log table entries below the configured floor")
+        object.__setattr__(self, "logs", arr)
+
+    @property
+    def matrix(self) -> np.ndarray:
+        return self.logs.reshape(ALPHABET_SIZE, ALPHABET_SIZE)
+
+
+def parse_bigram_file(lines) -> BigramTable:
+    """`<bigram> <integer>` per line; blank lines skipped; missing bigrams are 0;
+    a repeated bigram keeps its last value with a warning (ngrams.py:76-108)."""
+    if isinstance(lines, str):
+        lines = lines.splitlines()
+    scores = np.zeros(TABLE_SIZE, dtype=np.int64)
+    seen = set()
+    for lineno, line in enumerate(lines, start=1):
+        fields = line.split()
+        if not fields:
+            continue
+        if len(fields) != 2:
+            raise ValueError(f"line {lineno}: expected '<bigram> <score>', got {line!r}")
+        bigram, value_text = fields
+        if len(bigram) != 2 or any(not ("a" <= c <= "z") for c in bigram):
+            raise ValueError(f"line {lineno}: bad bigram {bigram!r}")
+        try:
+            value = int(value_text)
+        except ValueError:
+            raise ValueError(f"line {lineno}: bad score {value_text!r}") from None
+        if value < 0:
+            raise ValueError(f"line {lineno}: negative score {value}")
+        idx = bigram_index(ord(bigram[0]) - 97, ord(bigram[1]) - 97)
+        if idx in seen:
+            warnings.warn(f"duplicate bigram {bigram!r}; keeping the later value")
+        seen.add(idx)
+        scores[idx] = value
+    return BigramTable(scores)
+
+
+def format_bigram_file(table: BigramTable) -> str:
+    """All 676 records in lexicographic order (round-trips through parse_bigram_file)."""
+    rows = (f"{chr(97 + i // 26)}{chr(97 + i % 26)} {int(v)}" for i, v in enumerate(table.scores))
+    return "\n".join(rows) + "\n"
+
+
+def build_table_from_corpus(corpus: str) -> BigramTable:
+    sym = map_text(normalize(corpus))
+    if sym.size < 2:
+        return BigramTable(np.zeros(TABLE_SIZE, dtype=np.int64))
+    return BigramTable(np.bincount(sym[:-1] * ALPHABET_SIZE + sym[1:], minlength=TABLE_SIZE))
+
+
+def build_log_table(table: BigramTable, floor: float = DEFAULT_LOG_FLOOR) -> LogBigramTable:
+    """log2(count / total); zero counts get `floor`, which must lie below every
+    observed bigram (ngrams.py:143-163)."""
+    if floor >= 0:
+        raise ValueError("floor must be negative")
+    total = int(table.scores.sum())
+    if total == 0:
+        raise ValueError("cannot build probabilities from an all-zero table")
+    seen = table.scores > 0
+    logs = np.full(TABLE_SIZE, floor, dtype=np.float64)
+    logs[seen] = np.log2(table.scores[seen] / total)
+    if seen.any() and logs[seen].min() < floor:
+        raise ValueError(
+            f"floor {floor} is above the rarest observed bigram ({float(logs[seen].min()):.3f}); "
+            "pass a lower floor"
+        )
+    return LogBigramTable(logs, floor)
+
+
+def _device():
+    from .engine import default_device
+
+    return _lib.context(default_device())
+
+
+def score_text_batch(texts, table: BigramTable) -> np.ndarray:
+    """score_text for many texts in one GPU call."""
+    flat, off = _lib.ragged(texts)
+    out = np.empty(len(off) - 1, dtype=np.int64)
+    ctx = _device()
+    with ctx.lock:
+        _lib.check(_lib.load().ccg_score_text_batch(ctx.handle, _lib.ptr(flat), _lib.ptr(off),
+                                                    out.size, _lib.ptr(table.scores), _lib.ptr(out)),
+                   "score_text")
+    return out
+
+
+def log_score_text_batch(texts, table: LogBigramTable) -> np.ndarray:
+    """log_score_text for many texts in one GPU call (numpy pairwise order)."""
+    flat, off = _lib.ragged(texts)
+    out = np.empty(len(off) - 1, dtype=np.float64)
+    ctx = _device()
+    with ctx.lock:
+        _lib.check(_lib.load().ccg_log_score_text_batch(ctx.handle, _lib.ptr(flat), _lib.ptr(off),
+                                                        out.size, _lib.ptr(table.logs),
+                                                        _lib.ptr(out)),
+                   "log_score_text")
+    return out
+
+
+def score_text(text: MappedText, table: BigramTable) -> int:
+    """Sum of table scores over adjacent letter pairs (ngrams.py:134-140), on the GPU."""
+    return int(score_text_batch([text], table)[0])
+
+
+def log_score_text(text: MappedText, table: LogBigramTable) -> float:
+    """Sum of log2 bigram probabilities (ngrams.py:166-172), on the GPU, bit-exact."""
+    return float(log_score_text_batch([text], table)[0])

@@ -1,0 +1,150 @@
+"""Single-columnar-transposition attack (reference sct.py:1-210), GPU-backed.
+
+sct_worker / solve_sct run on the GPU: one warp per worker, candidate keys mutated in
+registers, decryption by index arithmetic, float64 scoring in numpy's pairwise order
+(csrc/ccg_sct.cu).  The operator functions below are the reference's host-side helpers,
+drawing from a (GPU-generated) WorkerRng stream; the climb itself never calls them.
+"""
+from __future__ import annotations
+
+import enum
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import engine
+from .ciphers import sct_decrypt
+from .codec import MappedText
+from .ngrams import LogBigramTable
+from .rng import WorkerRng, philox_keys, worker_stream_index
+from .search import RestartSummary, SolveResult
+from .mas import _batched_restarts
+
+
+class Operator(enum.Enum):
+    ELEMENT_SWAP = 1
+    BLOCK_SWAP = 2
+    BLOCK_SHIFT = 3
+
+
+@dataclass
+class SctSolverConfig:
+    """sct.py:43-66."""
+
+    key_length: int
+    workers: int = 64
+    climbings: int = 15_000
+    p1: int = 33
+    p2: int = 66
+    op1_hop: int = 3
+    op2_hop: int = 3
+    restarts: int = 1
+    global_seed: int = 0
+
+    def __post_init__(self):
+        if self.key_length < 2:
+            raise ValueError("key_length must be at least 2")
+        if not 0 <= self.p1 <= self.p2 <= 100:
+            raise ValueError("thresholds must satisfy 0 <= p1 <= p2 <= 100")
+        if self.climbings < 0:
+            raise ValueError("climbings must be non-negative")
+        for name in ("workers", "op1_hop", "op2_hop", "restarts"):
+            if getattr(self, name) < 1:
+                raise ValueError(f"{name} must be at least 1")
+
+
+def select_operator(u_percent: int, p1: int, p2: int) -> Operator:
+    """[0,p1) -> I, [p1,p2) -> II, [p2,100) -> III (sct.py:69-79)."""
+    if not 0 <= p1 <= p2 <= 100:
+        raise ValueError("thresholds must satisfy 0 <= p1 <= p2 <= 100")
+    if not 0 <= u_percent < 100:
+        raise ValueError("u_percent must lie in [0, 100)")
+    if u_percent < p1:
+        return Operator.ELEMENT_SWAP
+    return Operator.BLOCK_SWAP if u_percent < p2 else Operator.BLOCK_SHIFT
+
+
+def apply_element_swaps(key: np.ndarray, state: WorkerRng, max_hops: int) -> np.ndarray:
+    """1..max_hops random position swaps (sct.py:82-89)."""
+    out = np.array(key, dtype=np.int64, copy=True)
+    for _ in range(1 + state.next_int_below(max_hops)):
+        i, j = state.next_distinct_pair(out.size)
+        out[[i, j]] = out[[j, i]]
+    return out
+
+
+def apply_block_swaps(key: np.ndarray, state: WorkerRng, max_hops: int) -> np.ndarray:
+    """1..max_hops swaps of equal, non-overlapping blocks (sct.py:92-112)."""
+    out = np.array(key, dtype=np.int64, copy=True)
+    k = out.size
+    for _ in range(1 + state.next_int_below(max_hops)):
+        length = 1 + state.next_int_below(k // 2)
+        while True:
+            p, q = state.next_distinct_pair(k - length + 1)
+            if abs(p - q) >= length:
+                break
+        p, q = min(p, q), max(p, q)
+        out[p:p + length], out[q:q + length] = out[q:q + length].copy(), out[p:p + length].copy()
+    return out
+
+
+def apply_block_shift(key: np.ndarray, state: WorkerRng) -> np.ndarray:
+    """Move one block to a different in-bounds position (sct.py:115-135)."""
+    out = np.array(key, dtype=np.int64, copy=True)
+    k = out.size
+    length = 1 + state.next_int_below(k - 1)
+    starts = k - length + 1
+    p = state.next_int_below(starts)
+    dest = state.next_int_below(starts)
+    while dest == p:
+        dest = state.next_int_below(starts)
+    lo, hi = min(p, dest), max(p, dest) + length
+    out[lo:hi] = np.roll(out[lo:hi], -length if dest > p else length)
+    return out
+
+
+def sct_worker(cipher: MappedText, logs: LogBigramTable, cfg: SctSolverConfig,
+               state: WorkerRng) -> tuple[np.ndarray, float]:
+    """One worker's climb from permutation(k) (sct.py:148-170) as a one-warp GPU launch;
+    `state` is advanced by exactly the draws consumed."""
+    text = np.asarray(cipher, dtype=np.int64)
+    if text.size < cfg.key_length:
+        raise ValueError("ciphertext shorter than the key")
+    res = engine.sct_climb([text], [0], [state.key], logs.logs, cfg.key_length, cfg.climbings,
+                           p1=cfg.p1, p2=cfg.p2, op1_hop=cfg.op1_hop, op2_hop=cfg.op2_hop,
+                           skips=[state.position], draws_used=True)
+    state.advance(int(res.draws_used[0]))
+    return res.keys[0].astype(np.int64), float(res.scores[0])
+
+
+def _restart_batch(text, logs, cfg, restarts):
+    W = cfg.workers
+    streams = [worker_stream_index(r, w) for r in restarts for w in range(W)]
+    keys = philox_keys([cfg.global_seed], streams)
+    res = engine.sct_climb([text], np.zeros(len(streams), np.int32), keys, logs.logs,
+                           cfg.key_length, cfg.climbings, p1=cfg.p1, p2=cfg.p2,
+                           op1_hop=cfg.op1_hop, op2_hop=cfg.op2_hop, group_size=W)
+    out = []
+    for i, _ in enumerate(restarts):
+        sc = res.scores[i * W:(i + 1) * W]
+        best = int(res.group_best[i])
+        key = res.keys[i * W + best].astype(np.int64)
+        out.append(SolveResult(
+            best_text=sct_decrypt(text, key),
+            best_score=float(sc[best]),
+            per_worker_scores=[float(v) for v in sc],
+            history=[],
+            best_key=key,
+        ))
+    return out
+
+
+def solve_sct(cipher: MappedText, logs: LogBigramTable, cfg: SctSolverConfig, jobs: int = 1,
+              stop=None) -> tuple[SolveResult, list[RestartSummary]]:
+    """Workers x restarts on the GPU; lowest worker index wins ties, earliest restart wins
+    ties, `stop` applied restart by restart (sct.py:179-210)."""
+    text = np.asarray(cipher, dtype=np.int64)
+    if text.size < cfg.key_length:
+        raise ValueError("ciphertext shorter than the key")
+    return _batched_restarts(lambda rs: _restart_batch(text, logs, cfg, rs), cfg.restarts,
+                             cfg.workers, stop)

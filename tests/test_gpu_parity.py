@@ -1,0 +1,323 @@
+"""GPU parity: the CUDA engine (through the C ABI) vs the reference's golden outputs and
+the pinned CPU oracle.  Integer and index work must be bit-exact; SCT float64 scores
+must be bit-exact too (numpy pairwise order), so no tolerance appears below."""
+import numpy as np
+import pytest
+
+import paper_2103_13937_b200 as cc
+from paper_2103_13937_b200 import engine
+from paper_2103_13937_b200.rng import philox_key, philox_keys
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    from paper_2103_13937_b200 import _lib
+
+    if _lib.device_count() == 0:
+        pytest.fail("no CUDA device visible: GPU tests must run on the B200 box")
+
+
+# ------------------------------------------------------------------ rng (rng.py:58-97)
+def test_philox_uniforms_match_reference(golden):
+    g = golden.load("rng")
+    for i, (s, w) in enumerate(zip(g["keys_seed"], g["keys_stream"])):
+        got = cc.rng.draws(int(s), int(w), 300)
+        assert np.array_equal(got, g["uniforms"][i]), (s, w)
+        for skip in (1, 3, 5, 130):
+            assert np.array_equal(cc.rng.draws(int(s), int(w), 40, skip=skip),
+                                  g["uniforms"][i][skip:skip + 40])
+
+
+def test_int_below_exact_against_float64():
+    from paper_2103_13937_b200 import _lib
+
+    ctx = _lib.context(0)
+    n = 1 << 20
+    for seed, stream in [(5, 9), (2**63 - 1, (7 << 32) | 3)]:
+        k0, k1 = philox_key(seed, stream)
+        u = np.empty(n)
+        _lib.check(_lib.load().ccg_philox_uniform(ctx.handle, k0, k1, 0, n, _lib.ptr(u)), "u")
+        for bound in (1, 2, 3, 7, 26, 99, 100, 1999, 2**20 + 3, 2**31 - 1):
+            got = np.empty(n, dtype=np.int64)
+            _lib.check(_lib.load().ccg_philox_int_below(ctx.handle, k0, k1, 0, bound, n,
+                                                        _lib.ptr(got)), "ib")
+            assert np.array_equal(got, (u * bound).astype(np.int64)), bound
+
+
+def test_worker_rng_api(golden):
+    g = golden.load("rng")
+    for b in (2, 3, 10, 26):
+        st = cc.WorkerRng(17, b)
+        got = np.array([st.next_distinct_pair(b) for _ in range(2000)])
+        assert np.array_equal(got, g[f"pairs_{b}"])
+    for n in (1, 2, 3, 5, 10, 26, 40, 64):
+        assert np.array_equal(cc.WorkerRng(19, n).permutation(n), g[f"perm_{n}"])
+
+
+# ------------------------------------------------------------------ fitness
+def test_score_text_batch_matches_reference(golden):
+    g = golden.load("scoring")
+    texts = golden.scoring_texts()
+    rnd = cc.BigramTable(g["rnd_table"])
+    eng = cc.BigramTable(golden.english_scores())
+    assert np.array_equal(cc.score_text_batch(texts, rnd), g["int_scores"])
+    assert np.array_equal(cc.score_text_batch(texts, eng), g["eng_scores"])
+
+
+def test_log_score_text_bit_exact(golden):
+    g = golden.load("scoring")
+    logs = cc.LogBigramTable(golden.english_logs(), -24.0)
+    got = cc.log_score_text_batch(golden.scoring_texts(), logs)
+    assert got.tolist() == g["log_scores"].tolist()  # bit-exact float64
+    assert cc.log_score_text(np.array([3]), logs) == 0.0
+
+
+def test_log_score_random_lengths_vs_oracle():
+    rng = np.random.default_rng(7)
+    logs = -rng.random(676) * 20 - 1
+    tab = cc.LogBigramTable(logs, -30.0)
+    lens = list(range(0, 300)) + [511, 512, 513, 1000, 1025, 1500, 2047, 2048, 2049, 3000, 4096]
+    texts = [rng.integers(0, 26, L) for L in lens]
+    got = cc.log_score_text_batch(texts, tab)
+    want = [O.log_score_text(t, logs) for t in texts]
+    assert got.tolist() == want
+
+
+def test_delta_acceptance_05(golden):
+    table, cases, want = golden.delta_cases()
+    got = engine.mas_delta_batch([c[0] for c in cases], [(c[1], c[2]) for c in cases], table)
+    assert np.array_equal(got, want)
+
+
+def test_delta_wide_tables_vs_oracle():
+    rng = np.random.default_rng(8)
+    for high in (70_000, 2**40):
+        table = rng.integers(0, high, 676)
+        texts = [rng.integers(0, 26, int(rng.integers(2, 400))) for _ in range(300)]
+        pairs = [tuple(rng.choice(26, 2, replace=False)) for _ in texts]
+        got = engine.mas_delta_batch(texts, pairs, table)
+        want = [O.text_swap_delta(t, a, b, table) for t, (a, b) in zip(texts, pairs)]
+        assert got.tolist() == want
+
+
+def test_swap_delta_on_count_matrices():
+    rng = np.random.default_rng(9)
+    for signed in (False, True):
+        S = rng.integers(-500 if signed else 0, 900, 676)
+        for _ in range(50):
+            t = rng.integers(0, 26, int(rng.integers(2, 300)))
+            a, b = (int(v) for v in rng.choice(26, 2, replace=False))
+            counts = cc.bigram_count_matrix(t)
+            assert cc.swap_delta(counts, a, b, S.reshape(26, 26)) == O.text_swap_delta(t, a, b, S)
+
+
+# ------------------------------------------------------------------ MAS climb
+def test_stochastic_worker_golden(golden):
+    for cipher, table, climb, seed, stream, want_text, want_score in golden.mas_worker_cases(
+            O.permutation):
+        st = cc.WorkerRng(seed, stream)
+        text, score = cc.stochastic_worker(cipher, cc.BigramTable(table), climb, st)
+        assert score == want_score
+        assert np.array_equal(text, want_text)
+
+
+def test_stochastic_worker_advances_state_like_reference():
+    # after a worker, the state continues exactly where the reference's generator would
+    t = np.random.default_rng(1).integers(0, 26, 120)
+    tab = cc.BigramTable(np.random.default_rng(2).integers(0, 500, 676))
+    st = cc.WorkerRng(3, 4)
+    cc.stochastic_worker(t, tab, 700, st)
+    # the oracle consumes the same number of draws: replay by counting pairs
+    pairs = O.distinct_pairs(3, 4, 26, 700)
+    u = O.uniforms(3, 4, 2000)
+    ints = (u * 26).astype(int)
+    pos = 0
+    for _ in range(700):
+        a = ints[pos]; pos += 1
+        b = ints[pos]; pos += 1
+        while b == a:
+            b = ints[pos]; pos += 1
+    assert st.position == pos
+    assert pairs.shape == (700, 2)
+    # and a second worker from the advanced state matches the oracle with skip
+    text2, score2 = cc.stochastic_worker(t, tab, 300, st)
+    o_text, o_score, _, _ = O.stochastic_worker(t, tab.scores, 300, 3, 4, skip=pos)
+    assert score2 == o_score and np.array_equal(text2, o_text)
+
+
+@pytest.mark.parametrize("early_exit", [False, True])
+def test_mas_solve_golden_per_worker(golden, early_exit):
+    g = golden.load("mas_solve")
+    cipher = g["cipher"].astype(np.int64)
+    eng = golden.english_scores()
+    for r in range(2):
+        keys = philox_keys([7000], [(r << 32) | w for w in range(64)])
+        res = engine.mas_climb([cipher], np.zeros(64, np.int32), keys, eng, 10_000, group_size=64,
+                               early_exit=early_exit, tries_done=True)
+        assert res.scores.tolist() == g["per_worker"][r].tolist()
+        best = int(res.group_best[0])
+        assert best == int(np.argmax(g["per_worker"][r]))
+        assert np.array_equal(res.keys[best][cipher], g["best_text"][r])
+        if early_exit:
+            assert res.tries_done.max() <= 10_000
+        else:
+            assert (res.tries_done == 10_000).all()
+
+
+def test_solve_stochastic_api_golden(golden):
+    g = golden.load("mas_solve")
+    cipher = g["cipher"].astype(np.int64)
+    table = cc.BigramTable(golden.english_scores())
+    cfg = cc.MasSolverConfig(workers=64, climbings=10_000, restarts=20, global_seed=7000)
+    for r in range(2):
+        res = cc.solve_stochastic(cipher, table, cfg, restart=r)
+        assert res.per_worker_scores == g["per_worker"][r].tolist()
+        assert res.best_score == g["best_score"][r]
+        assert np.array_equal(res.best_text, g["best_text"][r])
+
+
+def test_mas_random_batch_vs_oracle():
+    rng = np.random.default_rng(11)
+    ciphers = [rng.integers(0, 26, int(L)) for L in rng.integers(2, 700, 40)]
+    ciphers[0] = np.array([4, 4, 9])  # tiny
+    tables = [rng.integers(0, 900, 676), rng.integers(0, 65_536, 676), rng.integers(0, 10**9, 676)]
+    for table in tables:
+        n = 160
+        cof = rng.integers(0, len(ciphers), n).astype(np.int32)
+        seeds = rng.integers(0, 2**62, n)
+        streams = rng.integers(0, 2**40, n)
+        keys = philox_keys(seeds.tolist(), streams.tolist())
+        for early in (False, True):
+            res = engine.mas_climb(ciphers, cof, keys, table, 1500, early_exit=early)
+            want_s, want_m = O.mas_workers(ciphers, cof, seeds.tolist(), streams.tolist(), table,
+                                           1500)
+            assert res.scores.tolist() == want_s.tolist()
+            assert np.array_equal(res.keys.astype(np.int64), want_m)
+
+
+def test_mas_results_independent_of_device_split():
+    rng = np.random.default_rng(12)
+    ciphers = [rng.integers(0, 26, 300) for _ in range(3)]
+    table = rng.integers(0, 900, 676)
+    n = 96
+    keys = philox_keys([5], list(range(n)))
+    cof = np.repeat(np.arange(3), 32).astype(np.int32)
+    one = engine.mas_climb(ciphers, cof, keys, table, 2000, group_size=32)
+    two = engine.mas_climb(ciphers, cof, keys, table, 2000, group_size=32, devices_=[0, 0, 0])
+    assert np.array_equal(one.scores, two.scores)
+    assert np.array_equal(one.keys, two.keys)
+    assert np.array_equal(one.group_best, two.group_best)
+
+
+def test_restarts_stop_and_prefix(golden):
+    table = cc.BigramTable(np.random.default_rng(29).integers(0, 500, 676))
+    cipher = np.random.default_rng(30).integers(0, 26, 120)
+    short = cc.MasSolverConfig(workers=4, climbings=800, restarts=2, global_seed=3)
+    longer = cc.MasSolverConfig(workers=4, climbings=800, restarts=4, global_seed=3)
+    b1, r1 = cc.solve_with_restarts(cipher, table, short)
+    b2, r2 = cc.solve_with_restarts(cipher, table, longer)
+    assert [r.score for r in r2[:2]] == [r.score for r in r1]
+    assert b2.best_score >= b1.best_score
+    assert [r.restart for r in r2] == [0, 1, 2, 3]
+    _, runs = cc.solve_with_restarts(cipher, table, longer, stop=lambda r: True)
+    assert len(runs) == 1
+    # each restart equals the oracle's workers on streams (r << 32) | w
+    for r in range(4):
+        want, _ = O.mas_workers([cipher], np.zeros(4, np.int32), [3] * 4,
+                                [(r << 32) | w for w in range(4)], table.scores, 800)
+        assert r2[r].score == want.max()
+
+
+# ------------------------------------------------------------------ SCT
+def test_sct_score_batch_vs_oracle():
+    rng = np.random.default_rng(13)
+    logs = -rng.random(676) * 20 - 1
+    cases = []
+    for k in list(range(1, 41)) + [47, 63, 64]:
+        for n in (k, k + 1, 2 * k + 3, 7 * k + 5, 400, 596, 1024, 2049):
+            if n >= k:
+                cases.append((k, n))
+    for k, n in cases:
+        cipher = rng.integers(0, 26, n)
+        keys = np.array([rng.permutation(k) for _ in range(3)], dtype=np.uint8)
+        got = engine.sct_score_batch([cipher], np.zeros(3, np.int32), keys, logs)
+        want = [O.sct_score(cipher, logs, kk) for kk in keys]
+        assert got.tolist() == want, (k, n)
+
+
+def test_sct_worker_golden(golden):
+    for cipher, logs, k, climb, seed, stream, want_key, want_score in golden.sct_worker_cases():
+        cfg = cc.SctSolverConfig(key_length=k, climbings=climb, workers=1)
+        lt = cc.LogBigramTable(logs, float(np.min(logs)))
+        key, score = cc.sct_worker(cipher, lt, cfg, cc.WorkerRng(seed, stream))
+        assert np.array_equal(key, want_key), (k, cipher.size)
+        assert score == want_score
+
+
+def test_sct_solve_golden(golden):
+    g = golden.load("sct_solve")
+    cipher = g["cipher"].astype(np.int64)
+    logs = cc.LogBigramTable(golden.english_logs(), -24.0)
+    cfg = cc.SctSolverConfig(key_length=10, workers=64, climbings=15_000, restarts=1,
+                             global_seed=8000)
+    best, runs = cc.solve_sct(cipher, logs, cfg)
+    assert best.per_worker_scores == g["per_worker"].tolist()
+    assert np.array_equal(best.best_key, g["best_key"])
+    assert np.array_equal(best.best_text, g["best_text"])
+    assert best.best_score == float(g["best_score"])
+    assert len(runs) == 1
+
+
+def test_sct_random_workers_vs_oracle():
+    rng = np.random.default_rng(14)
+    logs = -rng.random(676) * 20 - 1
+    for k, n in [(2, 9), (3, 40), (5, 400), (8, 8), (12, 100), (20, 400), (31, 300), (33, 500),
+                 (40, 800), (64, 700), (7, 1500)]:
+        ciphers = [rng.integers(0, 26, n) for _ in range(2)]
+        m = 24
+        cof = (np.arange(m) % 2).astype(np.int32)
+        seeds = rng.integers(0, 2**62, m)
+        streams = rng.integers(0, 2**40, m)
+        p1, p2 = sorted(rng.integers(0, 101, 2).tolist())
+        h1, h2 = int(rng.integers(1, 5)), int(rng.integers(1, 5))
+        res = engine.sct_climb(ciphers, cof, philox_keys(seeds.tolist(), streams.tolist()), logs, k,
+                               400, p1=p1, p2=p2, op1_hop=h1, op2_hop=h2)
+        want_s, want_k = O.sct_workers(ciphers, cof, seeds.tolist(), streams.tolist(), logs, k, 400,
+                                       p1=p1, p2=p2, op1_hop=h1, op2_hop=h2)
+        assert res.scores.tolist() == want_s.tolist(), (k, n)
+        assert np.array_equal(res.keys.astype(np.int64), want_k), (k, n)
+
+
+def test_sct_end_to_end_small(golden):
+    plain = golden.plain_sct()[:80]
+    key = np.random.default_rng(52).permutation(4)
+    cipher = cc.sct_encrypt(plain, key)
+    logs = cc.LogBigramTable(golden.english_logs(), -24.0)
+    cfg = cc.SctSolverConfig(key_length=4, workers=8, climbings=2000, global_seed=12)
+    best, _ = cc.solve_sct(cipher, logs, cfg)
+    assert best.best_score >= O.log_score_text(plain, golden.english_logs())
+    assert np.array_equal(best.best_text, plain)
+
+
+# ------------------------------------------------------------------ acceptance-style end to end
+def test_mas_acceptance_07_shape(golden):
+    """tests/test_acceptance.py:146-167 (first 3 experiments): GPU run must reproduce the
+    oracle's restart-by-restart outcome and recover the plaintext."""
+    plain = golden.plain_mas(471)
+    table = cc.BigramTable(golden.english_scores())
+    ok = 0
+    for e in range(3):
+        key = O.permutation(700 + e, cc.KEYGEN_STREAM, 26)
+        cipher = key[plain]
+        cfg = cc.MasSolverConfig(workers=64, climbings=10_000, restarts=20, global_seed=7000 + e)
+        best, runs = cc.solve_with_restarts(cipher, table, cfg,
+                                            stop=lambda r: bool(np.array_equal(r.best_text, plain)))
+        ok += bool(np.array_equal(best.best_text, plain))
+        last = runs[-1].restart
+        want, _ = O.mas_workers([cipher], np.zeros(64, np.int32), [7000 + e] * 64,
+                                [(last << 32) | w for w in range(64)], table.scores, 10_000)
+        assert runs[-1].score == want.max()
+    assert ok >= 2
