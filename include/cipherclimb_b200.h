@@ -158,6 +158,9 @@ typedef struct {
 int ccg_sct_climb(ccg_ctx *ctx, const ccg_sct_climb_args *args);
 int ccg_sct_climb_dev(ccg_ctx *ctx, const ccg_sct_climb_args *args);
 
+/* Roofline denominator: measured shared-memory (LDS) bandwidth of this device, bytes/s. */
+int ccg_bench_smem_bandwidth(ccg_ctx *ctx, double *out_bytes_per_s);
+
 #ifdef __cplusplus
 }
 #endif

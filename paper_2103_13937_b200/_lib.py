@@ -80,6 +80,7 @@ EXPORTS = {
     "ccg_sct_score_batch": (C.c_int, [_P, _P, _P, _i64, _P, _P, _i32, _i64, _P, _P]),
     "ccg_sct_climb": (C.c_int, [_P, C.POINTER(SctClimbArgs)]),
     "ccg_sct_climb_dev": (C.c_int, [_P, C.POINTER(SctClimbArgs)]),
+    "ccg_bench_smem_bandwidth": (C.c_int, [_P, _P]),
 }
 
 _lib = None

@@ -532,6 +532,8 @@ static int check_climb_common(int64_t n_workers, int64_t climbings, int32_t grou
                               const void* scores, const void* keys, const void* cipher_of) {
   if (n_workers < 0) return fail(CCG_ERR_INVALID, "n_workers must be non-negative");
   if (climbings < 0) return fail(CCG_ERR_INVALID, "climbings must be non-negative");
+  if (climbings > 2147483647LL)
+    return fail(CCG_ERR_UNSUPPORTED, "climbings above 2^31-1 per call are not supported");
   if (n_workers > 0 && (!scores || !keys || !cipher_of))
     return fail(CCG_ERR_INVALID, "scores, keys and cipher_of are required");
   if (group_size < 0) return fail(CCG_ERR_INVALID, "group_size must be non-negative");
@@ -746,6 +748,16 @@ int ccg_sct_climb(ccg_ctx* ctx, const ccg_sct_climb_args* a) {
   if (a->tries_done && (rc = download(ctx, a->tries_done, d.tries_done, (size_t)nw * 8))) return rc;
   if (d.group_best && (rc = download(ctx, a->group_best, d.group_best, (size_t)ng * 8))) return rc;
   return finish(ctx, cudaSuccess, "sct_climb");
+}
+
+int ccg_bench_smem_bandwidth(ccg_ctx* ctx, double* out_bytes_per_s) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (!out_bytes_per_s) return fail(CCG_ERR_INVALID, "null out");
+  ctx->launches += 2;
+  cudaError_t e = bench_smem_bandwidth(ctx->stream, ctx->sm_count, out_bytes_per_s);
+  if (e != cudaSuccess) return cuda_fail(e, "smem bandwidth kernel");
+  return CCG_OK;
 }
 
 }  // extern "C"

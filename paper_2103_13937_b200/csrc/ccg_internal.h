@@ -99,4 +99,6 @@ cudaError_t launch_sct_score_long(cudaStream_t s, const uint8_t* ciphers, const 
 cudaError_t launch_sct_climb(cudaStream_t s, const SctLaunch& p, const SumPlan& plan,
                              int sm_count);
 
+cudaError_t bench_smem_bandwidth(cudaStream_t s, int sm_count, double* bytes_per_s);
+
 }  // namespace ccg

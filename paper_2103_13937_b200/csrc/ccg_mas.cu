@@ -36,35 +36,60 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kMasWarps = 8;  // warps (workers in flight) per block
 
-// 128 draws of one stream as letters int(u*26); lane L holds draws base+4L..base+4L+3.
+// 128 draws of one stream as letters int(u*26), 5 bits each.  Lane L holds the letters of
+// draws base+4L .. base+4L+7 (its own Philox block plus lane L+1's), so the next FOUR
+// letters -- two tries' pairs in the common no-redraw case -- come out of one 64-bit
+// shuffle.  Offsets are 32-bit; the Philox key is re-read from global memory at refill
+// time (keeps it out of registers).
 struct LetterWindow {
-  uint64_t k0, k1, base;
-  uint32_t packed;
+  const uint64_t* key;  // &keys[2*w] (global)
+  uint64_t base;        // stream index of window draw 0 (multiple of 4)
+  uint64_t packed;
+  uint32_t o;           // window offset of the next draw
 
-  __device__ __forceinline__ void refill(uint64_t pos, int lane) {
+  __device__ __forceinline__ void refill(int lane) {
+    const uint64_t pos = base + o;
     base = pos & ~3ULL;
+    o = (uint32_t)(pos & 3);
     uint64_t v0, v1, v2, v3;
-    philox4x64_10(k0, k1, (base >> 2) + 1 + (uint64_t)lane, v0, v1, v2, v3);
-    packed = int_below(v0, 26) | (int_below(v1, 26) << 8) | (int_below(v2, 26) << 16) |
-             (int_below(v3, 26) << 24);
+    philox4x64_10(__ldg(key), __ldg(key + 1), (base >> 2) + 1 + (uint64_t)lane, v0, v1, v2, v3);
+    const uint32_t p4 = int_below_small(v0, 26) | (int_below_small(v1, 26) << 5) |
+                        (int_below_small(v2, 26) << 10) | (int_below_small(v3, 26) << 15);
+    const uint32_t nxt = __shfl_down_sync(kFull, p4, 1);
+    packed = (uint64_t)p4 | ((uint64_t)nxt << 20);
   }
-  __device__ __forceinline__ uint32_t at(uint64_t pos) const {
-    const uint32_t o = (uint32_t)(pos - base);
-    return (__shfl_sync(kFull, packed, o >> 2) >> ((o & 3) * 8)) & 0xffu;
+  // letters of draws o .. o+3 in 5-bit fields; valid when o <= 124
+  __device__ __forceinline__ uint32_t peek4() const {
+    return (uint32_t)(shfl64(packed, (int)(o >> 2)) >> ((o & 3) * 5)) & 0xfffffu;
   }
-  __device__ __forceinline__ uint32_t next(uint64_t& pos, int lane) {
-    if (pos >= base + 128) refill(pos, lane);
-    return at(pos++);
+  __device__ __forceinline__ int next(int lane) {
+    if (o > 127) refill(lane);
+    const uint32_t w = (uint32_t)(shfl64(packed, (int)(o >> 2)) >> ((o & 3) * 5));
+    ++o;
+    return (int)(w & 31u);
   }
   // rng.py:81-89 next_distinct_pair(26)
-  __device__ __forceinline__ void pair(uint64_t& pos, int lane, int& a, int& b) {
-    if (pos + 2 > base + 128) refill(pos, lane);
-    a = (int)at(pos);
-    b = (int)at(pos + 1);
-    pos += 2;
-    while (b == a) b = (int)next(pos, lane);
+  __device__ __forceinline__ void pair(int lane, int& a, int& b) {
+    a = next(lane);
+    b = next(lane);
+    while (b == a) b = next(lane);
   }
+  __device__ __forceinline__ uint64_t position() const { return base + o; }
 };
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int lds_u16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return (int)v;
+}
 
 __device__ __forceinline__ int lo16(uint32_t v) { return (int)(v & 0xffffu); }
 __device__ __forceinline__ int hi16(uint32_t v) { return (int)(v >> 16); }
@@ -149,7 +174,7 @@ __device__ __forceinline__ void build_counts(uint32_t* C, const uint8_t* __restr
 }
 
 template <bool WIDE, bool EARLY>
-__global__ void __launch_bounds__(kMasWarps * 32)
+__global__ void __launch_bounds__(kMasWarps * 32, 4)
     mas_climb_kernel(const MasLaunch p) {
   __shared__ Tables<WIDE> tab;
   __shared__ uint32_t counts[kMasWarps][kAlpha * kRow];
@@ -159,6 +184,7 @@ __global__ void __launch_bounds__(kMasWarps * 32)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* C = counts[warp];
   const int64_t stride = (int64_t)gridDim.x * kMasWarps;
+  const uint32_t climbings = (uint32_t)p.climbings;
 
   for (int64_t w = (int64_t)blockIdx.x * kMasWarps + warp; w < p.n_workers; w += stride) {
     const int32_t cid = p.cipher_of[w];
@@ -174,51 +200,138 @@ __global__ void __launch_bounds__(kMasWarps * 32)
     int pv = lane < kAlpha ? lane : 0;  // pi(y)
     int inv = lane;                     // pi^-1(y)
     LetterWindow win;
-    win.k0 = p.keys[2 * w];
-    win.k1 = p.keys[2 * w + 1];
-    uint64_t pos = p.skips ? p.skips[w] : 0;
-    win.refill(pos, lane);
+    win.key = p.keys + 2 * w;
+    win.base = p.skips ? p.skips[w] : 0;
+    win.o = 0;
+    win.refill(lane);
 
-    int64_t last = -1, t = 0;
-    int since = 0, next_check = 256;
-    for (; t < p.climbings; ++t) {
-      int a, b;
-      win.pair(pos, lane, a, b);
-      const int xa = __shfl_sync(kFull, inv, a);
-      const int xb = __shfl_sync(kFull, inv, b);
-      const int64_t d = tab.delta(C, lane, pv, xa, xb, a, b);
-      if (d > 0) {
+    int last = -1;
+    uint32_t t = 0;
+    uint32_t since = 0, next_check = 256;
+    // exact local-optimum test over all 325 interchanges (CCG_FLAG_EARLY_EXIT)
+    auto improvable = [&]() {
+      for (int a2 = 0; a2 < kAlpha - 1; ++a2) {
+        const int x1 = __shfl_sync(kFull, inv, a2);
+        for (int b2 = a2 + 1; b2 < kAlpha; ++b2) {
+          const int x2 = __shfl_sync(kFull, inv, b2);
+          if (tab.delta(C, lane, pv, x1, x2, a2, b2) > 0) return true;
+        }
+      }
+      return false;
+    };
+    bool done = false;
+    if constexpr (!WIDE) {
+      // Fast path: two proposals per iteration.  Proposals never depend on the state
+      // (rng.py:81-89 draws only), so try t+1 is evaluated against the state before try t;
+      // if try t is accepted, try t+1 is re-evaluated against the new state.  Decisions
+      // are therefore exactly the sequential ones.
+      const uint32_t cl = smem_addr(&C[lane]);
+      const uint32_t ss0 = smem_addr(&tab.ss[0]);
+      uint32_t pofs = ss0 + 4u * (uint32_t)pv;
+      auto eval = [&](int a, int b, int xa, int xb) -> int {
+        const uint32_t ca = lds_u32(cl + 128u * (uint32_t)xa);
+        const uint32_t cb = lds_u32(cl + 128u * (uint32_t)xb);
+        const uint32_t sa = lds_u32(pofs + 128u * (uint32_t)a);
+        const uint32_t sb = lds_u32(pofs + 128u * (uint32_t)b);
+        const bool in_x = lane == xa || lane == xb;
+        const int p2 = lane == xa ? b : (lane == xb ? a : pv);
+        const uint32_t q2 = ss0 + 4u * (uint32_t)p2;
+        const int sa2 = lds_u16(q2 + 128u * (uint32_t)a);
+        const int sb2 = lds_u16(q2 + 128u * (uint32_t)b);
+        int v = lo16(ca) * (sb2 - lo16(sa)) + lo16(cb) * (sa2 - lo16(sb));
+        if (!in_x) v += (hi16(ca) - hi16(cb)) * (hi16(sb) - hi16(sa));
+        return __reduce_add_sync(kFull, v);
+      };
+      auto accept = [&](int a, int b, int xa, int xb, int d) {
         score += d;
         pv = lane == xa ? b : (lane == xb ? a : pv);
         inv = lane == a ? xb : (lane == b ? xa : inv);
-        last = t;
-        since = 0;
-        next_check = 256;
-      } else if (EARLY && ++since == next_check) {
-        // exact local-optimum test over all 325 interchanges
-        bool improvable = false;
-        for (int a2 = 0; a2 < kAlpha - 1 && !improvable; ++a2) {
-          const int x1 = __shfl_sync(kFull, inv, a2);
-          for (int b2 = a2 + 1; b2 < kAlpha; ++b2) {
-            const int x2 = __shfl_sync(kFull, inv, b2);
-            if (tab.delta(C, lane, pv, x1, x2, a2, b2) > 0) {
-              improvable = true;
-              break;
+        pofs = ss0 + 4u * (uint32_t)pv;
+      };
+      while (t < climbings && !done) {
+        int a1, b1, a2, b2;
+        bool two = false;
+        if (t + 1 < climbings) {
+          if (win.o > 124) win.refill(lane);
+          const uint32_t L4 = win.peek4();
+          a1 = (int)(L4 & 31u);
+          b1 = (int)((L4 >> 5) & 31u);
+          a2 = (int)((L4 >> 10) & 31u);
+          b2 = (int)((L4 >> 15) & 31u);
+          two = a1 != b1 && a2 != b2;
+        }
+        if (two) {
+          win.o += 4;
+          const int xa1 = __shfl_sync(kFull, inv, a1), xb1 = __shfl_sync(kFull, inv, b1);
+          const int xa2 = __shfl_sync(kFull, inv, a2), xb2 = __shfl_sync(kFull, inv, b2);
+          const int d1 = eval(a1, b1, xa1, xb1);
+          int d2 = eval(a2, b2, xa2, xb2);
+          if (d1 > 0) {
+            accept(a1, b1, xa1, xb1, d1);
+            last = (int)t;
+            const int ya = __shfl_sync(kFull, inv, a2), yb = __shfl_sync(kFull, inv, b2);
+            d2 = eval(a2, b2, ya, yb);
+            if (d2 > 0) {
+              accept(a2, b2, ya, yb, d2);
+              last = (int)t + 1;
             }
+          } else if (d2 > 0) {
+            accept(a2, b2, xa2, xb2, d2);
+            last = (int)t + 1;
           }
-        }
-        if (!improvable) {
+          t += 2;
+          if (EARLY) {
+            since = last >= (int)t - 2 ? (uint32_t)((int)t - 1 - last) : since + 2;
+            if (last >= (int)t - 2) next_check = 256;
+          }
+        } else {
+          int a, b;
+          win.pair(lane, a, b);
+          const int xa = __shfl_sync(kFull, inv, a), xb = __shfl_sync(kFull, inv, b);
+          const int d = eval(a, b, xa, xb);
+          if (d > 0) {
+            accept(a, b, xa, xb, d);
+            last = (int)t;
+            since = 0;
+            next_check = 256;
+          } else {
+            ++since;
+          }
           ++t;
-          break;
         }
-        next_check *= 4;
+        if (EARLY && since >= next_check) {
+          if (!improvable()) done = true;
+          next_check *= 4;
+        }
+      }
+    } else {
+      for (; t < climbings; ++t) {
+        int a, b;
+        win.pair(lane, a, b);
+        const int xa = __shfl_sync(kFull, inv, a);
+        const int xb = __shfl_sync(kFull, inv, b);
+        const int64_t d = tab.delta(C, lane, pv, xa, xb, a, b);
+        if (d > 0) {
+          score += d;
+          pv = lane == xa ? b : (lane == xb ? a : pv);
+          inv = lane == a ? xb : (lane == b ? xa : inv);
+          last = (int)t;
+          since = 0;
+          next_check = 256;
+        } else if (EARLY && ++since >= next_check) {
+          if (!improvable()) {
+            ++t;
+            break;
+          }
+          next_check *= 4;
+        }
       }
     }
 
     if (lane < kAlpha && p.maps) p.maps[w * kAlpha + lane] = (uint8_t)pv;
     if (lane == 0) {
       p.scores[w] = score;
-      if (p.draws_used) p.draws_used[w] = pos;
+      if (p.draws_used) p.draws_used[w] = win.position();
       if (p.last_accept) p.last_accept[w] = last;
       if (p.tries_done) p.tries_done[w] = t;
     }

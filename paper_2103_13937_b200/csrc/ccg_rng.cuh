@@ -61,6 +61,17 @@ __device__ __forceinline__ uint32_t int_below(uint64_t x, uint32_t bound) {
   return q;
 }
 
+// Same for 1 <= bound < 2^11, where m*bound < 2^64 needs no high product word.
+__device__ __forceinline__ uint32_t int_below_small(uint64_t x, uint32_t bound) {
+  const uint64_t P = (x >> 11) * (uint64_t)bound;
+  uint32_t q = (uint32_t)(P >> 53);
+  if (P >= (1ULL << 53)) {
+    const int s = (64 - __clzll(P)) - 53;
+    if ((1ULL << 53) - (P & ((1ULL << 53) - 1)) <= (1ULL << (s - 1))) ++q;
+  }
+  return q;
+}
+
 // u in [0,1) exactly as numpy: (x >> 11) * 2^-53.
 __device__ __forceinline__ double to_uniform(uint64_t x) {
   return (double)(x >> 11) * (1.0 / 9007199254740992.0);
