@@ -1,0 +1,198 @@
+"""CPU-only checks: the C-ABI library loads and exports its header, the host layer's
+reference semantics (key derivation, validation, table building, ciphers, restart fold),
+and that the product path fails loudly without a GPU (no CPU fallback)."""
+import re
+import ctypes
+import warnings
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2103_13937_b200 as cc
+from paper_2103_13937_b200 import _lib, engine
+from oracle import oracle as O
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def header_symbols():
+    text = (ROOT / "include" / "cipherclimb_b200.h").read_text()
+    return sorted(set(re.findall(r"\b(ccg_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    syms = header_symbols()
+    assert len(syms) >= 25
+    lib = ctypes.CDLL(str(_lib.LIB_PATH))
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    assert set(syms) == set(_lib.EXPORTS), set(syms) ^ set(_lib.EXPORTS)
+    assert _lib.load().ccg_abi_version() == _lib.ABI_VERSION
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", str(_lib.LIB_PATH)],
+                         capture_output=True, text=True).stdout
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
+
+
+def test_no_gpu_fails_loudly():
+    if _lib.device_count() > 0:
+        pytest.skip("a GPU is visible")
+    with pytest.raises(_lib.EngineError):
+        cc.solve_stochastic(np.array([0, 1, 2, 1]), cc.BigramTable(np.ones(676, np.int64)),
+                            cc.MasSolverConfig(workers=2, climbings=10))
+    with pytest.raises(_lib.EngineError):
+        cc.score_text(np.array([0, 1]), cc.BigramTable(np.ones(676, np.int64)))
+
+
+def test_philox_key_matches_numpy_conversion():
+    rng = np.random.default_rng(0)
+    vals = [0, 1, 2**53 + 1, 2**63 - 1, 2**63, 2**63 + 1025, 2**64 - 1, 2**64 - 1025, -1, -7,
+            (5 << 32) | 17, 2**32 - 2]
+    vals += [int(x) for x in rng.integers(0, 2**63, 10, dtype=np.uint64)]
+    for s in vals:
+        for w in vals:
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                k = np.asarray([s % 2**64, w % 2**64]).astype(np.uint64)
+            assert cc.philox_key(s, w) == (int(k[0]), int(k[1])) == O.reference_key(s, w)
+
+
+def test_stream_indices():
+    assert cc.worker_stream_index(3, 7) == (3 << 32) | 7
+    assert cc.pivot_stream_index(2) == (2 << 32) | (2**32 - 1)
+    with pytest.raises(ValueError):
+        cc.worker_stream_index(0, 2**32 - 2)
+    with pytest.raises(ValueError):
+        cc.worker_stream_index(-1, 0)
+    assert cc.uniform_to_int(0.999, 26) == 25
+    with pytest.raises(ValueError):
+        cc.uniform_to_int(0.5, 0)
+
+
+@pytest.mark.parametrize("n,shards,align", [(0, 3, 1), (1, 8, 1), (64, 8, 1), (100, 3, 1),
+                                            (640, 8, 64), (130, 4, 64), (7, 2, 5)])
+def test_shard_bounds(n, shards, align):
+    b = engine.shard_bounds(n, shards, align)
+    covered = [i for lo, hi in b for i in range(lo, hi)]
+    assert covered == list(range(n))
+    assert len(b) <= shards
+    for lo, hi in b[:-1]:
+        assert hi % align == 0
+    if b:
+        sizes = [hi - lo for lo, hi in b]
+        assert max(sizes) - min(sizes) <= align
+
+
+def test_configs_validate_like_reference():
+    with pytest.raises(ValueError, match="unknown mode"):
+        cc.MasSolverConfig(mode="x")
+    with pytest.raises(ValueError, match="workers=325"):
+        cc.MasSolverConfig(mode="deterministic", workers=64)
+    with pytest.raises(ValueError, match="climbings must be at least 1"):
+        cc.MasSolverConfig(climbings=0)
+    with pytest.raises(ValueError, match="key_length"):
+        cc.SctSolverConfig(key_length=1)
+    with pytest.raises(ValueError, match="thresholds"):
+        cc.SctSolverConfig(key_length=5, p1=70, p2=60)
+    with pytest.raises(ValueError, match="non-negative"):
+        cc.SctSolverConfig(key_length=5, climbings=-1)
+    cc.SctSolverConfig(key_length=5, climbings=0)
+    with pytest.raises(ValueError, match="two distinct letters"):
+        cc.solve_stochastic(np.array([3, 3, 3]), cc.BigramTable(np.ones(676, np.int64)),
+                            cc.MasSolverConfig())
+    with pytest.raises(ValueError, match="shorter than the key"):
+        cc.solve_sct(np.arange(5), cc.LogBigramTable(-np.ones(676), -2.0),
+                     cc.SctSolverConfig(key_length=10))
+
+
+def test_tables_from_corpus_match_reference(golden):
+    eng = golden.english_scores()
+    from paper_2103_13937_b200.codec import ALPHABET
+
+    corpus_text = "".join(ALPHABET[i] for i in golden.corpus())
+    t = cc.build_table_from_corpus(corpus_text)
+    assert np.array_equal(t.scores, eng)
+    logs = cc.build_log_table(t)
+    assert logs.logs.tolist() == golden.english_logs().tolist()  # bit-exact
+    text = cc.format_bigram_file(t)
+    assert np.array_equal(cc.parse_bigram_file(text).scores, eng)
+    with pytest.warns(UserWarning):
+        cc.parse_bigram_file("ab 3\nab 4\n")
+    for bad in ("ab", "abc 1", "aB 1", "ab x", "ab -1"):
+        with pytest.raises(ValueError):
+            cc.parse_bigram_file(bad)
+    with pytest.raises(ValueError):
+        cc.build_log_table(t, floor=-1.0)
+
+
+def test_codec():
+    assert cc.normalize("Always remember, that!") == "alwaysrememberthat"
+    assert cc.demap(cc.map_text("hello")) == "hello"
+    with pytest.raises(ValueError):
+        cc.map_text("Hello")
+    assert cc.demap(np.array([], dtype=np.int64)) == ""
+
+
+def test_pairs():
+    assert cc.index_to_pair(0) == (0, 1) and cc.index_to_pair(324) == (24, 25)
+    t = 0
+    for i in range(26):
+        for j in range(i + 1, 26):
+            assert cc.index_to_pair(t) == (i, j) and cc.pair_to_index(i, j) == t
+            t += 1
+
+
+def test_cipher_helpers_vs_oracle(golden):
+    for key, n, want in golden.gather_cases(O.permutation):
+        assert np.array_equal(cc.transposition_gather_map(key, n), want)
+    rng = np.random.default_rng(5)
+    for k in (2, 5, 10, 17):
+        for n in (k, 3 * k + 1, 100):
+            key = rng.permutation(k)
+            t = rng.integers(0, 26, n)
+            assert np.array_equal(cc.sct_decrypt(cc.sct_encrypt(t, key), key), t)
+            assert np.array_equal(cc.sct_decrypt(t, key), O.sct_decrypt(t, key))
+    mk = rng.permutation(26)
+    t = rng.integers(0, 26, 50)
+    assert np.array_equal(cc.mas_decrypt(cc.mas_encrypt(t, mk), mk), t)
+    assert np.array_equal(cc.apply_letter_swap(np.array([0, 1, 2]), 0, 2), [2, 1, 0])
+
+
+def test_select_operator():
+    Op = cc.Operator
+    assert cc.select_operator(10, 33, 66) is Op.ELEMENT_SWAP
+    assert cc.select_operator(33, 33, 66) is Op.BLOCK_SWAP
+    assert cc.select_operator(66, 33, 66) is Op.BLOCK_SHIFT
+    with pytest.raises(ValueError):
+        cc.select_operator(100, 33, 66)
+
+
+def test_max_element_and_restart_fold():
+    assert cc.max_element([4, 9, 9]) == (1, 9)
+    with pytest.raises(ValueError):
+        cc.max_element([])
+    from paper_2103_13937_b200.search import run_restarts
+
+    scores = [5, 7, 7, 3]
+
+    def solve_one(r):
+        return cc.SolveResult(np.array([r]), scores[r], [scores[r]], [])
+
+    best, runs = run_restarts(solve_one, 4)
+    assert best.restart_index == 1 and [r.restart for r in runs] == [0, 1, 2, 3]
+    best, runs = run_restarts(solve_one, 4, stop=lambda r: r.best_score == 7)
+    assert len(runs) == 2 and best.best_score == 7
+
+
+def test_bench_workload_keys_match_oracle():
+    import bench
+
+    for s in (100000, 100001, 100777):
+        assert np.array_equal(bench.reference_permutation(s, bench.KEYGEN_STREAM, 26),
+                              O.permutation(s, bench.KEYGEN_STREAM, 26))
