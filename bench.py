@@ -36,7 +36,8 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 KEYGEN_STREAM = 2**32 - 2
-EXEC_LDS_BYTES_PER_EVAL = 6 * 26 * 4   # executed: 6 packed-u32 LDS per active lane (ccg_mas.cu)
+EXEC_LDS_BYTES_PER_EVAL = 2 * 26 * 8 + 4  # executed: two LDS.64 rows per active lane + K(a,b)
+                                          # (ccg_mas_tform.cu)
 REF_LOOKUP_BYTES_PER_EVAL = 208 * 4    # reference-equivalent: 208 table lookups
 
 
@@ -403,7 +404,7 @@ def main():
             "e2e": e2e,
             "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
                          "frac": achieved / smem_peak, "traffic": traffic,
-                         "kernel": "mas_climb_kernel<false,false>",
+                         "kernel": "mas_climb_tform_kernel<false>",
                          "bytes_per_eval": EXEC_LDS_BYTES_PER_EVAL,
                          "peak_source": "measured on this GPU by ccg_bench_smem_bandwidth "
                                         "(128-bit conflict-free LDS, full occupancy)",

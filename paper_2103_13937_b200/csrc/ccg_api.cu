@@ -517,7 +517,9 @@ static int mas_launch(ccg_ctx* ctx, const ccg_mas_climb_args* a, int64_t max_len
   p.tries_done = a->tries_done;
   p.flags = a->flags;
   ctx->launches++;
-  cudaError_t e = launch_mas_climb(ctx->stream, p, mas_needs_wide(max_len, tmax), ctx->sm_count);
+  cudaError_t e = mas_tform_ok(max_len, tmax)
+                      ? launch_mas_climb_tform(ctx->stream, p, ctx->sm_count)
+                      : launch_mas_climb(ctx->stream, p, mas_needs_wide(max_len, tmax), ctx->sm_count);
   if (e != cudaSuccess) return cuda_fail(e, "mas_climb kernel");
   if (a->group_size > 0 && a->group_best) {
     ctx->launches++;

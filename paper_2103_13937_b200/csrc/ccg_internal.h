@@ -85,6 +85,9 @@ cudaError_t launch_mas_delta_counts(cudaStream_t s, const int64_t* counts, int64
                                     const int32_t* ab, const int64_t* table, bool wide,
                                     int64_t* out);
 cudaError_t launch_mas_climb(cudaStream_t s, const MasLaunch& p, bool wide, int sm_count);
+// T-form climb (ccg_mas_tform.cu): the fast path whenever mas_tform_ok(max_len, max(S)).
+bool mas_tform_ok(int64_t max_len, int64_t table_max);
+cudaError_t launch_mas_climb_tform(cudaStream_t s, const MasLaunch& p, int sm_count);
 cudaError_t launch_group_best_i64(cudaStream_t s, const int64_t* scores, int64_t n_groups,
                                   int32_t group_size, int64_t* out);
 cudaError_t launch_group_best_f64(cudaStream_t s, const double* scores, int64_t n_groups,

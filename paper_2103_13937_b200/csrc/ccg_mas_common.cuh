@@ -1,0 +1,76 @@
+// ccg_mas_common.cuh -- device helpers shared by the MAS climb kernels (ccg_mas.cu,
+// ccg_mas_tform.cu): the per-worker letter window over the numpy Philox stream
+// (rng.py:81-89 next_distinct_pair(26)) and raw shared-memory accessors.
+#pragma once
+#include "ccg_internal.h"
+#include "ccg_rng.cuh"
+
+namespace ccg {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// 128 draws of one stream as letters int(u*26), 5 bits each.  Lane L holds the letters of
+// draws base+4L .. base+4L+7 (its own Philox block plus lane L+1's), so the next FOUR
+// letters -- two tries' pairs in the common no-redraw case -- come out of one 64-bit
+// shuffle.  Offsets are 32-bit; the Philox key is re-read from global memory at refill
+// time (keeps it out of registers).
+struct LetterWindow {
+  const uint64_t* key;  // &keys[2*w] (global)
+  uint64_t base;        // stream index of window draw 0 (multiple of 4)
+  uint64_t packed;
+  uint32_t o;           // window offset of the next draw
+
+  __device__ __forceinline__ void refill(int lane) {
+    const uint64_t pos = base + o;
+    base = pos & ~3ULL;
+    o = (uint32_t)(pos & 3);
+    uint64_t v0, v1, v2, v3;
+    philox4x64_10(__ldg(key), __ldg(key + 1), (base >> 2) + 1 + (uint64_t)lane, v0, v1, v2, v3);
+    const uint32_t p4 = int_below_small(v0, 26) | (int_below_small(v1, 26) << 5) |
+                        (int_below_small(v2, 26) << 10) | (int_below_small(v3, 26) << 15);
+    const uint32_t nxt = __shfl_down_sync(kFull, p4, 1);
+    packed = (uint64_t)p4 | ((uint64_t)nxt << 20);
+  }
+  // letters of draws o .. o+3 in 5-bit fields; valid when o <= 124
+  __device__ __forceinline__ uint32_t peek4() const {
+    return (uint32_t)(shfl64(packed, (int)(o >> 2)) >> ((o & 3) * 5)) & 0xfffffu;
+  }
+  __device__ __forceinline__ int next(int lane) {
+    if (o > 127) refill(lane);
+    const uint32_t w = (uint32_t)(shfl64(packed, (int)(o >> 2)) >> ((o & 3) * 5));
+    ++o;
+    return (int)(w & 31u);
+  }
+  // rng.py:81-89 next_distinct_pair(26)
+  __device__ __forceinline__ void pair(int lane, int& a, int& b) {
+    a = next(lane);
+    b = next(lane);
+    while (b == a) b = next(lane);
+  }
+  __device__ __forceinline__ uint64_t position() const { return base + o; }
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int lds_u16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return (int)v;
+}
+
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint2 lds_u64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+
+}  // namespace ccg

@@ -198,6 +198,42 @@ def test_mas_random_batch_vs_oracle():
             assert np.array_equal(res.keys.astype(np.int64), want_m)
 
 
+@pytest.mark.parametrize("tmax", [900, 32_767, 32_768])
+def test_mas_budget_edges_and_bookkeeping(tmax):
+    """Odd and tiny budgets, stream skips, and the T-form gate (max S <= 32767) on both
+    sides: scores, maps, draw positions and last accepts equal the oracle's."""
+    rng = np.random.default_rng(tmax)
+    ciphers = [rng.integers(0, 26, int(L)) for L in (2, 3, 17, 160, 499)]
+    table = rng.integers(0, tmax + 1, 676)
+    table[int(rng.integers(676))] = tmax
+    for climb in (0, 1, 2, 3, 7, 255, 257, 1001):
+        for skip in (0, 5):
+            n = len(ciphers)
+            seeds, streams = [42] * n, [(3 << 32) | w for w in range(n)]
+            keys = philox_keys(seeds, streams)
+            res = engine.mas_climb(ciphers, np.arange(n, dtype=np.int32), keys, table, climb,
+                                   skips=np.full(n, skip, np.uint64), draws_used=True,
+                                   last_accept=True)
+            for w, c in enumerate(ciphers):
+                o_text, o_score, o_map, o_last = O.stochastic_worker(c, table, climb, seeds[w],
+                                                                     streams[w], skip=skip)
+                assert res.scores[w] == o_score, (climb, skip, w)
+                assert np.array_equal(res.keys[w].astype(np.int64)[c], o_text)
+                assert res.last_accept[w] == o_last
+                pairs_pos = skip
+                if climb:
+                    ints = (O.uniforms(seeds[w], streams[w], skip + 4 * climb + 64)[skip:] * 26)
+                    ints = ints.astype(int)
+                    pos = 0
+                    for _ in range(climb):
+                        a = ints[pos]; pos += 1
+                        b = ints[pos]; pos += 1
+                        while b == a:
+                            b = ints[pos]; pos += 1
+                    pairs_pos = skip + pos
+                assert int(res.draws_used[w]) == pairs_pos
+
+
 def test_mas_results_independent_of_device_split():
     rng = np.random.default_rng(12)
     ciphers = [rng.integers(0, 26, 300) for _ in range(3)]
