@@ -15,6 +15,9 @@
  *   ccg_mas_climb[_dev]                          mas.py:247-250 _stochastic_task -> mas.py:218-244
  *                                                stochastic_worker, for a whole run_worker_pool batch
  *                                                (mas.py:266-272) + search.py:19-25 max_element per group
+ *   ccg_mas_det_step_batch                       mas.py:84-120 deterministic_step (all 325 pair-worker scores)
+ *   ccg_mas_det_solve[_dev]                      mas.py:140-169 solve_deterministic, a batch of
+ *                                                (ciphertext, restart) jobs, whole loop on device
  *   ccg_sct_score_batch                          sct.py:158-160 candidate_score (ciphers.py:71-86,107-113)
  *   ccg_sct_climb[_dev]                          sct.py:173-176 _sct_task -> sct.py:148-170 sct_worker,
  *                                                for a whole batch (sct.py:194-200) + max_element
@@ -126,6 +129,36 @@ typedef struct {
 
 int ccg_mas_climb(ccg_ctx *ctx, const ccg_mas_climb_args *args);
 int ccg_mas_climb_dev(ccg_ctx *ctx, const ccg_mas_climb_args *args);
+
+/* mas.py:84-120 deterministic_step for a batch: text i with pivot (pivots[2i], pivots[2i+1])
+ * (distinct letters, both present in the text).  Writes the 325 pair-worker candidate scores of
+ * every text (out: int64[325 * n_texts], worker order of pairs.py:27-35; crosswise-excluded
+ * workers score 0).  The caller applies max_element (search.py:19-25). */
+int ccg_mas_det_step_batch(ccg_ctx *ctx, const uint8_t *texts, const int64_t *offsets,
+                           int64_t n_texts, const int32_t *pivots, const int64_t *table,
+                           int64_t *out);
+
+typedef struct {
+  const uint8_t *ciphers;     /* concatenated ciphertexts (each >= 2 distinct letters) */
+  const int64_t *offsets;     /* [n_ciphers + 1] */
+  int64_t n_ciphers;
+  const int32_t *cipher_of;   /* [n_jobs] cipher index of each job */
+  const uint64_t *keys;       /* [2 * n_jobs] Philox key of WorkerRng(seed, pivot_stream_index(r)) */
+  int64_t n_jobs;
+  int64_t iterations;         /* MasSolverConfig.iterations (mas.py:154) */
+  const int64_t *table;       /* [676] BigramTable.scores */
+  int64_t *scores;            /* [n_jobs] final score */
+  uint8_t *maps;              /* [26 * n_jobs] cipher letter -> plaintext letter, or NULL */
+  int32_t *hist_iter;         /* [iterations * n_jobs] accepted iteration numbers, or NULL */
+  int64_t *hist_score;        /* [iterations * n_jobs] score after each accept, or NULL */
+  int32_t *hist_len;          /* [n_jobs] number of accepts, or NULL */
+  uint64_t *draws_used;       /* [n_jobs] pivot draws consumed, or NULL */
+  int64_t max_len;            /* required by the _dev entry point only */
+  int64_t table_max;          /* required by the _dev entry point only */
+} ccg_mas_det_args;
+
+int ccg_mas_det_solve(ccg_ctx *ctx, const ccg_mas_det_args *args);
+int ccg_mas_det_solve_dev(ccg_ctx *ctx, const ccg_mas_det_args *args);
 
 /* sct.py:158-160: score of decrypting ciphers[cipher_of[i]] with keys[i*k:(i+1)*k]. */
 int ccg_sct_score_batch(ccg_ctx *ctx, const uint8_t *ciphers, const int64_t *offsets,

@@ -22,6 +22,8 @@
  *   ngrams.py:134-140 score_text;  ngrams.py:166-172 log_score_text (numpy pairwise sum)
  *   mas.py:172-178    bigram_count_matrix;  mas.py:181-210 swap_delta
  *   mas.py:218-244    stochastic_worker
+ *   mas.py:84-120     deterministic_step (325 pair-workers, full rescore, crosswise exclusion)
+ *   mas.py:133-169    _draw_present_letter / solve_deterministic (PIVOT stream, strict >)
  *   ciphers.py:71-86  transposition_gather_map;  ciphers.py:107-113 sct_decrypt
  *   sct.py:69-135     select_operator / apply_element_swaps / apply_block_swaps / apply_block_shift
  *   sct.py:148-170    sct_worker
@@ -227,6 +229,79 @@ int64_t cco_stochastic_worker(const int64_t *cipher, int64_t n, const int64_t *S
     if (out_text) for (int64_t i = 0; i < n; i++) out_text[i] = mapping[cipher[i]];
     if (out_map) for (int i = 0; i < ALPHA; i++) out_map[i] = mapping[i];
     if (out_last_accept) *out_last_accept = last;
+    return score;
+}
+
+/* ------------------------------------------------------------------ MAS deterministic */
+/* mas.py:84-120 deterministic_step: worker t = pair (L, R) (pairs.py:27-35, lexicographic)
+ * interchanges pivot pl with L, then pr with R (mas.py:75-81 _interchange_maps), and fully
+ * rescores the candidate text; crosswise-colliding workers (R == pl or L == pr) score 0.
+ * Writes all 325 scores; returns the first-max index (search.py:19-25). */
+int64_t cco_det_step(const int64_t *text, int64_t n, int64_t pl, int64_t pr, const int64_t *S,
+                     int64_t *scores, int64_t *cand) {
+    int64_t t = 0, best = 0;
+    for (int64_t L = 0; L < ALPHA; L++)
+        for (int64_t R = L + 1; R < ALPHA; R++, t++) {
+            if (R == pl || L == pr) { scores[t] = 0; }
+            else {
+                int64_t first[ALPHA], second[ALPHA], m[ALPHA];
+                for (int x = 0; x < ALPHA; x++) first[x] = second[x] = x;
+                first[pl] = L; first[L] = pl;
+                second[pr] = R; second[R] = pr;
+                for (int x = 0; x < ALPHA; x++) m[x] = second[first[x]];
+                int64_t s = 0;
+                for (int64_t i = 0; i + 1 < n; i++) s += S[ALPHA * m[text[i]] + m[text[i + 1]]];
+                scores[t] = s;
+            }
+            if (scores[t] > scores[best]) best = t;
+        }
+    if (cand) {
+        int64_t L = 0, R = 1, u = 0;
+        for (int64_t a = 0; a < ALPHA; a++)
+            for (int64_t b = a + 1; b < ALPHA; b++, u++)
+                if (u == best) { L = a; R = b; }
+        int64_t first[ALPHA], second[ALPHA];
+        for (int x = 0; x < ALPHA; x++) first[x] = second[x] = x;
+        first[pl] = L; first[L] = pl;
+        second[pr] = R; second[R] = pr;
+        for (int64_t i = 0; i < n; i++) cand[i] = second[first[text[i]]];
+    }
+    return best;
+}
+
+/* mas.py:133-137 */
+static int64_t draw_present(orng *g, const int *present, int64_t exclude) {
+    int64_t letter = orng_int_below(g, ALPHA);
+    while (!present[letter] || letter == exclude) letter = orng_int_below(g, ALPHA);
+    return letter;
+}
+
+/* mas.py:140-169 solve_deterministic on the PIVOT stream key (k0, k1).  Writes the final
+ * text, the history as (iteration, score) pairs (at most `iterations`), returns the score;
+ * *n_hist = number of accepted iterations. */
+int64_t cco_solve_deterministic(const int64_t *cipher, int64_t n, const int64_t *S,
+                                int64_t iterations, uint64_t k0, uint64_t k1,
+                                int64_t *out_text, int64_t *hist, int64_t *n_hist) {
+    orng g; orng_init(&g, k0, k1);
+    int64_t *text = out_text;
+    for (int64_t i = 0; i < n; i++) text[i] = cipher[i];
+    int64_t *cand = (int64_t *)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+    int64_t scores[325];
+    int64_t score = cco_score_text(text, n, S), nh = 0;
+    for (int64_t it = 1; it <= iterations; it++) {
+        int present[ALPHA] = {0};
+        for (int64_t i = 0; i < n; i++) present[text[i]] = 1;
+        int64_t pl = draw_present(&g, present, -1);
+        int64_t pr = draw_present(&g, present, pl);
+        int64_t best = cco_det_step(text, n, pl, pr, S, scores, cand);
+        if (scores[best] > score) {
+            memcpy(text, cand, sizeof(int64_t) * n);
+            score = scores[best];
+            hist[2 * nh] = it; hist[2 * nh + 1] = score; nh++;
+        }
+    }
+    free(cand);
+    *n_hist = nh;
     return score;
 }
 

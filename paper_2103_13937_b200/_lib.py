@@ -51,6 +51,15 @@ class SctClimbArgs(C.Structure):
     ]
 
 
+class MasDetArgs(C.Structure):
+    _fields_ = [
+        ("ciphers", _P), ("offsets", _P), ("n_ciphers", _i64), ("cipher_of", _P), ("keys", _P),
+        ("n_jobs", _i64), ("iterations", _i64), ("table", _P), ("scores", _P), ("maps", _P),
+        ("hist_iter", _P), ("hist_score", _P), ("hist_len", _P), ("draws_used", _P),
+        ("max_len", _i64), ("table_max", _i64),
+    ]
+
+
 EXPORTS = {
     # name: (restype, argtypes)
     "ccg_abi_version": (C.c_int, []),
@@ -77,6 +86,9 @@ EXPORTS = {
     "ccg_mas_delta_counts_batch": (C.c_int, [_P, _P, _i64, _P, _P, _P]),
     "ccg_mas_climb": (C.c_int, [_P, C.POINTER(MasClimbArgs)]),
     "ccg_mas_climb_dev": (C.c_int, [_P, C.POINTER(MasClimbArgs)]),
+    "ccg_mas_det_step_batch": (C.c_int, [_P, _P, _P, _i64, _P, _P, _P]),
+    "ccg_mas_det_solve": (C.c_int, [_P, C.POINTER(MasDetArgs)]),
+    "ccg_mas_det_solve_dev": (C.c_int, [_P, C.POINTER(MasDetArgs)]),
     "ccg_sct_score_batch": (C.c_int, [_P, _P, _P, _i64, _P, _P, _i32, _i64, _P, _P]),
     "ccg_sct_climb": (C.c_int, [_P, C.POINTER(SctClimbArgs)]),
     "ccg_sct_climb_dev": (C.c_int, [_P, C.POINTER(SctClimbArgs)]),

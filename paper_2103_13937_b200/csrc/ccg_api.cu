@@ -605,6 +605,139 @@ int ccg_mas_climb(ccg_ctx* ctx, const ccg_mas_climb_args* a) {
   return finish(ctx, cudaSuccess, "mas_climb");
 }
 
+// ------------------------------------------------------------------ MAS deterministic
+static int check_distinct_letters(const uint8_t* texts, const int64_t* offsets, int64_t i,
+                                  const char* what) {
+  uint32_t seen = 0;
+  for (int64_t q = offsets[i]; q < offsets[i + 1]; ++q) seen |= 1u << texts[q];
+  if (offsets[i + 1] - offsets[i] < 2 || __builtin_popcount(seen) < 2)
+    return fail(CCG_ERR_INVALID, "%s: ciphertext must contain at least two distinct letters", what);
+  return CCG_OK;
+}
+
+int ccg_mas_det_step_batch(ccg_ctx* ctx, const uint8_t* texts, const int64_t* offsets,
+                           int64_t n_texts, const int32_t* pivots, const int64_t* table,
+                           int64_t* out) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  int64_t max_len = 0, tmax = 0;
+  if ((rc = check_ragged(texts, offsets, n_texts, "det_step", &max_len))) return rc;
+  if ((rc = check_table(table, &tmax))) return rc;
+  if (n_texts == 0) return CCG_OK;
+  if (!pivots || !out) return fail(CCG_ERR_INVALID, "null argument");
+  for (int64_t i = 0; i < n_texts; ++i) {
+    const int pl = pivots[2 * i], pr = pivots[2 * i + 1];
+    if (pl < 0 || pl >= kAlpha || pr < 0 || pr >= kAlpha)
+      return fail(CCG_ERR_INVALID, "pivot %lld: letters must lie in 0..25", (long long)i);
+    if (pl == pr) return fail(CCG_ERR_INVALID, "pivot letters must differ");
+    bool hl = false, hr = false;
+    for (int64_t q = offsets[i]; q < offsets[i + 1]; ++q) {
+      hl |= texts[q] == pl;
+      hr |= texts[q] == pr;
+    }
+    if (!(hl && hr)) return fail(CCG_ERR_INVALID, "both pivot letters must occur in the text");
+  }
+  void *dt, *doff, *dpiv, *dtab, *dout;
+  if ((rc = upload(ctx, 0, texts, (size_t)offsets[n_texts], &dt))) return rc;
+  if ((rc = upload(ctx, 1, offsets, (size_t)(n_texts + 1) * 8, &doff))) return rc;
+  if ((rc = upload(ctx, 2, pivots, (size_t)n_texts * 8, &dpiv))) return rc;
+  if ((rc = upload(ctx, 3, table, kAlpha * kAlpha * 8, &dtab))) return rc;
+  if ((rc = ctx->buf(4, (size_t)n_texts * 325 * 8, &dout))) return rc;
+  ctx->launches++;
+  cudaError_t e = launch_mas_det_step(ctx->stream, (const uint8_t*)dt, (const int64_t*)doff, n_texts,
+                                      (const int32_t*)dpiv, (const int64_t*)dtab,
+                                      mas_needs_wide(max_len, tmax), (int64_t*)dout);
+  if (e != cudaSuccess) return cuda_fail(e, "det_step kernel");
+  if ((rc = download(ctx, out, dout, (size_t)n_texts * 325 * 8))) return rc;
+  return finish(ctx, cudaSuccess, "det_step");
+}
+
+static int det_launch(ccg_ctx* ctx, const ccg_mas_det_args* a, int64_t max_len, int64_t tmax) {
+  MasDetLaunch p;
+  p.ciphers = a->ciphers;
+  p.offsets = a->offsets;
+  p.cipher_of = a->cipher_of;
+  p.keys = a->keys;
+  p.n_jobs = a->n_jobs;
+  p.iterations = a->iterations;
+  p.table = a->table;
+  p.scores = a->scores;
+  p.maps = a->maps;
+  p.hist_iter = a->hist_iter;
+  p.hist_score = a->hist_score;
+  p.hist_len = a->hist_len;
+  p.draws_used = a->draws_used;
+  ctx->launches++;
+  cudaError_t e = launch_mas_det_solve(ctx->stream, p, mas_needs_wide(max_len, tmax));
+  if (e != cudaSuccess) return cuda_fail(e, "det_solve kernel");
+  return CCG_OK;
+}
+
+static int check_det_common(const ccg_mas_det_args* a) {
+  if (!a) return fail(CCG_ERR_INVALID, "null args");
+  if (a->n_jobs < 0) return fail(CCG_ERR_INVALID, "n_jobs must be non-negative");
+  if (a->iterations < 0) return fail(CCG_ERR_INVALID, "iterations must be non-negative");
+  if (a->iterations > 2147483647LL)
+    return fail(CCG_ERR_UNSUPPORTED, "iterations above 2^31-1 per call are not supported");
+  if (a->n_jobs > 2147483647LL) return fail(CCG_ERR_UNSUPPORTED, "too many jobs in one call");
+  if (a->n_jobs > 0 && (!a->scores || !a->keys || !a->cipher_of))
+    return fail(CCG_ERR_INVALID, "scores, keys and cipher_of are required");
+  if ((a->hist_iter || a->hist_score) && !a->hist_len)
+    return fail(CCG_ERR_INVALID, "hist_len is required with a history buffer");
+  return CCG_OK;
+}
+
+int ccg_mas_det_solve_dev(ccg_ctx* ctx, const ccg_mas_det_args* a) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if ((rc = check_det_common(a))) return rc;
+  if (a->table_max < 0) return fail(CCG_ERR_INVALID, "table_max must be set");
+  return det_launch(ctx, a, a->max_len, a->table_max);
+}
+
+int ccg_mas_det_solve(ccg_ctx* ctx, const ccg_mas_det_args* a) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if ((rc = check_det_common(a))) return rc;
+  int64_t max_len = 0, tmax = 0;
+  if ((rc = check_ragged(a->ciphers, a->offsets, a->n_ciphers, "mas_det_solve", &max_len))) return rc;
+  if ((rc = check_table(a->table, &tmax))) return rc;
+  const int64_t nj = a->n_jobs, it = a->iterations;
+  if (nj == 0) return CCG_OK;
+  for (int64_t i = 0; i < nj; ++i)
+    if (a->cipher_of[i] < 0 || a->cipher_of[i] >= a->n_ciphers)
+      return fail(CCG_ERR_INVALID, "cipher_of[%lld] out of range", (long long)i);
+  for (int64_t c = 0; c < a->n_ciphers; ++c)
+    if ((rc = check_distinct_letters(a->ciphers, a->offsets, c, "mas_det_solve"))) return rc;
+  ccg_mas_det_args d = *a;
+  void* p;
+  if ((rc = upload(ctx, 0, a->ciphers, (size_t)a->offsets[a->n_ciphers], &p))) return rc;
+  d.ciphers = (const uint8_t*)p;
+  if ((rc = upload(ctx, 1, a->offsets, (size_t)(a->n_ciphers + 1) * 8, &p))) return rc;
+  d.offsets = (const int64_t*)p;
+  if ((rc = upload(ctx, 2, a->cipher_of, (size_t)nj * 4, &p))) return rc;
+  d.cipher_of = (const int32_t*)p;
+  if ((rc = upload(ctx, 3, a->keys, (size_t)nj * 16, &p))) return rc;
+  d.keys = (const uint64_t*)p;
+  if ((rc = upload(ctx, 4, a->table, kAlpha * kAlpha * 8, &p))) return rc;
+  d.table = (const int64_t*)p;
+  if ((rc = ctx->buf(5, (size_t)nj * 8, &p))) return rc;
+  d.scores = (int64_t*)p;
+  if (a->maps) { if ((rc = ctx->buf(6, (size_t)nj * kAlpha, &p))) return rc; d.maps = (uint8_t*)p; }
+  if (a->hist_iter) { if ((rc = ctx->buf(7, (size_t)nj * it * 4, &p))) return rc; d.hist_iter = (int32_t*)p; }
+  if (a->hist_score) { if ((rc = ctx->buf(8, (size_t)nj * it * 8, &p))) return rc; d.hist_score = (int64_t*)p; }
+  if (a->hist_len) { if ((rc = ctx->buf(9, (size_t)nj * 4, &p))) return rc; d.hist_len = (int32_t*)p; }
+  if (a->draws_used) { if ((rc = ctx->buf(10, (size_t)nj * 8, &p))) return rc; d.draws_used = (uint64_t*)p; }
+  if ((rc = det_launch(ctx, &d, max_len, tmax))) return rc;
+  if ((rc = download(ctx, a->scores, d.scores, (size_t)nj * 8))) return rc;
+  if (a->maps && (rc = download(ctx, a->maps, d.maps, (size_t)nj * kAlpha))) return rc;
+  if (a->hist_iter && (rc = download(ctx, a->hist_iter, d.hist_iter, (size_t)nj * it * 4))) return rc;
+  if (a->hist_score && (rc = download(ctx, a->hist_score, d.hist_score, (size_t)nj * it * 8))) return rc;
+  if (a->hist_len && (rc = download(ctx, a->hist_len, d.hist_len, (size_t)nj * 4))) return rc;
+  if (a->draws_used && (rc = download(ctx, a->draws_used, d.draws_used, (size_t)nj * 8))) return rc;
+  return finish(ctx, cudaSuccess, "mas_det_solve");
+}
+
 // ------------------------------------------------------------------ SCT
 int ccg_sct_score_batch(ccg_ctx* ctx, const uint8_t* ciphers, const int64_t* offsets,
                         int64_t n_ciphers, const int32_t* cipher_of, const uint8_t* keys,

@@ -35,6 +35,23 @@ struct MasLaunch {
   uint32_t flags;
 };
 
+// Deterministic best-neighbour MAS (ccg_mas_det.cu): one job = one (ciphertext, restart).
+struct MasDetLaunch {
+  const uint8_t* ciphers;
+  const int64_t* offsets;
+  const int32_t* cipher_of;
+  const uint64_t* keys;  // PIVOT-stream Philox key per job
+  int64_t n_jobs;
+  int64_t iterations;
+  const int64_t* table;
+  int64_t* scores;
+  uint8_t* maps;
+  int32_t* hist_iter;
+  int64_t* hist_score;
+  int32_t* hist_len;
+  uint64_t* draws_used;
+};
+
 // numpy pairwise-sum plan for the (n-1) bigram terms of an n-letter text
 // (numpy/_core/src/umath/loops_utils.h.src pairwise_sum): leaves in order, and the
 // post-order list of leaf merges (dst += src) that reproduces the recursion.
@@ -88,6 +105,10 @@ cudaError_t launch_mas_climb(cudaStream_t s, const MasLaunch& p, bool wide, int 
 // T-form climb (ccg_mas_tform.cu): the fast path whenever mas_tform_ok(max_len, max(S)).
 bool mas_tform_ok(int64_t max_len, int64_t table_max);
 cudaError_t launch_mas_climb_tform(cudaStream_t s, const MasLaunch& p, int sm_count);
+cudaError_t launch_mas_det_step(cudaStream_t s, const uint8_t* texts, const int64_t* offsets,
+                                int64_t n, const int32_t* pivots, const int64_t* table, bool wide,
+                                int64_t* out);
+cudaError_t launch_mas_det_solve(cudaStream_t s, const MasDetLaunch& p, bool wide);
 cudaError_t launch_group_best_i64(cudaStream_t s, const int64_t* scores, int64_t n_groups,
                                   int32_t group_size, int64_t* out);
 cudaError_t launch_group_best_f64(cudaStream_t s, const double* scores, int64_t n_groups,

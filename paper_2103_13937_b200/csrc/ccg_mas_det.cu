@@ -1,0 +1,297 @@
+// ccg_mas_det.cu -- the deterministic best-neighbour MAS climb on the GPU
+// (reference mas.py:84-169: deterministic_step, climb, _draw_present_letter,
+// solve_deterministic; pairs.py:27-35 for the worker <-> letter-pair numbering).
+//
+// Layout: one CTA per job (a ciphertext x restart), 352 threads; thread t < 325 is the
+// reference's pair-worker t = (L, R) (lexicographic, pairs.py).  The whole 500-iteration
+// loop stays on the device -- the per-iteration host round trip that the paper names as
+// its first bottleneck is gone.
+//
+// State: the bigram-count matrix T of the CURRENT plaintext (int32, 26x26, shared) and the
+// score table S (shared, in the accumulator type).  Worker t's candidate applies the letter
+// map m = (pr R) o (pl L) (mas.py:75-81) to the text; its score is computed exactly as the
+// current score plus
+//     sum_{u in D} sum_v T[u][v] (S[m u][m v] - S[u][v])
+//   + sum_{u not in D} sum_{v in D} T[u][v] (S[u][m v] - S[u][v]),   D = {pl, L, pr, R},
+// which equals the reference's full rescore (mas.py:114-116) as an integer.  Crosswise
+// workers (R == pl or L == pr) score 0 (mas.py:117); the best is the FIRST maximum
+// (search.py:19-25), accepted iff strictly greater (mas.py:161).
+//
+// Pivot draws (mas.py:133-137, 155-158) come from the PIVOT stream on thread 0 (scalar
+// numpy-exact Philox, ccg_rng.cuh); the letters present in the current text are a 26-bit
+// mask that is permuted with the text on every accept.
+#include "ccg_internal.h"
+#include "ccg_rng.cuh"
+
+namespace ccg {
+namespace {
+
+constexpr int kDetThreads = 352;  // 11 warps: 325 pair-workers + idle lanes
+constexpr int kPairs = 325;
+
+// pair index t -> (L, R), L < R, lexicographic (pairs.py:27-35)
+__device__ __forceinline__ void pair_of(int t, int& L, int& R) {
+  int l = 0, rem = t;
+  while (rem >= kAlpha - 1 - l) {
+    rem -= kAlpha - 1 - l;
+    ++l;
+  }
+  L = l;
+  R = l + 1 + rem;
+}
+
+// m = second o first: first swaps pl<->L, second swaps pr<->R (mas.py:75-81)
+struct LetterMap {
+  int pl, L, pr, R;
+  __device__ __forceinline__ int operator()(int x) const {
+    const int y = x == pl ? L : (x == L ? pl : x);
+    return y == pr ? R : (y == R ? pr : y);
+  }
+};
+
+// Exact score change of applying m to the text whose bigram counts are T.
+template <typename Acc>
+__device__ Acc candidate_delta(const int* T, const Acc* S, const LetterMap& m) {
+  int d[4];
+  int nd = 0;
+  const int cand[4] = {m.pl, m.L, m.pr, m.R};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    bool dup = false;
+    for (int j = 0; j < nd; ++j) dup |= d[j] == cand[i];
+    if (!dup) d[nd++] = cand[i];
+  }
+  auto inD = [&](int x) {
+    bool r = false;
+    for (int j = 0; j < nd; ++j) r |= d[j] == x;
+    return r;
+  };
+  Acc acc = 0;
+  for (int j = 0; j < nd; ++j) {
+    const int u = d[j], mu = m(u);
+    for (int v = 0; v < kAlpha; ++v) {
+      const int t = T[u * kAlpha + v];
+      if (t) acc += (Acc)t * (S[mu * kAlpha + m(v)] - S[u * kAlpha + v]);
+    }
+  }
+  for (int j = 0; j < nd; ++j) {
+    const int v = d[j], mv = m(v);
+    if (mv == v) continue;
+    for (int u = 0; u < kAlpha; ++u) {
+      if (inD(u)) continue;
+      const int t = T[u * kAlpha + v];
+      if (t) acc += (Acc)t * (S[u * kAlpha + mv] - S[u * kAlpha + v]);
+    }
+  }
+  return acc;
+}
+
+// (value, index) first-max over the block; every thread gets the result.
+template <typename Acc>
+__device__ __forceinline__ void block_first_max(Acc v, int idx, Acc* sv, int* si, Acc& out_v,
+                                                int& out_i) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const Acc ov = __shfl_down_sync(0xffffffffu, v, o);
+    const int oi = __shfl_down_sync(0xffffffffu, idx, o);
+    if (ov > v || (ov == v && oi < idx)) {
+      v = ov;
+      idx = oi;
+    }
+  }
+  if (lane == 0) {
+    sv[warp] = v;
+    si[warp] = idx;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < kDetThreads / 32 ? sv[lane] : (Acc)(-1);
+    idx = lane < kDetThreads / 32 ? si[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const Acc ov = __shfl_down_sync(0xffffffffu, v, o);
+      const int oi = __shfl_down_sync(0xffffffffu, idx, o);
+      if (ov > v || (ov == v && oi < idx)) {
+        v = ov;
+        idx = oi;
+      }
+    }
+    if (lane == 0) {
+      sv[0] = v;
+      si[0] = idx;
+    }
+  }
+  __syncthreads();
+  out_v = sv[0];
+  out_i = si[0];
+  __syncthreads();
+}
+
+template <typename Acc>
+struct DetShared {
+  Acc S[kAlpha * kAlpha];
+  int T[kAlpha * kAlpha];
+  Acc red_v[kDetThreads / 32];
+  int red_i[kDetThreads / 32];
+  uint8_t map[32];
+  int pivot[2];
+  uint32_t present;
+};
+
+// T = bigram counts of text[0..n), S = table; returns the score (thread-uniform).
+template <typename Acc>
+__device__ Acc load_state(DetShared<Acc>& sh, const uint8_t* text, int64_t n, const int64_t* table) {
+  for (int i = threadIdx.x; i < kAlpha * kAlpha; i += blockDim.x) {
+    sh.S[i] = (Acc)table[i];
+    sh.T[i] = 0;
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i + 1 < n; i += blockDim.x)
+    atomicAdd(&sh.T[text[i] * kAlpha + text[i + 1]], 1);
+  __syncthreads();
+  Acc part = 0;
+  for (int i = threadIdx.x; i < kAlpha * kAlpha; i += blockDim.x) part += (Acc)sh.T[i] * sh.S[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
+  if ((threadIdx.x & 31) == 0) sh.red_v[threadIdx.x >> 5] = part;
+  __syncthreads();
+  Acc total = 0;
+  for (int w = 0; w < kDetThreads / 32; ++w) total += sh.red_v[w];
+  __syncthreads();
+  return total;
+}
+
+// mas.py:84-120 for a batch of (text, pivot): all 325 candidate scores per text.
+template <typename Acc>
+__global__ void __launch_bounds__(kDetThreads) det_step_kernel(const uint8_t* texts,
+                                                               const int64_t* offsets,
+                                                               const int32_t* pivots,
+                                                               const int64_t* table,
+                                                               int64_t* out) {
+  __shared__ DetShared<Acc> sh;
+  const int64_t j = blockIdx.x;
+  const int64_t off = offsets[j], n = offsets[j + 1] - off;
+  const Acc score = load_state(sh, texts + off, n, table);
+  const int t = threadIdx.x;
+  if (t < kPairs) {
+    int L, R;
+    pair_of(t, L, R);
+    const int pl = pivots[2 * j], pr = pivots[2 * j + 1];
+    Acc c = 0;
+    if (!(R == pl || L == pr)) c = score + candidate_delta(sh.T, sh.S, LetterMap{pl, L, pr, R});
+    out[j * kPairs + t] = (int64_t)c;
+  }
+}
+
+// mas.py:140-169 solve_deterministic, one job per CTA.
+template <typename Acc>
+__global__ void __launch_bounds__(kDetThreads) det_solve_kernel(const MasDetLaunch p) {
+  __shared__ DetShared<Acc> sh;
+  const int64_t job = blockIdx.x;
+  const int32_t cid = p.cipher_of[job];
+  const int64_t off = p.offsets[cid], n = p.offsets[cid + 1] - off;
+  const uint8_t* text = p.ciphers + off;
+  Acc score = load_state(sh, text, n, p.table);
+  const int t = threadIdx.x;
+  if (t < 32) sh.map[t] = (uint8_t)t;
+  if (t == 0) {
+    uint32_t pres = 0;
+    for (int i = 0; i < kAlpha * kAlpha; ++i)
+      if (sh.T[i]) pres |= (1u << (i / kAlpha)) | (1u << (i % kAlpha));
+    if (n == 1) pres = 1u << text[0];
+    sh.present = pres;
+  }
+  int L = 0, R = 1;
+  if (t < kPairs) pair_of(t, L, R);
+
+  // thread 0's PIVOT-stream state (scalar Philox, numpy order)
+  const uint64_t k0 = p.keys[2 * job], k1 = p.keys[2 * job + 1];
+  uint64_t blk[4] = {0, 0, 0, 0};
+  uint64_t drawn = 0;  // draws consumed
+  auto next26 = [&]() -> int {
+    if ((drawn & 3) == 0) philox4x64_10(k0, k1, (drawn >> 2) + 1, blk[0], blk[1], blk[2], blk[3]);
+    const uint64_t x = blk[drawn & 3];
+    ++drawn;
+    return (int)int_below_small(x, kAlpha);
+  };
+  int32_t nh = 0;
+  __syncthreads();
+  for (int64_t it = 1; it <= p.iterations; ++it) {
+    if (t == 0) {  // mas.py:155-158 via _draw_present_letter (mas.py:133-137)
+      const uint32_t pres = sh.present;
+      int pl = next26();
+      while (!((pres >> pl) & 1u)) pl = next26();
+      int pr = next26();
+      while (!((pres >> pr) & 1u) || pr == pl) pr = next26();
+      sh.pivot[0] = pl;
+      sh.pivot[1] = pr;
+    }
+    __syncthreads();
+    const int pl = sh.pivot[0], pr = sh.pivot[1];
+    Acc c = (Acc)(-1);
+    if (t < kPairs) {
+      c = 0;
+      if (!(R == pl || L == pr)) c = score + candidate_delta(sh.T, sh.S, LetterMap{pl, L, pr, R});
+    }
+    Acc best;
+    int bi;
+    block_first_max(c, t, sh.red_v, sh.red_i, best, bi);
+    if (best > score) {  // mas.py:160-164: climb(text, best_index, pivot)
+      int bL, bR;
+      pair_of(bi, bL, bR);
+      const LetterMap m{pl, bL, pr, bR};
+      int v0 = 0, v1 = 0;
+      const int e0 = t, e1 = t + kDetThreads;
+      if (e0 < kAlpha * kAlpha) v0 = sh.T[e0];
+      if (e1 < kAlpha * kAlpha) v1 = sh.T[e1];
+      uint8_t mp = 0;
+      if (t < kAlpha) mp = sh.map[t];
+      __syncthreads();
+      if (e0 < kAlpha * kAlpha) sh.T[m(e0 / kAlpha) * kAlpha + m(e0 % kAlpha)] = v0;
+      if (e1 < kAlpha * kAlpha) sh.T[m(e1 / kAlpha) * kAlpha + m(e1 % kAlpha)] = v1;
+      if (t < kAlpha) sh.map[t] = (uint8_t)m(mp);
+      if (t == 0) {
+        uint32_t np = 0;
+        for (int y = 0; y < kAlpha; ++y)
+          if ((sh.present >> y) & 1u) np |= 1u << m(y);
+        sh.present = np;
+        if (p.hist_iter) p.hist_iter[job * p.iterations + nh] = (int32_t)it;
+        if (p.hist_score) p.hist_score[job * p.iterations + nh] = (int64_t)best;
+      }
+      score = best;
+      ++nh;
+      __syncthreads();
+    }
+  }
+  if (t < kAlpha && p.maps) p.maps[job * kAlpha + t] = sh.map[t];
+  if (t == 0) {
+    p.scores[job] = (int64_t)score;
+    if (p.hist_len) p.hist_len[job] = nh;
+    if (p.draws_used) p.draws_used[job] = drawn;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_mas_det_step(cudaStream_t s, const uint8_t* texts, const int64_t* offsets,
+                                int64_t n, const int32_t* pivots, const int64_t* table, bool wide,
+                                int64_t* out) {
+  if (n <= 0) return cudaSuccess;
+  if (wide)
+    det_step_kernel<long long><<<(unsigned)n, kDetThreads, 0, s>>>(texts, offsets, pivots, table, out);
+  else
+    det_step_kernel<int><<<(unsigned)n, kDetThreads, 0, s>>>(texts, offsets, pivots, table, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mas_det_solve(cudaStream_t s, const MasDetLaunch& p, bool wide) {
+  if (p.n_jobs <= 0) return cudaSuccess;
+  if (wide)
+    det_solve_kernel<long long><<<(unsigned)p.n_jobs, kDetThreads, 0, s>>>(p);
+  else
+    det_solve_kernel<int><<<(unsigned)p.n_jobs, kDetThreads, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace ccg

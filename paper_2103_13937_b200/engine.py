@@ -247,3 +247,73 @@ def sct_score_batch(ciphers, cipher_of, keys, logs) -> np.ndarray:
                                                    kk.shape[1], cof.size, _lib.ptr(lg),
                                                    _lib.ptr(out)), "sct_score")
     return out
+
+
+def mas_det_step_batch(texts, pivots, table_scores) -> np.ndarray:
+    """All 325 pair-worker scores of deterministic_step (mas.py:84-120) for many
+    (text, pivot) on the GPU: int64[n, 325]."""
+    flat, off = _lib.ragged(texts)
+    pv = np.ascontiguousarray(pivots, dtype=np.int32).reshape(-1, 2)
+    table = np.ascontiguousarray(table_scores, dtype=np.int64)
+    out = np.empty((off.size - 1, 325), dtype=np.int64)
+    ctx = _lib.context(default_device())
+    with ctx.lock:
+        _lib.check(_lib.load().ccg_mas_det_step_batch(ctx.handle, _lib.ptr(flat), _lib.ptr(off),
+                                                      off.size - 1, _lib.ptr(pv), _lib.ptr(table),
+                                                      _lib.ptr(out)), "det_step")
+    return out
+
+
+@dataclass
+class DetResult:
+    scores: np.ndarray          # int64 per job
+    maps: np.ndarray            # uint8[n, 26] cipher letter -> plaintext letter
+    history: list               # per job: [(iteration, score), ...]
+    draws_used: np.ndarray
+    launches: int
+
+
+def mas_det_solve(ciphers, cipher_of, keys, table_scores, iterations, *, devices_=None) -> DetResult:
+    """solve_deterministic (mas.py:140-169) for a batch of jobs, one CTA each, the whole
+    iteration loop on the device.  keys: uint64[n, 2] PIVOT-stream Philox keys."""
+    flat, off = _lib.ragged(ciphers)
+    cof = np.ascontiguousarray(cipher_of, dtype=np.int32).reshape(-1)
+    keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, 2)
+    table = np.ascontiguousarray(table_scores, dtype=np.int64)
+    n, it = cof.size, int(iterations)
+    if keys.shape[0] != n:
+        raise ValueError("one Philox key per job required")
+    devs = devices_ or devices()
+
+    def run(dev, lo, hi):
+        m = hi - lo
+        out = DetResult(scores=np.empty(m, dtype=np.int64), maps=np.empty((m, 26), dtype=np.uint8),
+                        history=[], draws_used=np.empty(m, dtype=np.uint64), launches=0)
+        if m == 0:
+            return out
+        hi_it = np.empty((m, max(1, it)), dtype=np.int32)
+        hi_sc = np.empty((m, max(1, it)), dtype=np.int64)
+        hl = np.empty(m, dtype=np.int32)
+        c_of = np.ascontiguousarray(cof[lo:hi])
+        k = np.ascontiguousarray(keys[lo:hi])
+        a = _lib.MasDetArgs()
+        a.ciphers, a.offsets, a.n_ciphers = _lib.ptr(flat), _lib.ptr(off), off.size - 1
+        a.cipher_of, a.keys, a.n_jobs, a.iterations = _lib.ptr(c_of), _lib.ptr(k), m, it
+        a.table, a.scores, a.maps = _lib.ptr(table), _lib.ptr(out.scores), _lib.ptr(out.maps)
+        a.hist_iter, a.hist_score, a.hist_len = _lib.ptr(hi_it), _lib.ptr(hi_sc), _lib.ptr(hl)
+        a.draws_used = _lib.ptr(out.draws_used)
+        ctx = _lib.context(dev)
+        with ctx.lock:
+            before = ctx.launches()
+            _lib.check(_lib.load().ccg_mas_det_solve(ctx.handle, a), "mas_det_solve")
+            out.launches = ctx.launches() - before
+        out.history = [list(zip(hi_it[j, :hl[j]].tolist(), hi_sc[j, :hl[j]].tolist()))
+                       for j in range(m)]
+        return out
+
+    parts = _run_sharded(n, 0, devs, run)
+    return DetResult(scores=np.concatenate([p.scores for p in parts]),
+                     maps=np.concatenate([p.maps for p in parts]),
+                     history=[h for p in parts for h in p.history],
+                     draws_used=np.concatenate([p.draws_used for p in parts]),
+                     launches=sum(p.launches for p in parts))

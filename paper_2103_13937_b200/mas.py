@@ -1,11 +1,12 @@
 """Monoalphabetic-substitution attack (reference mas.py:1-299), GPU-backed.
 
 Stochastic better-neighbour climbing (mas.py:218-299) runs entirely on the GPU: one
-warp per worker (csrc/ccg_mas.cu).  Signatures, defaults, validation messages and
+warp per worker (csrc/ccg_mas_tform.cu, csrc/ccg_mas.cu).  The deterministic best-neighbour
+variant (mas.py:84-169) runs one CTA of 325 pair-workers per restart with the whole
+iteration loop on the device (csrc/ccg_mas_det.cu).  Signatures, defaults, validation messages and
 result objects follow the reference so this module drops in for it; `jobs` is accepted
 for signature compatibility and has no effect on results (the reference guarantees the
-same: search.py:4-7).  The deterministic best-neighbour variant (mas.py:84-169) is the
-next item on the build plan and is not yet on the GPU.
+same: search.py:4-7).
 """
 from __future__ import annotations
 
@@ -18,7 +19,7 @@ from . import engine
 from .codec import ALPHABET_SIZE, MappedText
 from .ngrams import BigramTable
 from .pairs import PAIR_TOTAL, index_to_pair
-from .rng import WorkerRng, philox_keys, worker_stream_index
+from .rng import WorkerRng, philox_keys, pivot_stream_index, worker_stream_index
 from .search import RestartSummary, SolveResult, fold_restarts
 
 
@@ -134,36 +135,63 @@ def _batched_restarts(make_batch, restarts: int, workers: int, stop):
 def solve_with_restarts(cipher: MappedText, table: BigramTable, cfg: MasSolverConfig,
                         jobs: int = 1, stop=None) -> tuple[SolveResult, list[RestartSummary]]:
     """mas.py:281-299."""
-    if cfg.mode == "deterministic":
-        from .search import run_restarts
-
-        return run_restarts(lambda r: solve_deterministic(cipher, table, cfg, restart=r),
-                            cfg.restarts, stop=stop)
     text = _check_cipher(cipher)
+    if cfg.mode == "deterministic":
+        return _batched_restarts(lambda rs: _det_batch(text, table, cfg, rs), cfg.restarts,
+                                 PAIR_TOTAL, stop)
     return _batched_restarts(lambda rs: _restart_batch(text, table, cfg, rs), cfg.restarts,
                              cfg.workers, stop)
 
 
 # ------------------------------------------------------------------ deterministic mode
-_NEXT = ("the deterministic best-neighbour MAS solver (reference mas.py:84-169) is the next "
-         "build item (SURVEY.md 8f-1) and is not on the CUDA engine yet")
+def deterministic_step(current: MappedText, pivot: tuple[int, int],
+                       table: BigramTable) -> tuple[np.ndarray, int, int]:
+    """Evaluate all 325 pair-workers for one pivot on the GPU; return the first best
+    (candidate text, score, worker index) (mas.py:84-120)."""
+    text = np.asarray(current, dtype=np.int64)
+    pl, pr = int(pivot[0]), int(pivot[1])
+    if pl == pr:
+        raise ValueError("pivot letters must differ")
+    present = np.zeros(ALPHABET_SIZE, dtype=bool)
+    present[text] = True
+    if not (0 <= pl < ALPHABET_SIZE and 0 <= pr < ALPHABET_SIZE and present[pl] and present[pr]):
+        raise ValueError("both pivot letters must occur in the text")
+    scores = engine.mas_det_step_batch([text], [(pl, pr)], table.scores)[0]
+    best_index = int(np.argmax(scores))  # first maximum (search.py:19-25)
+    return climb_unchecked(text, best_index, (pl, pr)), int(scores[best_index]), best_index
 
 
-def deterministic_step(current, pivot, table):
-    raise NotImplementedError(_NEXT)
+def climb_unchecked(current, best_index, pivot):
+    other_left, other_right = index_to_pair(best_index)
+    pl, pr = int(pivot[0]), int(pivot[1])
+    first = np.arange(ALPHABET_SIZE, dtype=np.int64)
+    first[pl], first[other_left] = other_left, pl
+    second = np.arange(ALPHABET_SIZE, dtype=np.int64)
+    second[pr], second[other_right] = other_right, pr
+    return second[first][np.asarray(current, dtype=np.int64)]
 
 
-def climb(current, best_index, pivot):
+def climb(current: MappedText, best_index: int, pivot: tuple[int, int]) -> np.ndarray:
+    """Reconstruct the winning worker's candidate from its index (mas.py:123-130)."""
     other_left, other_right = index_to_pair(best_index)
     pl, pr = int(pivot[0]), int(pivot[1])
     if pl == other_right or pr == other_left:
         raise ValueError(f"worker {best_index} is excluded for pivot ({pl}, {pr})")
-    first = np.arange(ALPHABET_SIZE, dtype=np.int64)
-    first[[pl, other_left]] = first[[other_left, pl]]
-    second = np.arange(ALPHABET_SIZE, dtype=np.int64)
-    second[[pr, other_right]] = second[[other_right, pr]]
-    return second[first][np.asarray(current, dtype=np.int64)]
+    return climb_unchecked(current, best_index, pivot)
 
 
-def solve_deterministic(cipher, table, cfg, restart: int = 0):
-    raise NotImplementedError(_NEXT)
+def _det_batch(text, table, cfg, restarts):
+    keys = philox_keys([cfg.global_seed], [pivot_stream_index(r) for r in restarts])
+    res = engine.mas_det_solve([text], np.zeros(len(restarts), np.int32), keys, table.scores,
+                               cfg.iterations)
+    return [SolveResult(best_text=res.maps[i].astype(np.int64)[text], best_score=int(res.scores[i]),
+                        per_worker_scores=[], history=[(int(a), int(b)) for a, b in res.history[i]])
+            for i in range(len(restarts))]
+
+
+def solve_deterministic(cipher: MappedText, table: BigramTable, cfg: MasSolverConfig,
+                        restart: int = 0) -> SolveResult:
+    """The best-neighbour climb for cfg.iterations iterations (mas.py:140-169), the whole
+    loop in one GPU launch (one CTA, 325 pair-workers)."""
+    text = _check_cipher(cipher)
+    return _det_batch(text, table, cfg, [restart])[0]

@@ -113,3 +113,36 @@ def gather_cases(permutation):
         out.append((key, int(n), g["maps"][pos:pos + n]))
         pos += n
     return out
+
+
+def det_step_cases():
+    """[(text, (pl, pr), table, want_score, want_index, want_candidate)] from
+    tests/golden/mas_det.npz (reference deterministic_step, mas.py:84-120)."""
+    g = load("mas_det")
+    out, pos = [], 0
+    for i, L in enumerate(g["step_len"]):
+        L = int(L)
+        text = g["step_text"][pos:pos + L].astype(np.int64)
+        cand = g["step_cand"][pos:pos + L].astype(np.int64)
+        pos += L
+        pl, pr = (int(v) for v in g["step_pivot"][i])
+        out.append((text, (pl, pr), g["tables"][int(g["step_table"][i])], int(g["step_score"][i]),
+                    int(g["step_index"][i]), cand))
+    return out
+
+
+def det_run_cases():
+    """[(cipher, table, seed, restart, iterations, want_text, want_score, want_history)] from
+    reference solve_deterministic runs (mas.py:140-169)."""
+    g = load("mas_det")
+    out, pos, hpos = [], 0, 0
+    for i, L in enumerate(g["run_len"]):
+        L = int(L)
+        nh = int(g["run_nhist"][i])
+        hist = [(int(a), int(b)) for a, b in g["run_hist"][hpos:hpos + nh]]
+        hpos += nh
+        out.append((g["run_cipher"][pos:pos + L].astype(np.int64), g["tables"][int(g["run_table"][i])],
+                    int(g["run_seed"][i]), int(g["run_restart"][i]), int(g["run_iters"][i]),
+                    g["run_text"][pos:pos + L].astype(np.int64), int(g["run_score"][i]), hist))
+        pos += L
+    return out

@@ -357,3 +357,82 @@ def test_mas_acceptance_07_shape(golden):
                                 [(last << 32) | w for w in range(64)], table.scores, 10_000)
         assert runs[-1].score == want.max()
     assert ok >= 2
+
+
+# ------------------------------------------------------------------ deterministic MAS (mas.py:84-169)
+def test_det_step_matches_reference(golden):
+    cases = golden.det_step_cases()
+    for text, pivot, table, score, index, cand in cases:
+        got_t, got_s, got_i = cc.deterministic_step(text, pivot, cc.BigramTable(table))
+        assert (got_s, got_i) == (score, index)
+        assert np.array_equal(got_t, cand)
+
+
+def test_det_step_all_scores_vs_oracle():
+    # every one of the 325 pair-worker scores, including excluded ones and wide tables
+    rng = np.random.default_rng(31)
+    texts, pivots, tables = [], [], []
+    for i in range(60):
+        L = int(rng.integers(2, 700))
+        t = rng.integers(0, 26, L)
+        if np.unique(t).size < 2:
+            t[0], t[-1] = 3, 4
+        texts.append(t)
+        pivots.append(tuple(int(v) for v in rng.choice(np.unique(t), 2, replace=False)))
+    for hi in (900, 40_000, 2**40):
+        table = rng.integers(0, hi, 676)
+        got = engine.mas_det_step_batch(texts, pivots, table)
+        for t, pv, row in zip(texts, pivots, got):
+            want, _, _ = O.det_step(t, pv, table)
+            assert np.array_equal(row, want)
+
+
+def test_det_step_validation():
+    table = cc.BigramTable(np.arange(676))
+    with pytest.raises(ValueError):
+        cc.deterministic_step(cc.map_text("abcabc"), (0, 0), table)
+    with pytest.raises(ValueError):
+        cc.deterministic_step(cc.map_text("abcabc"), (0, 25), table)
+
+
+def test_solve_deterministic_matches_reference(golden):
+    for cipher, table, seed, r, iters, text, score, hist in golden.det_run_cases():
+        cfg = cc.MasSolverConfig(mode="deterministic", workers=325, iterations=iters,
+                                 global_seed=seed)
+        res = cc.solve_deterministic(cipher, cc.BigramTable(table), cfg, restart=r)
+        assert res.best_score == score and res.history == hist
+        assert np.array_equal(res.best_text, text)
+        assert res.per_worker_scores == []
+
+
+def test_solve_deterministic_batch_vs_oracle():
+    # many jobs in one launch, random tables (narrow and wide accumulators), vs the oracle
+    rng = np.random.default_rng(44)
+    for hi in (700, 3_000_000):
+        table = rng.integers(0, hi, 676)
+        ciphers = [rng.integers(0, 26, int(rng.integers(2, 400))) for _ in range(24)]
+        for c in ciphers:
+            if np.unique(c).size < 2:
+                c[0], c[-1] = 1, 2
+        seed = int(rng.integers(0, 2**63))
+        cof = np.repeat(np.arange(len(ciphers), dtype=np.int32), 2)
+        restarts = [0, 3] * len(ciphers)
+        keys = philox_keys([seed], [((r << 32) | (2**32 - 1)) for r in restarts])
+        res = engine.mas_det_solve(ciphers, cof, keys, table, 120)
+        for j, (c, r) in enumerate(zip(cof, restarts)):
+            t, s, h = O.solve_deterministic(ciphers[c], table, 120, seed, r)
+            assert int(res.scores[j]) == s and res.history[j] == h
+            assert np.array_equal(res.maps[j].astype(np.int64)[ciphers[c]], t)
+
+
+def test_solve_with_restarts_deterministic_fold_and_stop(golden):
+    cipher, table, seed, _, iters, _, _, _ = golden.det_run_cases()[0]
+    cfg = cc.MasSolverConfig(mode="deterministic", workers=325, iterations=iters,
+                             global_seed=seed, restarts=4)
+    best, summ = cc.solve_with_restarts(cipher, cc.BigramTable(table), cfg)
+    want = [O.solve_deterministic(cipher, table, iters, seed, r)[1] for r in range(4)]
+    assert [s.score for s in summ] == want
+    assert best.best_score == max(want) and best.restart_index == want.index(max(want))
+    best2, summ2 = cc.solve_with_restarts(cipher, cc.BigramTable(table), cfg,
+                                          stop=lambda res: res.restart_index == 1)
+    assert len(summ2) == 2

@@ -141,3 +141,40 @@ def test_sct_solve_per_worker_scores(golden):
     assert scores.tolist() == g["per_worker"].tolist()
     best = int(np.argmax(scores))
     assert np.array_equal(keys[best], g["best_key"])
+
+
+# ------------------------------------------------------------------ deterministic MAS
+def test_det_step_matches_reference(golden):
+    for text, pivot, table, score, index, cand in golden.det_step_cases():
+        scores, best, got = O.det_step(text, pivot, table)
+        assert (int(scores[best]), best) == (score, index)
+        assert np.array_equal(got, cand)
+
+
+def test_det_step_brute_force_property():
+    # every candidate score is the full rescore of its explicitly built text
+    # (reference tests/test_mas.py:31-51 brute_force_step)
+    rng = np.random.default_rng(3)
+    table = rng.integers(0, 700, 676)
+    for _ in range(5):
+        text = rng.integers(0, 26, 90)
+        pl, pr = (int(v) for v in rng.choice(np.unique(text), 2, replace=False))
+        scores, _, _ = O.det_step(text, (pl, pr), table)
+        t = 0
+        for L in range(26):
+            for R in range(L + 1, 26):
+                if R == pl or L == pr:
+                    assert scores[t] == 0
+                else:
+                    c = text.copy()
+                    c = np.where(c == pl, L, np.where(c == L, pl, c))
+                    c = np.where(c == pr, R, np.where(c == R, pr, c))
+                    assert scores[t] == O.score_text(c, table)
+                t += 1
+
+
+def test_solve_deterministic_matches_reference(golden):
+    for cipher, table, seed, r, iters, text, score, hist in golden.det_run_cases():
+        got_t, got_s, got_h = O.solve_deterministic(cipher, table, iters, seed, r)
+        assert got_s == score and got_h == hist
+        assert np.array_equal(got_t, text)
