@@ -15,6 +15,9 @@
  *   ccg_mas_climb[_dev]                          mas.py:247-250 _stochastic_task -> mas.py:218-244
  *                                                stochastic_worker, for a whole run_worker_pool batch
  *                                                (mas.py:266-272) + search.py:19-25 max_element per group
+ *   ccg_ngram_score_batch                        ngrams.py:134-140 score_text generalised to order-n windows
+ *   ccg_mas_ngram_climb[_dev]                    mas.py:218-244 stochastic_worker generalised to an order-n
+ *                                                (n = 2, 3, 4) integer table (BASELINE configs 4-5)
  *   ccg_mas_det_step_batch                       mas.py:84-120 deterministic_step (all 325 pair-worker scores)
  *   ccg_mas_det_solve[_dev]                      mas.py:140-169 solve_deterministic, a batch of
  *                                                (ciphertext, restart) jobs, whole loop on device
@@ -129,6 +132,37 @@ typedef struct {
 
 int ccg_mas_climb(ccg_ctx *ctx, const ccg_mas_climb_args *args);
 int ccg_mas_climb_dev(ccg_ctx *ctx, const ccg_mas_climb_args *args);
+
+/* n-gram extension (the reference has bigrams only).  Window index
+ * sum_j 26^(order-1-j) t_{s+j}; a text of n letters has max(0, n-order+1) windows. */
+/* ngrams.py:134-140 generalised: table int64[26^order], entries >= 0. */
+int ccg_ngram_score_batch(ccg_ctx *ctx, const uint8_t *texts, const int64_t *offsets,
+                          int64_t n_texts, int32_t order, const int64_t *table, int64_t *out);
+
+typedef struct {
+  const uint8_t *ciphers;     /* concatenated ciphertexts (each <= 4096 letters) */
+  const int64_t *offsets;     /* [n_ciphers + 1] */
+  int64_t n_ciphers;
+  const int32_t *cipher_of;   /* [n_workers] */
+  const uint64_t *keys;       /* [2 * n_workers] Philox key (k0, k1) per worker */
+  const uint64_t *skips;      /* [n_workers] draws already consumed, or NULL */
+  int64_t n_workers;
+  int64_t climbings;
+  int32_t order;              /* 2, 3 or 4 */
+  const uint16_t *table;      /* [26^order] integer n-gram scores (e.g. a quantised log table) */
+  int64_t *scores;            /* [n_workers] */
+  uint8_t *maps;              /* [26 * n_workers] cipher letter -> plaintext letter, or NULL */
+  uint64_t *draws_used;
+  int64_t *last_accept;
+  int64_t *tries_done;
+  int32_t group_size;
+  int64_t *group_best;
+  int64_t max_len;            /* required by the _dev entry point only */
+  uint32_t flags;
+} ccg_mas_ngram_args;
+
+int ccg_mas_ngram_climb(ccg_ctx *ctx, const ccg_mas_ngram_args *args);
+int ccg_mas_ngram_climb_dev(ccg_ctx *ctx, const ccg_mas_ngram_args *args);
 
 /* mas.py:84-120 deterministic_step for a batch: text i with pivot (pivots[2i], pivots[2i+1])
  * (distinct letters, both present in the text).  Writes the 325 pair-worker candidate scores of

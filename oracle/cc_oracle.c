@@ -28,6 +28,16 @@
  *   sct.py:69-135     select_operator / apply_element_swaps / apply_block_swaps / apply_block_shift
  *   sct.py:148-170    sct_worker
  *   search.py:19-25   max_element (first maximum)
+ *
+ * n-gram extension (orders 3 and 4; BASELINE.json configs 3-5).  The reference implements
+ * bigrams only (ngrams.py:21), so these functions generalise its semantics to
+ * windows of `order` letters: index sum_i 26^(order-1-i) t_i, integer score = sum of table
+ * entries over the n-order+1 windows (ngrams.py:134-140), log score = numpy pairwise sum of
+ * the window log-probabilities (ngrams.py:166-172), MAS worker = stochastic_worker with
+ * the exact score change computed by FULL RESCORE of the swapped text, SCT worker =
+ * sct_worker with the order-n candidate score.  At order 2 each reduces to the reference
+ * function and is pinned by the reference's golden vectors (tests/test_oracle_golden.py);
+ * orders 3/4 have no reference outputs ("parity unpinned" beyond that reduction).
  */
 #include <stdint.h>
 #include <stdlib.h>
@@ -158,6 +168,62 @@ double cco_log_score_text(const int64_t *t, int64_t n, const double *logs, doubl
     if (n < 2) return 0.0;
     for (int64_t i = 0; i + 1 < n; i++) scratch[i] = logs[ALPHA * t[i] + t[i + 1]];
     return cco_pairwise_sum(scratch, n - 1);
+}
+
+/* ------------------------------------------------------------------ n-gram generalisation */
+static inline int64_t ngram_index(const int64_t *t, int order) {
+    int64_t idx = 0;
+    for (int j = 0; j < order; j++) idx = idx * ALPHA + t[j];
+    return idx;
+}
+
+int64_t cco_ngram_score_text(const int64_t *t, int64_t n, int order, const int64_t *table) {
+    int64_t s = 0;
+    for (int64_t i = 0; i + order <= n; i++) s += table[ngram_index(t + i, order)];
+    return s;
+}
+
+double cco_ngram_log_score_text(const int64_t *t, int64_t n, int order, const double *logs,
+                                double *scratch) {
+    if (n < order) return 0.0;
+    for (int64_t i = 0; i + order <= n; i++) scratch[i] = logs[ngram_index(t + i, order)];
+    return cco_pairwise_sum(scratch, n - order + 1);
+}
+
+/* stochastic_worker (mas.py:218-244) with an order-n integer table: per try a distinct
+ * letter pair, the exact score change of interchanging the two letters in the current text
+ * (here: full rescore of the swapped text minus the current score), commit iff > 0. */
+int64_t cco_ngram_worker(const int64_t *cipher, int64_t n, int order, const int64_t *S,
+                         int64_t climbings, uint64_t seed, uint64_t stream, int64_t skip,
+                         int64_t *out_text, int64_t *out_map, int64_t *out_last_accept) {
+    orng g; orng_init(&g, seed, stream);
+    for (int64_t i = 0; i < skip; i++) orng_next_u64(&g);
+    int64_t *text = (int64_t *)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+    int64_t *cand = (int64_t *)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+    memcpy(text, cipher, sizeof(int64_t) * n);
+    int64_t mapping[ALPHA];
+    for (int i = 0; i < ALPHA; i++) mapping[i] = i;
+    int64_t score = cco_ngram_score_text(text, n, order, S), last = -1;
+    for (int64_t t = 0; t < climbings; t++) {
+        int64_t a, b;
+        orng_distinct_pair(&g, ALPHA, &a, &b);
+        for (int64_t i = 0; i < n; i++) cand[i] = text[i] == a ? b : (text[i] == b ? a : text[i]);
+        int64_t delta = cco_ngram_score_text(cand, n, order, S) - score;
+        if (delta > 0) {
+            score += delta;
+            memcpy(text, cand, sizeof(int64_t) * n);
+            for (int x = 0; x < ALPHA; x++) {
+                if (mapping[x] == a) mapping[x] = b;
+                else if (mapping[x] == b) mapping[x] = a;
+            }
+            last = t;
+        }
+    }
+    if (out_text) memcpy(out_text, text, sizeof(int64_t) * n);
+    if (out_map) for (int i = 0; i < ALPHA; i++) out_map[i] = mapping[i];
+    if (out_last_accept) *out_last_accept = last;
+    free(text); free(cand);
+    return score;
 }
 
 /* ------------------------------------------------------------------ MAS */
@@ -323,7 +389,7 @@ void cco_sct_decrypt(const int64_t *cipher, int64_t n, const int64_t *key, int64
 }
 
 typedef struct {
-    int64_t k, climbings, p1, p2, op1_hop, op2_hop;
+    int64_t k, climbings, p1, p2, op1_hop, op2_hop, order;
 } sct_cfg;
 
 /* sct.py:82-89 */
@@ -387,16 +453,17 @@ void cco_apply_operator(int op, const int64_t *key, int64_t k, int64_t max_hops,
 }
 
 static double sct_candidate_score(const int64_t *cipher, int64_t n, const int64_t *key, int64_t k,
-                                  const double *logs, int64_t *plain, int64_t *map, double *terms) {
+                                  const double *logs, int order, int64_t *plain, int64_t *map,
+                                  double *terms) {
     cco_sct_decrypt(cipher, n, key, k, plain, map);
-    return cco_log_score_text(plain, n, logs, terms);
+    return cco_ngram_log_score_text(plain, n, order, logs, terms);
 }
 
 /* sct.py:148-170.  Returns the final score; writes the final key. */
 double cco_sct_worker(const int64_t *cipher, int64_t n, const double *logs, const int64_t *cfgv,
                       uint64_t seed, uint64_t stream, int64_t skip, int64_t *out_key,
                       int64_t *out_last_accept) {
-    sct_cfg cfg = {cfgv[0], cfgv[1], cfgv[2], cfgv[3], cfgv[4], cfgv[5]};
+    sct_cfg cfg = {cfgv[0], cfgv[1], cfgv[2], cfgv[3], cfgv[4], cfgv[5], cfgv[6]};
     int64_t k = cfg.k;
     orng g; orng_init(&g, seed, stream);
     for (int64_t i = 0; i < skip; i++) orng_next_u64(&g);
@@ -405,7 +472,7 @@ double cco_sct_worker(const int64_t *cipher, int64_t n, const double *logs, cons
     double *terms = (double *)malloc(sizeof(double) * (n > 1 ? n : 1));
     int64_t key[256], cand[256];
     orng_permutation(&g, k, key);
-    double score = sct_candidate_score(cipher, n, key, k, logs, plain, map, terms);
+    double score = sct_candidate_score(cipher, n, key, k, logs, (int)cfg.order, plain, map, terms);
     int64_t last = -1;
     for (int64_t t = 0; t < cfg.climbings; t++) {
         int64_t u = orng_int_below(&g, 100);
@@ -413,7 +480,7 @@ double cco_sct_worker(const int64_t *cipher, int64_t n, const double *logs, cons
         if (u < cfg.p1) op_element_swaps(cand, k, &g, cfg.op1_hop);
         else if (u < cfg.p2) op_block_swaps(cand, k, &g, cfg.op2_hop);
         else op_block_shift(cand, k, &g);
-        double cs = sct_candidate_score(cipher, n, cand, k, logs, plain, map, terms);
+        double cs = sct_candidate_score(cipher, n, cand, k, logs, (int)cfg.order, plain, map, terms);
         if (cs > score) {
             memcpy(key, cand, sizeof(int64_t) * k);
             score = cs;
@@ -427,11 +494,11 @@ double cco_sct_worker(const int64_t *cipher, int64_t n, const double *logs, cons
 }
 
 double cco_sct_score(const int64_t *cipher, int64_t n, const double *logs, const int64_t *key,
-                     int64_t k) {
+                     int64_t k, int order) {
     int64_t *plain = (int64_t *)malloc(sizeof(int64_t) * n);
     int64_t *map = (int64_t *)malloc(sizeof(int64_t) * n);
     double *terms = (double *)malloc(sizeof(double) * (n > 1 ? n : 1));
-    double s = sct_candidate_score(cipher, n, key, k, logs, plain, map, terms);
+    double s = sct_candidate_score(cipher, n, key, k, logs, order, plain, map, terms);
     free(plain); free(map); free(terms);
     return s;
 }
@@ -443,7 +510,8 @@ double cco_sct_score(const int64_t *cipher, int64_t n, const double *logs, const
 #include <pthread.h>
 
 typedef struct {
-    int kind;  /* 0 = MAS, 1 = SCT */
+    int kind;  /* 0 = MAS, 1 = SCT, 2 = MAS order-n */
+    int order;
     const int64_t *ciphers, *offsets;
     const int32_t *cipher_of;
     const uint64_t *seeds, *streams;
@@ -465,7 +533,11 @@ static void *batch_thread(void *arg) {
         int32_t c = J->cipher_of[w];
         const int64_t *txt = J->ciphers + J->offsets[c];
         int64_t n = J->offsets[c + 1] - J->offsets[c];
-        if (J->kind == 0) {
+        if (J->kind == 2) {
+            J->out_iscores[w] = cco_ngram_worker(txt, n, J->order, J->S, J->climbings, J->seeds[w],
+                                                 J->streams[w], 0, NULL,
+                                                 J->out_keys ? J->out_keys + 26 * w : NULL, NULL);
+        } else if (J->kind == 0) {
             J->out_iscores[w] = cco_stochastic_worker(txt, n, J->S, J->climbings, J->seeds[w],
                                                       J->streams[w], 0, NULL,
                                                       J->out_keys ? J->out_keys + 26 * w : NULL,
@@ -511,5 +583,17 @@ void cco_sct_workers(const int64_t *ciphers, const int64_t *offsets, const int32
     J.kind = 1; J.ciphers = ciphers; J.offsets = offsets; J.cipher_of = cipher_of;
     J.seeds = seeds; J.streams = streams; J.n_workers = n_workers; J.logs = logs; J.cfgv = cfgv;
     J.out_fscores = out_scores; J.out_keys = out_keys;
+    run_batch(&J, nthreads);
+}
+
+void cco_ngram_workers(const int64_t *ciphers, const int64_t *offsets, const int32_t *cipher_of,
+                       const uint64_t *seeds, const uint64_t *streams, int64_t n_workers, int order,
+                       const int64_t *S, int64_t climbings, int64_t *out_scores, int64_t *out_maps,
+                       int nthreads) {
+    batch_job J;
+    memset(&J, 0, sizeof J);
+    J.kind = 2; J.order = order; J.ciphers = ciphers; J.offsets = offsets; J.cipher_of = cipher_of;
+    J.seeds = seeds; J.streams = streams; J.n_workers = n_workers; J.S = S;
+    J.climbings = climbings; J.out_iscores = out_scores; J.out_keys = out_maps;
     run_batch(&J, nthreads);
 }

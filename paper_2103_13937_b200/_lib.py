@@ -51,6 +51,16 @@ class SctClimbArgs(C.Structure):
     ]
 
 
+class MasNgramArgs(C.Structure):
+    _fields_ = [
+        ("ciphers", _P), ("offsets", _P), ("n_ciphers", _i64), ("cipher_of", _P), ("keys", _P),
+        ("skips", _P), ("n_workers", _i64), ("climbings", _i64), ("order", _i32), ("table", _P),
+        ("scores", _P), ("maps", _P), ("draws_used", _P), ("last_accept", _P),
+        ("tries_done", _P), ("group_size", _i32), ("group_best", _P), ("max_len", _i64),
+        ("flags", _u32),
+    ]
+
+
 class MasDetArgs(C.Structure):
     _fields_ = [
         ("ciphers", _P), ("offsets", _P), ("n_ciphers", _i64), ("cipher_of", _P), ("keys", _P),
@@ -86,6 +96,9 @@ EXPORTS = {
     "ccg_mas_delta_counts_batch": (C.c_int, [_P, _P, _i64, _P, _P, _P]),
     "ccg_mas_climb": (C.c_int, [_P, C.POINTER(MasClimbArgs)]),
     "ccg_mas_climb_dev": (C.c_int, [_P, C.POINTER(MasClimbArgs)]),
+    "ccg_ngram_score_batch": (C.c_int, [_P, _P, _P, _i64, _i32, _P, _P]),
+    "ccg_mas_ngram_climb": (C.c_int, [_P, C.POINTER(MasNgramArgs)]),
+    "ccg_mas_ngram_climb_dev": (C.c_int, [_P, C.POINTER(MasNgramArgs)]),
     "ccg_mas_det_step_batch": (C.c_int, [_P, _P, _P, _i64, _P, _P, _P]),
     "ccg_mas_det_solve": (C.c_int, [_P, C.POINTER(MasDetArgs)]),
     "ccg_mas_det_solve_dev": (C.c_int, [_P, C.POINTER(MasDetArgs)]),

@@ -605,6 +605,161 @@ int ccg_mas_climb(ccg_ctx* ctx, const ccg_mas_climb_args* a) {
   return finish(ctx, cudaSuccess, "mas_climb");
 }
 
+// ------------------------------------------------------------------ n-gram extension
+static int check_order(int32_t order) {
+  if (order < 2 || order > 4)
+    return fail(CCG_ERR_UNSUPPORTED, "n-gram order %d: the engine supports 2..4", order);
+  return CCG_OK;
+}
+
+static int64_t pow26_i(int order) {
+  int64_t v = 1;
+  for (int i = 0; i < order; ++i) v *= kAlpha;
+  return v;
+}
+
+int ccg_ngram_score_batch(ccg_ctx* ctx, const uint8_t* texts, const int64_t* offsets,
+                          int64_t n_texts, int32_t order, const int64_t* table, int64_t* out) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if ((rc = check_order(order))) return rc;
+  if ((rc = check_ragged(texts, offsets, n_texts, "ngram_score", nullptr))) return rc;
+  if (!table) return fail(CCG_ERR_INVALID, "null table");
+  const int64_t T = pow26_i(order);
+  for (int64_t i = 0; i < T; ++i)
+    if (table[i] < 0) return fail(CCG_ERR_INVALID, "n-gram scores must be non-negative");
+  if (n_texts == 0) return CCG_OK;
+  if (!out) return fail(CCG_ERR_INVALID, "null out");
+  void *dt, *doff, *dtab, *dout;
+  if ((rc = upload(ctx, 0, texts, (size_t)offsets[n_texts], &dt))) return rc;
+  if ((rc = upload(ctx, 1, offsets, (size_t)(n_texts + 1) * 8, &doff))) return rc;
+  if ((rc = upload(ctx, 2, table, (size_t)T * 8, &dtab))) return rc;
+  if ((rc = ctx->buf(3, (size_t)n_texts * 8, &dout))) return rc;
+  ctx->launches++;
+  cudaError_t e = launch_ngram_score(ctx->stream, (const uint8_t*)dt, (const int64_t*)doff, n_texts,
+                                     order, (const int64_t*)dtab, (int64_t*)dout);
+  if (e != cudaSuccess) return cuda_fail(e, "ngram_score kernel");
+  if ((rc = download(ctx, out, dout, (size_t)n_texts * 8))) return rc;
+  return finish(ctx, cudaSuccess, "ngram_score");
+}
+
+static int ngram_launch(ccg_ctx* ctx, const ccg_mas_ngram_args* a, int64_t max_len) {
+  if (max_len > kNgramMaxLen)
+    return fail(CCG_ERR_UNSUPPORTED,
+                "ciphertext of %lld letters exceeds the n-gram engine limit %lld",
+                (long long)max_len, (long long)kNgramMaxLen);
+  MasNgramLaunch p;
+  p.ciphers = a->ciphers;
+  p.offsets = a->offsets;
+  p.cipher_of = a->cipher_of;
+  p.keys = a->keys;
+  p.skips = a->skips;
+  p.n_workers = a->n_workers;
+  p.climbings = a->climbings;
+  p.order = a->order;
+  p.table = a->table;
+  p.max_len = max_len < 1 ? 1 : max_len;
+  p.scores = a->scores;
+  p.maps = a->maps;
+  p.draws_used = a->draws_used;
+  p.last_accept = a->last_accept;
+  p.tries_done = a->tries_done;
+  p.flags = a->flags;
+  ctx->launches++;
+  cudaError_t e = launch_mas_ngram_climb(ctx->stream, p, ctx->sm_count);
+  if (e != cudaSuccess) return cuda_fail(e, "mas_ngram kernel");
+  if (a->group_size > 0 && a->group_best) {
+    ctx->launches++;
+    e = launch_group_best_i64(ctx->stream, a->scores, a->n_workers / a->group_size, a->group_size,
+                              a->group_best);
+    if (e != cudaSuccess) return cuda_fail(e, "group_best kernel");
+  }
+  return CCG_OK;
+}
+
+int ccg_mas_ngram_climb_dev(ccg_ctx* ctx, const ccg_mas_ngram_args* a) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (!a) return fail(CCG_ERR_INVALID, "null args");
+  if ((rc = check_order(a->order))) return rc;
+  if ((rc = check_climb_common(a->n_workers, a->climbings, a->group_size, a->scores, a->keys,
+                               a->cipher_of)))
+    return rc;
+  if (!a->table) return fail(CCG_ERR_INVALID, "null table");
+  return ngram_launch(ctx, a, a->max_len);
+}
+
+int ccg_mas_ngram_climb(ccg_ctx* ctx, const ccg_mas_ngram_args* a) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (!a) return fail(CCG_ERR_INVALID, "null args");
+  if ((rc = check_order(a->order))) return rc;
+  if ((rc = check_climb_common(a->n_workers, a->climbings, a->group_size, a->scores, a->keys,
+                               a->cipher_of)))
+    return rc;
+  if (!a->table) return fail(CCG_ERR_INVALID, "null table");
+  int64_t max_len = 0;
+  if ((rc = check_ragged(a->ciphers, a->offsets, a->n_ciphers, "mas_ngram_climb", &max_len)))
+    return rc;
+  const int64_t nw = a->n_workers;
+  if (nw == 0) return CCG_OK;
+  for (int64_t i = 0; i < nw; ++i)
+    if (a->cipher_of[i] < 0 || a->cipher_of[i] >= a->n_ciphers)
+      return fail(CCG_ERR_INVALID, "cipher_of[%lld] out of range", (long long)i);
+  const int64_t T = pow26_i(a->order);
+  ccg_mas_ngram_args d = *a;
+  void* p;
+  if ((rc = upload(ctx, 0, a->ciphers, (size_t)a->offsets[a->n_ciphers], &p))) return rc;
+  d.ciphers = (const uint8_t*)p;
+  if ((rc = upload(ctx, 1, a->offsets, (size_t)(a->n_ciphers + 1) * 8, &p))) return rc;
+  d.offsets = (const int64_t*)p;
+  if ((rc = upload(ctx, 2, a->cipher_of, (size_t)nw * 4, &p))) return rc;
+  d.cipher_of = (const int32_t*)p;
+  if ((rc = upload(ctx, 3, a->keys, (size_t)nw * 16, &p))) return rc;
+  d.keys = (const uint64_t*)p;
+  if (a->skips) {
+    if ((rc = upload(ctx, 4, a->skips, (size_t)nw * 8, &p))) return rc;
+    d.skips = (const uint64_t*)p;
+  }
+  if ((rc = upload(ctx, 5, a->table, (size_t)T * 2, &p))) return rc;
+  d.table = (const uint16_t*)p;
+  if ((rc = ctx->buf(6, (size_t)nw * 8, &p))) return rc;
+  d.scores = (int64_t*)p;
+  if (a->maps) {
+    if ((rc = ctx->buf(7, (size_t)nw * kAlpha, &p))) return rc;
+    d.maps = (uint8_t*)p;
+  }
+  if (a->draws_used) {
+    if ((rc = ctx->buf(8, (size_t)nw * 8, &p))) return rc;
+    d.draws_used = (uint64_t*)p;
+  }
+  if (a->last_accept) {
+    if ((rc = ctx->buf(9, (size_t)nw * 8, &p))) return rc;
+    d.last_accept = (int64_t*)p;
+  }
+  if (a->tries_done) {
+    if ((rc = ctx->buf(10, (size_t)nw * 8, &p))) return rc;
+    d.tries_done = (int64_t*)p;
+  }
+  const int64_t ng = a->group_size > 0 ? nw / a->group_size : 0;
+  if (a->group_best && ng) {
+    if ((rc = ctx->buf(11, (size_t)ng * 8, &p))) return rc;
+    d.group_best = (int64_t*)p;
+  } else {
+    d.group_best = nullptr;
+  }
+  if ((rc = ngram_launch(ctx, &d, max_len))) return rc;
+  if ((rc = download(ctx, a->scores, d.scores, (size_t)nw * 8))) return rc;
+  if (a->maps && (rc = download(ctx, a->maps, d.maps, (size_t)nw * kAlpha))) return rc;
+  if (a->draws_used && (rc = download(ctx, a->draws_used, d.draws_used, (size_t)nw * 8))) return rc;
+  if (a->last_accept && (rc = download(ctx, a->last_accept, d.last_accept, (size_t)nw * 8)))
+    return rc;
+  if (a->tries_done && (rc = download(ctx, a->tries_done, d.tries_done, (size_t)nw * 8))) return rc;
+  if (ng && a->group_best && (rc = download(ctx, a->group_best, d.group_best, (size_t)ng * 8)))
+    return rc;
+  return finish(ctx, cudaSuccess, "mas_ngram_climb");
+}
+
 // ------------------------------------------------------------------ MAS deterministic
 static int check_distinct_letters(const uint8_t* texts, const int64_t* offsets, int64_t i,
                                   const char* what) {

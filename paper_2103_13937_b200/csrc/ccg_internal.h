@@ -35,6 +35,27 @@ struct MasLaunch {
   uint32_t flags;
 };
 
+// MAS climb with an order-G n-gram table (ccg_mas_ngram.cu).
+constexpr int64_t kNgramMaxLen = 4096;
+struct MasNgramLaunch {
+  const uint8_t* ciphers;
+  const int64_t* offsets;
+  const int32_t* cipher_of;
+  const uint64_t* keys;
+  const uint64_t* skips;
+  int64_t n_workers;
+  int64_t climbings;
+  int32_t order;
+  const uint16_t* table;
+  int64_t max_len;
+  int64_t* scores;
+  uint8_t* maps;
+  uint64_t* draws_used;
+  int64_t* last_accept;
+  int64_t* tries_done;
+  uint32_t flags;
+};
+
 // Deterministic best-neighbour MAS (ccg_mas_det.cu): one job = one (ciphertext, restart).
 struct MasDetLaunch {
   const uint8_t* ciphers;
@@ -105,6 +126,10 @@ cudaError_t launch_mas_climb(cudaStream_t s, const MasLaunch& p, bool wide, int 
 // T-form climb (ccg_mas_tform.cu): the fast path whenever mas_tform_ok(max_len, max(S)).
 bool mas_tform_ok(int64_t max_len, int64_t table_max);
 cudaError_t launch_mas_climb_tform(cudaStream_t s, const MasLaunch& p, int sm_count);
+size_t mas_ngram_smem_bytes(int order, int64_t max_len);
+cudaError_t launch_mas_ngram_climb(cudaStream_t s, const MasNgramLaunch& p, int sm_count);
+cudaError_t launch_ngram_score(cudaStream_t s, const uint8_t* texts, const int64_t* offsets,
+                               int64_t n, int order, const int64_t* table, int64_t* out);
 cudaError_t launch_mas_det_step(cudaStream_t s, const uint8_t* texts, const int64_t* offsets,
                                 int64_t n, const int32_t* pivots, const int64_t* table, bool wide,
                                 int64_t* out);

@@ -50,6 +50,57 @@ struct LetterWindow {
   __device__ __forceinline__ uint64_t position() const { return base + o; }
 };
 
+// 128 draws of one stream as letters int(u*26), one byte each.  Lane L holds the letters
+// of draws base+4L .. base+4L+3 (its own Philox block) in `lo` and lane L+1's in `hi`,
+// so the next four letters -- two tries' pairs when no redraw happens -- come out of two
+// 32-bit shuffles and one funnel shift.  The Philox key is re-read from global memory at
+// refill time (keeps it out of registers).
+struct ByteWindow {
+  const uint64_t* key;
+  uint64_t base;  // stream index of window draw 0 (multiple of 4)
+  uint32_t lo, hi;
+  uint32_t o;     // window offset of the next draw
+
+  __device__ __forceinline__ void refill(int lane) {
+    const uint64_t pos = base + o;
+    base = pos & ~3ULL;
+    o = (uint32_t)(pos & 3);
+    uint64_t v0, v1, v2, v3;
+    philox4x64_10(__ldg(key), __ldg(key + 1), (base >> 2) + 1 + (uint64_t)lane, v0, v1, v2, v3);
+    lo = int_below_small(v0, 26) | (int_below_small(v1, 26) << 8) |
+         (int_below_small(v2, 26) << 16) | (int_below_small(v3, 26) << 24);
+    hi = __shfl_down_sync(kFull, lo, 1);
+  }
+  // letters of draws o .. o+3, one per byte; valid when o <= 124
+  __device__ __forceinline__ uint32_t peek4() const {
+    const int src = (int)(o >> 2);
+    const uint32_t x = __shfl_sync(kFull, lo, src), y = __shfl_sync(kFull, hi, src);
+    return __funnelshift_r(x, y, (o & 3u) * 8u);
+  }
+  // letters of draws o .. o+7 (La: o..o+3, Lb: o+4..o+7); valid when o <= 120
+  __device__ __forceinline__ void peek8(uint32_t& La, uint32_t& Lb) const {
+    const int src = (int)(o >> 2);
+    const uint32_t x0 = __shfl_sync(kFull, lo, src), x1 = __shfl_sync(kFull, hi, src);
+    const uint32_t x2 = __shfl_sync(kFull, hi, src + 1);
+    La = __funnelshift_r(x0, x1, (o & 3u) * 8u);
+    Lb = __funnelshift_r(x1, x2, (o & 3u) * 8u);
+  }
+  __device__ __forceinline__ int next(int lane) {
+    if (o > 127) refill(lane);
+    const uint32_t x = __shfl_sync(kFull, lo, (int)(o >> 2));
+    const int v = (int)((x >> ((o & 3u) * 8u)) & 0xffu);
+    ++o;
+    return v;
+  }
+  // rng.py:81-89 next_distinct_pair(26)
+  __device__ __forceinline__ void pair(int lane, int& a, int& b) {
+    a = next(lane);
+    b = next(lane);
+    while (b == a) b = next(lane);
+  }
+  __device__ __forceinline__ uint64_t position() const { return base + o; }
+};
+
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }

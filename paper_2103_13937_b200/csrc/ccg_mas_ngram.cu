@@ -1,0 +1,394 @@
+// ccg_mas_ngram.cu -- the MAS stochastic climb with an order-G n-gram table (G = 2, 3, 4):
+// stochastic_worker (mas.py:218-244) generalised from bigrams to windows of G letters
+// (BASELINE.json configs 4-5; the reference itself has bigrams only).
+//
+// Fitness = sum over the n-G+1 windows of table[sum_j 26^(G-1-j) t_{s+j}] (integer, uint16
+// entries).  The proposal stream, the accept rule (exact score change > 0) and the result
+// are those of stochastic_worker; the oracle is oracle/cc_oracle.c cco_ngram_worker, which
+// reduces to the reference at G = 2 (tests/test_oracle_golden.py).
+//
+// Position-based delta.  A 26x26 count-matrix delta (mas.py:181-210) does not extend to
+// G > 2, so the warp keeps the current PLAINTEXT in shared memory together with the
+// per-ciphertext occurrence lists (positions grouped by cipher letter).  Interchanging
+// plaintext letters a, b touches exactly the positions of cipher letters xa = pi^-1(a) and
+// xb = pi^-1(b); each such position i re-scores the windows that contain it and whose
+// FIRST touched position is i (so a window holding several touched positions is counted
+// once).  Cost per evaluation ~ (occurrences of a and b) x G x 2 lookups instead of O(n).
+//
+// Warp layout.  Four proposals are evaluated per iteration, one per 8-lane group (lanes
+// 8g..8g+7 walk the touched positions of proposal g).  Proposals never read the state
+// (rng.py:81-89), so all four are scored against the state before the first; the common
+// all-rejected case is exactly the sequential outcome, otherwise the batch is replayed in
+// order with re-evaluation after the first accept (as in ccg_mas_tform.cu).  The window
+// bytes around a position come from three 32-bit shared loads and two funnel shifts; the
+// a/b tests and the swapped copy are SWAR byte operations on those words.
+//
+// Tables: G <= 3 are staged in shared memory (1.3 KB / 34 KB of uint16); the quadgram
+// table (914 KB uint16) is read through L1/L2 with __ldg.
+#include "ccg_mas_common.cuh"
+
+namespace ccg {
+namespace {
+
+constexpr int kNgWarps = 8;
+
+__host__ __device__ constexpr int pow26(int g) { return g == 0 ? 1 : 26 * pow26(g - 1); }
+
+// per-warp shared layout (bytes)
+__host__ __device__ inline uint32_t ng_text_stride(int max_len) {
+  return ((uint32_t)max_len + 12u + 15u) & ~15u;  // plaintext at +4, >= 8 bytes of slack after
+}
+__host__ __device__ inline uint32_t ng_warp_bytes(int max_len) {
+  return ng_text_stride(max_len) + ((2u * (uint32_t)max_len + 15u) & ~15u) + 32u * 2u + 32u * 4u;
+}
+
+// per-byte equality mask (0x80 in each byte of x equal to the byte in rep), exact for bytes < 0x80
+__device__ __forceinline__ uint32_t eq_bytes(uint32_t x, uint32_t rep) {
+  const uint32_t d = x ^ rep;
+  const uint32_t t = (d & 0x7f7f7f7fu) + 0x7f7f7f7fu;
+  return ~(t | d) & 0x80808080u;
+}
+__device__ __forceinline__ uint32_t expand_mask(uint32_t m80) { return (m80 >> 7) * 0xffu; }
+
+template <int G, bool SMEM_TAB>
+struct NgState {
+  const uint16_t* tab;   // global table (G = 4)
+  uint32_t tab_s;        // shared address of the staged table (G <= 3)
+  uint32_t text_base;    // shared address of the plaintext buffer (plain[i] at +4+i)
+  const uint16_t* occ;   // occurrence lists (shared)
+  const uint16_t* start; // start[x] .. start[x+1] (shared)
+  int n;
+
+  __device__ __forceinline__ int lookup(int idx) const {
+    if (SMEM_TAB) return lds_u16(tab_s + 2u * (uint32_t)idx);
+    return (int)__ldg(tab + idx);
+  }
+
+  // Score change contributed by position i for the interchange a<->b (a, b plaintext
+  // letters, i holds a or b): windows containing i whose first touched position is i.
+  __device__ __forceinline__ int position_delta(int i, uint32_t arep, uint32_t brep) const {
+    // bytes plain[i-(G-1)] .. plain[i+(G-1)] as lo (bytes 0..3) and hi (bytes 4..7),
+    // starting at buffer offset 4 + i - 3 = i + 1 (G = 4; smaller G use a subset)
+    const uint32_t off = (uint32_t)(i + 1);
+    const uint32_t wa = text_base + (off & ~3u);
+    const uint32_t w0 = lds_u32(wa), w1 = lds_u32(wa + 4), w2 = lds_u32(wa + 8);
+    const uint32_t sh = (off & 3u) * 8u;
+    const uint32_t lo = __funnelshift_r(w0, w1, sh), hi = __funnelshift_r(w1, w2, sh);
+    // byte j of (lo,hi) is plain[i - 3 + j]; the centre is byte 3
+    const uint32_t ma_lo = eq_bytes(lo, arep), mb_lo = eq_bytes(lo, brep);
+    const uint32_t ma_hi = eq_bytes(hi, arep), mb_hi = eq_bytes(hi, brep);
+    const uint32_t ea_lo = expand_mask(ma_lo), eb_lo = expand_mask(mb_lo);
+    const uint32_t ea_hi = expand_mask(ma_hi), eb_hi = expand_mask(mb_hi);
+    const uint32_t nlo = (lo & ~(ea_lo | eb_lo)) | (brep & ea_lo) | (arep & eb_lo);
+    const uint32_t nhi = (hi & ~(ea_hi | eb_hi)) | (brep & ea_hi) | (arep & eb_hi);
+    // touched bytes before the centre: bits of (ma|mb) in bytes 0..2 of lo
+    const uint32_t touched_lo = (ma_lo | mb_lo) >> 7;  // bit 8j set for touched byte j
+    int delta = 0;
+    // window k covers bytes 3-(G-1)+k .. 3+k (k = 0..G-1), start s = i-(G-1)+k
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      const int s = i - (G - 1) + k;
+      const int first = 3 - (G - 1) + k;  // first byte of the window
+      // no touched byte in [first, 3) (positions s .. i-1)
+      uint32_t before = 0;
+#pragma unroll
+      for (int j = first; j < 3; ++j) before |= touched_lo & (1u << (8 * j));
+      const bool valid = s >= 0 && s + G <= n && before == 0;
+      if (valid) {
+        int io = 0, in = 0;
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          const int b = first + j;
+          const uint32_t ob = b < 4 ? (lo >> (8 * b)) & 0xffu : (hi >> (8 * (b - 4))) & 0xffu;
+          const uint32_t nb = b < 4 ? (nlo >> (8 * b)) & 0xffu : (nhi >> (8 * (b - 4))) & 0xffu;
+          io = io * kAlpha + (int)ob;
+          in = in * kAlpha + (int)nb;
+        }
+        delta += lookup(in) - lookup(io);
+      }
+    }
+    return delta;
+  }
+
+  // touched position j (0 <= j < na + nb) of the interchange with cipher letters xa, xb
+  __device__ __forceinline__ int touched(int j, int sa, int na, int sb) const {
+    return j < na ? (int)occ[sa + j] : (int)occ[sb + j - na];
+  }
+};
+
+template <int G, bool SMEM_TAB>
+__global__ void __launch_bounds__(kNgWarps * 32) mas_ngram_kernel(const MasNgramLaunch p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kTab = pow26(G);
+  uint32_t tab_bytes = 0;
+  if (SMEM_TAB) {
+    uint16_t* stab = reinterpret_cast<uint16_t*>(smem_raw);
+    for (int i = threadIdx.x; i < kTab; i += blockDim.x) stab[i] = p.table[i];
+    tab_bytes = ((uint32_t)kTab * 2u + 15u) & ~15u;
+    __syncthreads();
+  }
+  const int max_len = (int)p.max_len;
+  unsigned char* wb = smem_raw + tab_bytes + (size_t)warp * ng_warp_bytes(max_len);
+  uint8_t* text = wb;  // plain[i] at text[4 + i]
+  uint16_t* occ = reinterpret_cast<uint16_t*>(wb + ng_text_stride(max_len));
+  uint16_t* start = reinterpret_cast<uint16_t*>(wb + ng_text_stride(max_len) +
+                                                ((2u * (uint32_t)max_len + 15u) & ~15u));
+  uint32_t* cursor = reinterpret_cast<uint32_t*>(start + 32);
+
+  NgState<G, SMEM_TAB> st;
+  st.tab = p.table;
+  st.tab_s = smem_addr(smem_raw);
+  st.text_base = smem_addr(text);
+  st.occ = occ;
+  st.start = start;
+
+  const int64_t stride = (int64_t)gridDim.x * kNgWarps;
+  const uint32_t climbings = (uint32_t)p.climbings;
+  const int g8 = lane >> 3, sl = lane & 7;
+
+  for (int64_t w = (int64_t)blockIdx.x * kNgWarps + warp; w < p.n_workers; w += stride) {
+    const int32_t cid = p.cipher_of[w];
+    const int64_t off = p.offsets[cid];
+    const int n = (int)(p.offsets[cid + 1] - off);
+    const uint8_t* ct = p.ciphers + off;
+    st.n = n;
+
+    // plaintext := ciphertext (the worker starts at the ciphertext, mas.py:229)
+    for (int i = lane; i < n + 12; i += 32) text[i] = (i >= 4 && i < n + 4) ? ct[i - 4] : 0xff;
+    cursor[lane] = 0;
+    __syncwarp();
+    // occurrence lists: counting sort of positions by cipher letter
+    for (int i = lane; i < n; i += 32) atomicAdd(&cursor[ct[i]], 1u);
+    __syncwarp();
+    {
+      const int c = (int)cursor[lane];
+      int inc = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += u;
+      }
+      start[lane] = (uint16_t)(inc - c);  // lanes >= 26: start = n
+      cursor[lane] = (uint32_t)(inc - c);
+    }
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) occ[atomicAdd(&cursor[ct[i]], 1u)] = (uint16_t)i;
+    __syncwarp();
+
+    // initial score (mas.py:232)
+    int64_t score = 0;
+    {
+      int part = 0;
+      for (int s = lane; s + G <= n; s += 32) {
+        int idx = 0;
+#pragma unroll
+        for (int j = 0; j < G; ++j) idx = idx * kAlpha + text[4 + s + j];
+        part += st.lookup(idx);
+      }
+      // partial sums < 32 x ceil(n/32) x 65535 < 2^31 for n <= 32768
+      score = (int64_t)(int)__reduce_add_sync(kFull, (uint32_t)part);
+    }
+    int pinv = lane < kAlpha ? lane : 0;  // pi^-1(lane): the cipher letter holding plaintext lane
+
+    ByteWindow win;
+    win.key = p.keys + 2 * w;
+    win.base = p.skips ? p.skips[w] : 0;
+    win.o = 0;
+    win.refill(lane);
+
+    // group-of-W evaluation of the interchange (a, b): every lane of the group gets the sum
+    auto eval_group = [&](uint32_t a, uint32_t b) -> int {
+      const int xa = __shfl_sync(kFull, pinv, (int)a), xb = __shfl_sync(kFull, pinv, (int)b);
+      const int sa = start[xa], na = (int)start[xa + 1] - sa;
+      const int sb = start[xb], nb = (int)start[xb + 1] - sb;
+      const uint32_t arep = a * 0x01010101u, brep = b * 0x01010101u;
+      int d = 0;
+      for (int j = sl; j < na + nb; j += 8) d += st.position_delta(st.touched(j, sa, na, sb), arep, brep);
+      d += __shfl_xor_sync(kFull, d, 1);
+      d += __shfl_xor_sync(kFull, d, 2);
+      d += __shfl_xor_sync(kFull, d, 4);
+      return d;
+    };
+    auto eval_one = [&](uint32_t a, uint32_t b) -> int {
+      const int xa = __shfl_sync(kFull, pinv, (int)a), xb = __shfl_sync(kFull, pinv, (int)b);
+      const int sa = start[xa], na = (int)start[xa + 1] - sa;
+      const int sb = start[xb], nb = (int)start[xb + 1] - sb;
+      const uint32_t arep = a * 0x01010101u, brep = b * 0x01010101u;
+      int d = 0;
+      for (int j = lane; j < na + nb; j += 32) d += st.position_delta(st.touched(j, sa, na, sb), arep, brep);
+      return (int)__reduce_add_sync(kFull, (uint32_t)d);
+    };
+    // commit a<->b (mas.py:237-243)
+    auto accept = [&](int a, int b, int d) {
+      score += d;
+      const int xa = __shfl_sync(kFull, pinv, a), xb = __shfl_sync(kFull, pinv, b);
+      const int sa = start[xa], na = (int)start[xa + 1] - sa;
+      const int sb = start[xb], nb = (int)start[xb + 1] - sb;
+      __syncwarp();
+      for (int j = lane; j < na + nb; j += 32) {
+        const int i = st.touched(j, sa, na, sb);
+        text[4 + i] = (uint8_t)(j < na ? b : a);
+      }
+      if (lane == a) pinv = xb;
+      if (lane == b) pinv = xa;
+      __syncwarp();
+    };
+    auto improvable = [&]() {
+      for (uint32_t a2 = 0; a2 < kAlpha - 1; ++a2)
+        for (uint32_t b2 = a2 + 1; b2 < kAlpha; ++b2)
+          if (eval_one(a2, b2) > 0) return true;
+      return false;
+    };
+
+    int last = -1;
+    uint32_t t = 0, since = 0, next_check = 256;
+    bool dirty = false;
+    auto step = [&](uint32_t a, uint32_t b, int dd) -> bool {
+      if (a == b) return false;
+      const int d = dirty ? eval_one(a, b) : dd;
+      win.o += 2;
+      if (d > 0) {
+        accept((int)a, (int)b, d);
+        last = (int)t;
+        dirty = true;
+        since = 0;
+        next_check = 256;
+      } else {
+        ++since;
+      }
+      ++t;
+      return true;
+    };
+    while (t + 3 < climbings) {
+      if (win.o > 120) win.refill(lane);
+      uint32_t La, Lb;
+      win.peek8(La, Lb);
+      // group g takes pair g: bytes (2g, 2g+1) of La:Lb
+      const uint32_t Lg = g8 < 2 ? La : Lb;
+      const uint32_t ga = (Lg >> (16 * (g8 & 1))) & 0xffu, gb = (Lg >> (16 * (g8 & 1) + 8)) & 0xffu;
+      const int dg = eval_group(ga, gb);
+      const int d1 = __shfl_sync(kFull, dg, 0), d2 = __shfl_sync(kFull, dg, 8);
+      const int d3 = __shfl_sync(kFull, dg, 16), d4 = __shfl_sync(kFull, dg, 24);
+      const uint32_t a1 = La & 0xffu, b1 = (La >> 8) & 0xffu, a2 = (La >> 16) & 0xffu, b2 = La >> 24;
+      const uint32_t a3 = Lb & 0xffu, b3 = (Lb >> 8) & 0xffu, a4 = (Lb >> 16) & 0xffu, b4 = Lb >> 24;
+      const bool ok = a1 != b1 && a2 != b2 && a3 != b3 && a4 != b4;
+      if (ok && max(max(d1, d2), max(d3, d4)) <= 0) {
+        win.o += 8;
+        t += 4;
+        if (p.flags & CCG_FLAG_EARLY_EXIT) {
+          since += 4;
+          if (since >= next_check) {
+            if (!improvable()) break;
+            next_check *= 4;
+          }
+        }
+        continue;
+      }
+      dirty = false;
+      if (!(step(a1, b1, d1) && step(a2, b2, d2) && step(a3, b3, d3) && step(a4, b4, d4))) {
+        int a, b;
+        win.pair(lane, a, b);  // a redraw is due (rng.py:81-89)
+        const int d = eval_one((uint32_t)a, (uint32_t)b);
+        if (d > 0) {
+          accept(a, b, d);
+          last = (int)t;
+          since = 0;
+          next_check = 256;
+        } else {
+          ++since;
+        }
+        ++t;
+      }
+      if ((p.flags & CCG_FLAG_EARLY_EXIT) && since >= next_check) {
+        if (!improvable()) break;
+        next_check *= 4;
+      }
+    }
+    const bool done = (p.flags & CCG_FLAG_EARLY_EXIT) && t + 3 < climbings;
+    while (!done && t < climbings) {
+      int a, b;
+      win.pair(lane, a, b);
+      const int d = eval_one((uint32_t)a, (uint32_t)b);
+      if (d > 0) {
+        accept(a, b, d);
+        last = (int)t;
+      }
+      ++t;
+    }
+
+    if (lane < kAlpha && p.maps) p.maps[w * kAlpha + pinv] = (uint8_t)lane;
+    if (lane == 0) {
+      p.scores[w] = score;
+      if (p.draws_used) p.draws_used[w] = win.position();
+      if (p.last_accept) p.last_accept[w] = last;
+      if (p.tries_done) p.tries_done[w] = t;
+    }
+    __syncwarp();
+  }
+}
+
+template <int G, bool SMEM_TAB>
+cudaError_t launch_ng(cudaStream_t s, const MasNgramLaunch& p, int sm_count) {
+  auto kern = mas_ngram_kernel<G, SMEM_TAB>;
+  const size_t tab = SMEM_TAB ? (((size_t)pow26(G) * 2 + 15) & ~(size_t)15) : 0;
+  const size_t bytes = tab + (size_t)kNgWarps * ng_warp_bytes((int)p.max_len);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNgWarps * 32, bytes);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t need = (p.n_workers + kNgWarps - 1) / kNgWarps;
+  const int64_t resident = (int64_t)per_sm * sm_count;
+  const int grid = (int)(need < resident ? need : resident);
+  kern<<<grid, kNgWarps * 32, bytes, s>>>(p);
+  return cudaGetLastError();
+}
+
+// ngrams.py:134-140 generalised to order G: one warp per text, int64 sum.
+__global__ void ngram_score_kernel(const uint8_t* __restrict__ texts, const int64_t* __restrict__ offsets,
+                                   int64_t n_texts, int order, const int64_t* __restrict__ table,
+                                   int64_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (j >= n_texts) return;
+  const int64_t off = offsets[j], n = offsets[j + 1] - off;
+  long long part = 0;
+  for (int64_t s = lane; s + order <= n; s += 32) {
+    int64_t idx = 0;
+    for (int q = 0; q < order; ++q) idx = idx * kAlpha + texts[off + s + q];
+    part += table[idx];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
+  if (lane == 0) out[j] = part;
+}
+
+}  // namespace
+
+size_t mas_ngram_smem_bytes(int order, int64_t max_len) {
+  const size_t tab = order <= 3 ? (((size_t)pow26(order) * 2 + 15) & ~(size_t)15) : 0;
+  return tab + (size_t)kNgWarps * ng_warp_bytes((int)max_len);
+}
+
+cudaError_t launch_mas_ngram_climb(cudaStream_t s, const MasNgramLaunch& p, int sm_count) {
+  if (p.n_workers <= 0) return cudaSuccess;
+  switch (p.order) {
+    case 2: return launch_ng<2, true>(s, p, sm_count);
+    case 3: return launch_ng<3, true>(s, p, sm_count);
+    case 4: return launch_ng<4, false>(s, p, sm_count);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_ngram_score(cudaStream_t s, const uint8_t* texts, const int64_t* offsets,
+                               int64_t n, int order, const int64_t* table, int64_t* out) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t threads = n * 32;
+  ngram_score_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(texts, offsets, n, order,
+                                                                        table, out);
+  return cudaGetLastError();
+}
+
+}  // namespace ccg

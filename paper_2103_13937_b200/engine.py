@@ -90,15 +90,26 @@ def _concat(parts, name):
 
 def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, group_size=0,
               draws_used=False, last_accept=False, tries_done=False, early_exit=False,
-              devices_=None) -> ClimbResult:
+              order=2, ngram_kernel=False, devices_=None) -> ClimbResult:
     """Run stochastic_worker (mas.py:218-244) for every worker on the GPU(s).
 
     ciphers: list of letter arrays; cipher_of: int per worker; keys: uint64[n, 2] Philox
-    keys (rng.philox_keys); table_scores: int64[676]."""
+    keys (rng.philox_keys); table_scores: int64[26**order].  order 2 runs the bigram kernels
+    (ccg_mas_climb); order 3/4 -- or ngram_kernel=True at order 2 -- the position-based
+    n-gram kernel (ccg_mas_ngram_climb, entries must fit uint16)."""
     flat, off = _lib.ragged(ciphers)
     cof = np.ascontiguousarray(cipher_of, dtype=np.int32).reshape(-1)
     keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, 2)
-    table = np.ascontiguousarray(table_scores, dtype=np.int64)
+    order = int(order)
+    use_ng = ngram_kernel or order != 2
+    table = np.ascontiguousarray(table_scores, dtype=np.int64).reshape(-1)
+    if table.size != 26**order:
+        raise ValueError(f"expected {26**order} table entries for order {order}, got {table.size}")
+    if use_ng:
+        if table.size and (table.min() < 0 or table.max() > 65535):
+            raise _lib.EngineError("the n-gram kernel takes table entries in 0..65535 "
+                                   "(quantise the table with ngrams.quantize_log_table)")
+        table = np.ascontiguousarray(table, dtype=np.uint16)
     n = cof.size
     if keys.shape[0] != n:
         raise ValueError("one Philox key per worker required")
@@ -121,7 +132,7 @@ def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, 
         c_of = np.ascontiguousarray(cof[lo:hi])
         k = np.ascontiguousarray(keys[lo:hi])
         s = None if sk is None else np.ascontiguousarray(sk[lo:hi])
-        a = _lib.MasClimbArgs()
+        a = _lib.MasNgramArgs() if use_ng else _lib.MasClimbArgs()
         a.ciphers, a.offsets, a.n_ciphers = _lib.ptr(flat), _lib.ptr(off), off.size - 1
         a.cipher_of, a.keys, a.skips = _lib.ptr(c_of), _lib.ptr(k), _lib.ptr(s)
         a.n_workers, a.climbings, a.table = m, int(climbings), _lib.ptr(table)
@@ -130,10 +141,13 @@ def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, 
         a.tries_done = _lib.ptr(out.tries_done)
         a.group_size, a.group_best = int(group_size), _lib.ptr(out.group_best)
         a.flags = _lib.FLAG_EARLY_EXIT if early_exit else 0
+        if use_ng:
+            a.order = order
         ctx = _lib.context(dev)
         with ctx.lock:
             before = ctx.launches()
-            _lib.check(_lib.load().ccg_mas_climb(ctx.handle, a), "mas_climb")
+            fn = _lib.load().ccg_mas_ngram_climb if use_ng else _lib.load().ccg_mas_climb
+            _lib.check(fn(ctx.handle, a), "mas_climb")
             out.launches = ctx.launches() - before
         return out
 
@@ -317,3 +331,18 @@ def mas_det_solve(ciphers, cipher_of, keys, table_scores, iterations, *, devices
                      history=[h for p in parts for h in p.history],
                      draws_used=np.concatenate([p.draws_used for p in parts]),
                      launches=sum(p.launches for p in parts))
+
+
+def ngram_score_batch(texts, order, table_scores) -> np.ndarray:
+    """Integer n-gram fitness (ngrams.py:134-140 generalised to order-n windows) on the GPU."""
+    flat, off = _lib.ragged(texts)
+    table = np.ascontiguousarray(table_scores, dtype=np.int64).reshape(-1)
+    if table.size != 26**int(order):
+        raise ValueError(f"expected {26**int(order)} table entries")
+    out = np.empty(off.size - 1, dtype=np.int64)
+    ctx = _lib.context(default_device())
+    with ctx.lock:
+        _lib.check(_lib.load().ccg_ngram_score_batch(ctx.handle, _lib.ptr(flat), _lib.ptr(off),
+                                                     off.size - 1, int(order), _lib.ptr(table),
+                                                     _lib.ptr(out)), "ngram_score")
+    return out

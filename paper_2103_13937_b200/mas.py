@@ -7,6 +7,11 @@ iteration loop on the device (csrc/ccg_mas_det.cu).  Signatures, defaults, valid
 result objects follow the reference so this module drops in for it; `jobs` is accepted
 for signature compatibility and has no effect on results (the reference guarantees the
 same: search.py:4-7).
+
+n-gram extension: every stochastic entry point also accepts an ngrams.NgramTable of order
+3 or 4 (BASELINE.json configs 4-5; the reference has bigrams only); the climb
+then runs the position-based n-gram kernel (csrc/ccg_mas_ngram.cu) with the same proposal
+stream and accept rule.
 """
 from __future__ import annotations
 
@@ -17,7 +22,7 @@ import numpy as np
 
 from . import engine
 from .codec import ALPHABET_SIZE, MappedText
-from .ngrams import BigramTable
+from .ngrams import BigramTable, as_ngram_table
 from .pairs import PAIR_TOTAL, index_to_pair
 from .rng import WorkerRng, philox_keys, pivot_stream_index, worker_stream_index
 from .search import RestartSummary, SolveResult, fold_restarts
@@ -77,7 +82,8 @@ def stochastic_worker(cipher: MappedText, table: BigramTable, climbings: int,
     """One worker's climb from the ciphertext (mas.py:218-244) as a one-warp GPU launch.
     `state` is advanced by exactly the draws the worker consumed."""
     text = np.asarray(cipher, dtype=np.int64)
-    res = engine.mas_climb([text], [0], [state.key], table.scores, climbings,
+    t = as_ngram_table(table)
+    res = engine.mas_climb([text], [0], [state.key], t.scores, climbings, order=t.order,
                            skips=[state.position], draws_used=True)
     state.advance(int(res.draws_used[0]))
     return res.keys[0].astype(np.int64)[text], int(res.scores[0])
@@ -88,8 +94,9 @@ def _restart_batch(text, table, cfg, restarts, early_exit=True):
     W = cfg.workers
     streams = [worker_stream_index(r, w) for r in restarts for w in range(W)]
     keys = philox_keys([cfg.global_seed], streams)
-    res = engine.mas_climb([text], np.zeros(len(streams), np.int32), keys, table.scores,
-                           cfg.climbings, group_size=W, early_exit=early_exit)
+    t = as_ngram_table(table)
+    res = engine.mas_climb([text], np.zeros(len(streams), np.int32), keys, t.scores,
+                           cfg.climbings, order=t.order, group_size=W, early_exit=early_exit)
     out = []
     for i, _ in enumerate(restarts):
         sc = res.scores[i * W:(i + 1) * W]

@@ -168,3 +168,147 @@ def score_text(text: MappedText, table: BigramTable) -> int:
 def log_score_text(text: MappedText, table: LogBigramTable) -> float:
     """Sum of log2 bigram probabilities (ngrams.py:166-172), on the GPU, bit-exact."""
     return float(log_score_text_batch([text], table)[0])
+
+
+# ------------------------------------------------------------------ n-gram extension
+# The reference implements bigrams only (SPEC.md:182, ngrams.py:21).  BASELINE.json's
+# configs 3-5 ask for trigram and quadgram scoring; these classes generalise the bigram ones
+# with the same conventions: index sum_j 26^(order-1-j) t_j (order 2 == bigram_index),
+# non-negative integer scores summed over the text's windows, log2(count/total) with unseen
+# n-grams at a floor below the rarest observed one.
+def ngram_index(letters) -> int:
+    idx = 0
+    for x in letters:
+        x = int(x)
+        if not 0 <= x < ALPHABET_SIZE:
+            raise ValueError(f"letter index out of range: {x}")
+        idx = idx * ALPHABET_SIZE + x
+    return idx
+
+
+def _window_index(t: np.ndarray, order: int) -> np.ndarray:
+    m = t.size - order + 1
+    idx = np.zeros(max(0, m), dtype=np.int64)
+    for j in range(order):
+        idx = idx * ALPHABET_SIZE + t[j:j + m]
+    return idx
+
+
+def _check_order(order: int) -> int:
+    order = int(order)
+    if not 2 <= order <= 4:
+        raise ValueError(f"n-gram order must be 2, 3 or 4, got {order}")
+    return order
+
+
+@dataclass(frozen=True)
+class NgramTable:
+    """26**order non-negative integer scores indexed by ngram_index (order 2 = BigramTable)."""
+
+    order: int
+    scores: np.ndarray
+
+    def __post_init__(self):
+        order = _check_order(self.order)
+        arr = np.ascontiguousarray(self.scores, dtype=np.int64)
+        if arr.shape != (ALPHABET_SIZE**order,):
+            raise ValueError(f"expected {ALPHABET_SIZE**order} entries, got {arr.shape}")
+        if arr.size and arr.min() < 0:
+            raise ValueError("n-gram scores must be non-negative")
+        object.__setattr__(self, "order", order)
+        object.__setattr__(self, "scores", arr)
+
+
+@dataclass(frozen=True)
+class LogNgramTable:
+    """26**order log2 n-gram probabilities; unseen n-grams sit at `floor`."""
+
+    order: int
+    logs: np.ndarray
+    floor: float
+
+    def __post_init__(self):
+        order = _check_order(self.order)
+        arr = np.ascontiguousarray(self.logs, dtype=np.float64)
+        if arr.shape != (ALPHABET_SIZE**order,):
+            raise ValueError(f"expected {ALPHABET_SIZE**order} entries, got {arr.shape}")
+        if not np.isfinite(arr).all():
+            raise ValueError("log scores must be finite")
+        if arr.size and arr.max() > 0:
+            raise ValueError("log2 probabilities cannot be positive")
+        if arr.size and arr.min() < self.floor:
+            raise ValueError("log table entries below the configured floor")
+        object.__setattr__(self, "order", order)
+        object.__setattr__(self, "logs", arr)
+
+
+def as_ngram_table(table) -> NgramTable:
+    """BigramTable -> NgramTable(2, ...); NgramTable passes through."""
+    if isinstance(table, NgramTable):
+        return table
+    if isinstance(table, BigramTable):
+        return NgramTable(2, table.scores)
+    raise TypeError(f"not a score table: {type(table).__name__}")
+
+
+def as_log_ngram_table(table) -> LogNgramTable:
+    if isinstance(table, LogNgramTable):
+        return table
+    if isinstance(table, LogBigramTable):
+        return LogNgramTable(2, table.logs, table.floor)
+    raise TypeError(f"not a log table: {type(table).__name__}")
+
+
+def build_ngram_table_from_corpus(corpus: str, order: int) -> NgramTable:
+    """Count the normalized corpus's windows of `order` letters (build_table_from_corpus,
+    ngrams.py:124-131, generalised)."""
+    order = _check_order(order)
+    sym = map_text(normalize(corpus))
+    counts = np.zeros(ALPHABET_SIZE**order, dtype=np.int64)
+    if sym.size >= order:
+        counts = np.bincount(_window_index(sym, order), minlength=ALPHABET_SIZE**order)
+    return NgramTable(order, counts.astype(np.int64))
+
+
+def build_log_ngram_table(table: NgramTable, floor: float = DEFAULT_LOG_FLOOR) -> LogNgramTable:
+    """log2(count / total); zero counts get `floor` (ngrams.py:143-163 generalised)."""
+    table = as_ngram_table(table)
+    if floor >= 0:
+        raise ValueError("floor must be negative")
+    total = int(table.scores.sum())
+    if total == 0:
+        raise ValueError("cannot build probabilities from an all-zero table")
+    seen = table.scores > 0
+    logs = np.full(table.scores.size, floor, dtype=np.float64)
+    logs[seen] = np.log2(table.scores[seen] / total)
+    if seen.any() and logs[seen].min() < floor:
+        raise ValueError(
+            f"floor {floor} is above the rarest observed n-gram ({float(logs[seen].min()):.3f}); "
+            "pass a lower floor"
+        )
+    return LogNgramTable(table.order, logs, floor)
+
+
+def quantize_log_table(table, max_value: int = 65535) -> NgramTable:
+    """Integer fitness table for the MAS climb: the affine map [floor, 0] -> [0, max_value]
+    of the log2 probabilities, rounded.  For a fixed text length the integer score is an
+    increasing affine function of the (rounded) log-probability sum, so the climb ranks
+    candidates as the log score does; entries fit the kernels' uint16 tables."""
+    t = as_log_ngram_table(table)
+    if not 1 <= int(max_value) <= 65535:
+        raise ValueError("max_value must lie in 1..65535")
+    q = np.rint((t.logs - t.floor) / (-t.floor) * int(max_value)).astype(np.int64)
+    return NgramTable(t.order, np.clip(q, 0, int(max_value)))
+
+
+def ngram_score_text_batch(texts, table) -> np.ndarray:
+    """Integer n-gram fitness of many texts in one GPU call."""
+    t = as_ngram_table(table)
+    from .engine import ngram_score_batch
+
+    return ngram_score_batch(texts, t.order, t.scores)
+
+
+def ngram_score_text(text: MappedText, table) -> int:
+    """Sum of table entries over the text's windows (score_text generalised), on the GPU."""
+    return int(ngram_score_text_batch([text], table)[0])

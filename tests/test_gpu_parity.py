@@ -436,3 +436,99 @@ def test_solve_with_restarts_deterministic_fold_and_stop(golden):
     best2, summ2 = cc.solve_with_restarts(cipher, cc.BigramTable(table), cfg,
                                           stop=lambda res: res.restart_index == 1)
     assert len(summ2) == 2
+
+
+# ------------------------------------------------------------------ n-gram extension (orders 2-4)
+def test_ngram_kernel_order2_matches_reference_workers(golden):
+    # the position-based n-gram kernel at order 2 must reproduce the reference's own
+    # stochastic_worker outputs (tables fit uint16)
+    cases = [c for c in golden.mas_worker_cases(O.permutation) if c[1].max() <= 65535]
+    assert len(cases) >= 20
+    for cipher, table, climb, seed, stream, want_text, want_score in cases:
+        res = engine.mas_climb([cipher], [0], [philox_key(seed, stream)], table, climb,
+                               ngram_kernel=True)
+        assert int(res.scores[0]) == want_score
+        assert np.array_equal(res.keys[0].astype(np.int64)[cipher], want_text)
+
+
+def _ngram_cases(rng, order, n_cases=40):
+    ciphers = []
+    for i in range(n_cases):
+        L = int(rng.choice([0, 1, order - 1, order, order + 1, 5, 17, 60, 100, 333, 600, 4096]))
+        ciphers.append(rng.integers(0, int(rng.choice([3, 8, 26])), L))
+    return ciphers
+
+
+@pytest.mark.parametrize("order", [2, 3, 4])
+def test_ngram_climb_vs_oracle(order):
+    rng = np.random.default_rng(100 + order)
+    ciphers = _ngram_cases(rng, order)
+    for table in (rng.integers(0, 65536, 26**order), rng.integers(0, 50, 26**order)):
+        seeds = [int(rng.integers(0, 2**63)) for _ in ciphers]
+        streams = [int(rng.integers(0, 2**40)) for _ in ciphers]
+        keys = np.array([philox_key(s, w) for s, w in zip(seeds, streams)], dtype=np.uint64)
+        res = engine.mas_climb(ciphers, np.arange(len(ciphers)), keys, table, 1500, order=order,
+                               draws_used=True, last_accept=True)
+        want_s, want_m = O.ngram_workers(ciphers, np.arange(len(ciphers)), seeds, streams, order,
+                                         table, 1500)
+        assert res.scores.tolist() == want_s.tolist()
+        for i, c in enumerate(ciphers):
+            assert np.array_equal(res.keys[i].astype(np.int64)[c], want_m[i][c]), i
+
+
+def test_ngram_climb_english_quadgram_and_early_exit(golden):
+    corpus = "".join(chr(97 + int(x)) for x in golden.corpus())
+    q4 = cc.quantize_log_table(cc.build_log_ngram_table(cc.build_ngram_table_from_corpus(corpus, 4)))
+    rng = np.random.default_rng(5)
+    plain = golden.plain_mas(471)
+    ciphers = []
+    for L in (60, 80, 100, 300, 471):
+        key = rng.permutation(26)
+        ciphers.append(key[plain[:L]])
+    cof = np.repeat(np.arange(len(ciphers), dtype=np.int32), 8)
+    seeds = [4242] * cof.size
+    streams = list(range(cof.size))
+    keys = philox_keys([4242], streams)
+    full = engine.mas_climb(ciphers, cof, keys, q4.scores, 6000, order=4, group_size=8,
+                            tries_done=True)
+    want_s, _ = O.ngram_workers(ciphers, cof, seeds, streams, 4, q4.scores, 6000)
+    assert full.scores.tolist() == want_s.tolist()
+    early = engine.mas_climb(ciphers, cof, keys, q4.scores, 6000, order=4, group_size=8,
+                             tries_done=True, early_exit=True)
+    assert early.scores.tolist() == full.scores.tolist()   # the early exit is exact
+    assert np.array_equal(early.keys, full.keys)
+    assert (early.tries_done <= 6000).all() and early.tries_done.min() < 6000
+    assert early.group_best.tolist() == [int(np.argmax(want_s[i:i + 8])) for i in range(0, cof.size, 8)]
+
+
+def test_ngram_skips_continue_the_stream():
+    rng = np.random.default_rng(8)
+    table = rng.integers(0, 1000, 26**3)
+    c = rng.integers(0, 26, 150)
+    key = philox_key(77, 3)
+    a = engine.mas_climb([c], [0], [key], table, 700, order=3, draws_used=True)
+    _, s_o, _, _ = O.ngram_worker(c, 3, table, 700, 77, 3, skip=int(a.draws_used[0]))
+    b = engine.mas_climb([c], [0], [key], table, 700, order=3, skips=a.draws_used)
+    assert int(b.scores[0]) == s_o
+
+
+@pytest.mark.parametrize("order", [2, 3, 4])
+def test_ngram_score_batch_vs_oracle(order):
+    rng = np.random.default_rng(order)
+    table = rng.integers(0, 2**40, 26**order)
+    texts = [rng.integers(0, 26, int(L)) for L in rng.integers(0, 3000, 50)] + [np.zeros(0, int)]
+    got = cc.ngram_score_text_batch(texts, cc.NgramTable(order, table))
+    assert got.tolist() == [O.ngram_score_text(t, order, table) for t in texts]
+
+
+def test_solve_stochastic_with_trigram_table():
+    rng = np.random.default_rng(12)
+    table = cc.NgramTable(3, rng.integers(0, 3000, 26**3))
+    cipher = rng.integers(0, 26, 250)
+    cfg = cc.MasSolverConfig(workers=16, climbings=3000, global_seed=99, restarts=2)
+    best, summ = cc.solve_with_restarts(cipher, table, cfg)
+    for r in range(2):
+        want, _ = O.ngram_workers([cipher], np.zeros(16, np.int32), [99] * 16,
+                                  [(r << 32) | w for w in range(16)], 3, table.scores, 3000)
+        assert summ[r].score == int(want.max())
+    assert best.best_score == cc.ngram_score_text(best.best_text, table)

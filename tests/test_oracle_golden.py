@@ -178,3 +178,57 @@ def test_solve_deterministic_matches_reference(golden):
         got_t, got_s, got_h = O.solve_deterministic(cipher, table, iters, seed, r)
         assert got_s == score and got_h == hist
         assert np.array_equal(got_t, text)
+
+
+# ------------------------------------------------------------------ n-gram generalisation
+# The reference has bigrams only.  The order-n oracle functions must reduce to
+# the reference at order 2 (pinned here against the reference's own outputs); orders 3 and 4
+# are checked against direct numpy restatements.
+def test_ngram_order2_reduces_to_reference(golden):
+    g = golden.load("scoring")
+    eng, logs = golden.english_scores(), golden.english_logs()
+    for i, t in enumerate(golden.scoring_texts()):
+        assert O.ngram_score_text(t, 2, eng) == g["eng_scores"][i]
+        assert O.ngram_log_score_text(t, 2, logs) == g["log_scores"][i]
+    for cipher, table, climb, seed, stream, want_text, want_score in \
+            golden.mas_worker_cases(O.permutation)[:12]:
+        text, score, mapping, _ = O.ngram_worker(cipher, 2, table, climb, seed, stream)
+        assert score == want_score and np.array_equal(text, want_text)
+
+
+def _np_index(t, order):
+    idx = np.zeros(t.size - order + 1, dtype=np.int64)
+    for j in range(order):
+        idx = idx * 26 + t[j:t.size - order + 1 + j]
+    return idx
+
+
+@pytest.mark.parametrize("order", [3, 4])
+def test_ngram_scores_vs_numpy(order):
+    rng = np.random.default_rng(order)
+    table = rng.integers(0, 30_000, 26**order)
+    logs = -rng.random(26**order) * 20 - 1
+    for L in [0, 1, order - 1, order, order + 1, 7, 64, 129, 300, 1000]:
+        t = rng.integers(0, 26, L)
+        want_i = int(table[_np_index(t, order)].sum()) if L >= order else 0
+        want_f = float(logs[_np_index(t, order)].sum()) if L >= order else 0.0
+        assert O.ngram_score_text(t, order, table) == want_i
+        assert O.ngram_log_score_text(t, order, logs) == want_f  # numpy pairwise order
+
+
+@pytest.mark.parametrize("order", [3, 4])
+def test_ngram_worker_semantics(order):
+    # replay the worker's own draws (oracle Philox is pinned) with a numpy full rescore
+    rng = np.random.default_rng(10 + order)
+    table = rng.integers(0, 1000, 26**order)
+    cipher = rng.integers(0, 26, 90)
+    text, score, mapping, last = O.ngram_worker(cipher, order, table, 400, 5, 9)
+    pairs = O.distinct_pairs(5, 9, 26, 400)
+    cur = cipher.copy()
+    cs = int(table[_np_index(cur, order)].sum())
+    for a, b in pairs:
+        cand = np.where(cur == a, b, np.where(cur == b, a, cur))
+        s = int(table[_np_index(cand, order)].sum())
+        if s > cs:
+            cur, cs = cand, s
+    assert score == cs and np.array_equal(text, cur) and np.array_equal(mapping[cipher], cur)
