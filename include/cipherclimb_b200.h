@@ -22,6 +22,8 @@
  *   ccg_mas_det_solve[_dev]                      mas.py:140-169 solve_deterministic, a batch of
  *                                                (ciphertext, restart) jobs, whole loop on device
  *   ccg_sct_score_batch                          sct.py:158-160 candidate_score (ciphers.py:71-86,107-113)
+ *   ccg_ngram_log_score_batch                    ngrams.py:166-172 generalised to order-n windows
+ *   ccg_sct_score_ngram_batch                    sct.py:158-160 with an order-n log table
  *   ccg_sct_climb[_dev]                          sct.py:173-176 _sct_task -> sct.py:148-170 sct_worker,
  *                                                for a whole batch (sct.py:194-200) + max_element
  *
@@ -220,7 +222,18 @@ typedef struct {
   int64_t *group_best;
   int64_t text_len;           /* required by ccg_sct_climb_dev: the common ciphertext length */
   uint32_t flags;
+  int32_t order;              /* n-gram order of `logs` ([26^order]): 0 or 2 = bigram (reference),
+                                 3 = trigram, 4 = quadgram (extension) */
 } ccg_sct_climb_args;
+
+/* n-gram extension of the two scoring entry points above: logs float64[26^order], windows of
+ * `order` letters, numpy pairwise order over the n-order+1 window terms. */
+int ccg_ngram_log_score_batch(ccg_ctx *ctx, const uint8_t *texts, const int64_t *offsets,
+                              int64_t n_texts, int32_t order, const double *logs, double *out);
+int ccg_sct_score_ngram_batch(ccg_ctx *ctx, const uint8_t *ciphers, const int64_t *offsets,
+                              int64_t n_ciphers, const int32_t *cipher_of, const uint8_t *keys,
+                              int32_t key_length, int64_t n_keys, int32_t order, const double *logs,
+                              double *out);
 
 int ccg_sct_climb(ccg_ctx *ctx, const ccg_sct_climb_args *args);
 int ccg_sct_climb_dev(ccg_ctx *ctx, const ccg_sct_climb_args *args);

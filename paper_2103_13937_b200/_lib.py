@@ -47,7 +47,7 @@ class SctClimbArgs(C.Structure):
         ("p1", _i32), ("p2", _i32), ("op1_hop", _i32), ("op2_hop", _i32), ("logs", _P),
         ("scores", _P), ("keys_out", _P), ("draws_used", _P), ("last_accept", _P),
         ("tries_done", _P), ("group_size", _i32), ("group_best", _P), ("text_len", _i64),
-        ("flags", _u32),
+        ("flags", _u32), ("order", _i32),
     ]
 
 
@@ -103,6 +103,8 @@ EXPORTS = {
     "ccg_mas_det_solve": (C.c_int, [_P, C.POINTER(MasDetArgs)]),
     "ccg_mas_det_solve_dev": (C.c_int, [_P, C.POINTER(MasDetArgs)]),
     "ccg_sct_score_batch": (C.c_int, [_P, _P, _P, _i64, _P, _P, _i32, _i64, _P, _P]),
+    "ccg_ngram_log_score_batch": (C.c_int, [_P, _P, _P, _i64, _i32, _P, _P]),
+    "ccg_sct_score_ngram_batch": (C.c_int, [_P, _P, _P, _i64, _P, _P, _i32, _i64, _i32, _P, _P]),
     "ccg_sct_climb": (C.c_int, [_P, C.POINTER(SctClimbArgs)]),
     "ccg_sct_climb_dev": (C.c_int, [_P, C.POINTER(SctClimbArgs)]),
     "ccg_bench_smem_bandwidth": (C.c_int, [_P, _P]),

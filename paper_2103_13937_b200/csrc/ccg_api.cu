@@ -333,7 +333,8 @@ int ccg_score_text_batch(ccg_ctx* ctx, const uint8_t* texts, const int64_t* offs
 // identity transposition, i.e. plain log_score_text).
 static int sct_score_grouped(ccg_ctx* ctx, const uint8_t* texts, const int64_t* offsets,
                              int64_t n_texts, const int32_t* cipher_of, const uint8_t* keys,
-                             int32_t k, int64_t n_keys, const double* logs, double* out) {
+                             int32_t k, int64_t n_keys, int order, const double* logs,
+                             double* out) {
   std::map<int64_t, std::vector<int64_t>> by_len;
   std::vector<int64_t> long_idx;
   for (int64_t i = 0; i < n_keys; ++i) {
@@ -341,8 +342,8 @@ static int sct_score_grouped(ccg_ctx* ctx, const uint8_t* texts, const int64_t* 
     if (c < 0 || c >= n_texts) return fail(CCG_ERR_INVALID, "cipher_of[%lld] out of range", (long long)i);
     const int64_t L = offsets[c + 1] - offsets[c];
     if (L < k) return fail(CCG_ERR_INVALID, "ciphertext shorter than the key");
-    if (L < 2) {
-      out[i] = 0.0;  // ngrams.py:169-170: fewer than two letters score 0.0
+    if (L < order) {
+      out[i] = 0.0;  // ngrams.py:169-170: fewer than two letters (one window) score 0.0
       continue;
     }
     if (L > kSctMaxLen) {
@@ -356,7 +357,9 @@ static int sct_score_grouped(ccg_ctx* ctx, const uint8_t* texts, const int64_t* 
   void *dt, *doffv, *dlogs;
   if ((rc = upload(ctx, 0, texts, (size_t)offsets[n_texts], &dt))) return rc;
   if ((rc = upload(ctx, 1, offsets, (size_t)(n_texts + 1) * 8, &doffv))) return rc;
-  if ((rc = upload(ctx, 2, logs, kAlpha * kAlpha * 8, &dlogs))) return rc;
+  int64_t T = 1;
+  for (int q = 0; q < order; ++q) T *= kAlpha;
+  if ((rc = upload(ctx, 2, logs, (size_t)T * 8, &dlogs))) return rc;
   const int64_t* doff = (const int64_t*)doffv;
   std::vector<int32_t> cof;
   std::vector<uint8_t> kbuf;
@@ -378,16 +381,17 @@ static int sct_score_grouped(ccg_ctx* ctx, const uint8_t* texts, const int64_t* 
     cudaError_t e;
     SumPlan plan;
     if (!long_path) {
-      build_sum_plan(L - 1, &plan);
+      build_sum_plan(L - order + 1, &plan);
       if (plan.n_leaves > kSctMaxLeaves) long_path = true;
     }
     ctx->launches++;
     if (long_path)
       e = launch_sct_score_long(ctx->stream, (const uint8_t*)dt, doff, (const int32_t*)dcof,
-                                (const uint8_t*)dkeys, k, m, (const double*)dlogs, (double*)dout);
+                                (const uint8_t*)dkeys, k, m, order, (const double*)dlogs,
+                                (double*)dout);
     else
       e = launch_sct_score(ctx->stream, (const uint8_t*)dt, doff, (const int32_t*)dcof,
-                           (const uint8_t*)dkeys, k, m, (const double*)dlogs, nullptr,
+                           (const uint8_t*)dkeys, k, m, order, (const double*)dlogs,
                            (double*)dout, (int32_t)L, plan);
     if (e != cudaSuccess) return cuda_fail(e, "sct_score kernel");
     res.resize(m);
@@ -402,10 +406,12 @@ static int sct_score_grouped(ccg_ctx* ctx, const uint8_t* texts, const int64_t* 
   return CCG_OK;
 }
 
-int ccg_log_score_text_batch(ccg_ctx* ctx, const uint8_t* texts, const int64_t* offsets,
-                             int64_t n_texts, const double* logs, double* out) {
+static int log_score_common(ccg_ctx* ctx, const uint8_t* texts, const int64_t* offsets,
+                            int64_t n_texts, int order, const double* logs, double* out) {
   int rc = enter(ctx);
   if (rc) return rc;
+  if (order < 2 || order > 4)
+    return fail(CCG_ERR_UNSUPPORTED, "n-gram order %d: the engine supports 2..4", order);
   if ((rc = check_ragged(texts, offsets, n_texts, "log_score_text", nullptr))) return rc;
   if ((rc = check_logs(logs))) return rc;
   if (n_texts == 0) return CCG_OK;
@@ -418,10 +424,20 @@ int ccg_log_score_text_batch(ccg_ctx* ctx, const uint8_t* texts, const int64_t* 
     if (offsets[i + 1] - offsets[i] >= 1) idx.push_back((int32_t)i);
   std::vector<double> res(idx.size());
   rc = sct_score_grouped(ctx, texts, offsets, n_texts, idx.data(), nullptr, 1,
-                         (int64_t)idx.size(), logs, res.data());
+                         (int64_t)idx.size(), order, logs, res.data());
   if (rc) return rc;
   for (size_t j = 0; j < idx.size(); ++j) out[idx[j]] = res[j];
   return CCG_OK;
+}
+
+int ccg_log_score_text_batch(ccg_ctx* ctx, const uint8_t* texts, const int64_t* offsets,
+                             int64_t n_texts, const double* logs, double* out) {
+  return log_score_common(ctx, texts, offsets, n_texts, 2, logs, out);
+}
+
+int ccg_ngram_log_score_batch(ccg_ctx* ctx, const uint8_t* texts, const int64_t* offsets,
+                              int64_t n_texts, int32_t order, const double* logs, double* out) {
+  return log_score_common(ctx, texts, offsets, n_texts, order, logs, out);
 }
 
 int ccg_mas_delta_batch(ccg_ctx* ctx, const uint8_t* texts, const int64_t* offsets,
@@ -894,11 +910,14 @@ int ccg_mas_det_solve(ccg_ctx* ctx, const ccg_mas_det_args* a) {
 }
 
 // ------------------------------------------------------------------ SCT
-int ccg_sct_score_batch(ccg_ctx* ctx, const uint8_t* ciphers, const int64_t* offsets,
-                        int64_t n_ciphers, const int32_t* cipher_of, const uint8_t* keys,
-                        int32_t key_length, int64_t n_keys, const double* logs, double* out) {
+static int sct_score_common(ccg_ctx* ctx, const uint8_t* ciphers, const int64_t* offsets,
+                            int64_t n_ciphers, const int32_t* cipher_of, const uint8_t* keys,
+                            int32_t key_length, int64_t n_keys, int order, const double* logs,
+                            double* out) {
   int rc = enter(ctx);
   if (rc) return rc;
+  if (order < 2 || order > 4)
+    return fail(CCG_ERR_UNSUPPORTED, "n-gram order %d: the engine supports 2..4", order);
   if ((rc = check_ragged(ciphers, offsets, n_ciphers, "sct_score", nullptr))) return rc;
   if ((rc = check_logs(logs))) return rc;
   if (key_length < 1) return fail(CCG_ERR_INVALID, "key_length must be at least 1");
@@ -916,7 +935,22 @@ int ccg_sct_score_batch(ccg_ctx* ctx, const uint8_t* ciphers, const int64_t* off
     }
   }
   return sct_score_grouped(ctx, ciphers, offsets, n_ciphers, cipher_of, keys, key_length, n_keys,
-                           logs, out);
+                           order, logs, out);
+}
+
+int ccg_sct_score_batch(ccg_ctx* ctx, const uint8_t* ciphers, const int64_t* offsets,
+                        int64_t n_ciphers, const int32_t* cipher_of, const uint8_t* keys,
+                        int32_t key_length, int64_t n_keys, const double* logs, double* out) {
+  return sct_score_common(ctx, ciphers, offsets, n_ciphers, cipher_of, keys, key_length, n_keys, 2,
+                          logs, out);
+}
+
+int ccg_sct_score_ngram_batch(ccg_ctx* ctx, const uint8_t* ciphers, const int64_t* offsets,
+                              int64_t n_ciphers, const int32_t* cipher_of, const uint8_t* keys,
+                              int32_t key_length, int64_t n_keys, int32_t order, const double* logs,
+                              double* out) {
+  return sct_score_common(ctx, ciphers, offsets, n_ciphers, cipher_of, keys, key_length, n_keys,
+                          order, logs, out);
 }
 
 static int sct_check(const ccg_sct_climb_args* a) {
@@ -931,6 +965,8 @@ static int sct_check(const ccg_sct_climb_args* a) {
     return fail(CCG_ERR_INVALID, "thresholds must satisfy 0 <= p1 <= p2 <= 100");
   if (a->op1_hop < 1 || a->op2_hop < 1) return fail(CCG_ERR_INVALID, "op hops must be at least 1");
   if (a->n_workers > 0 && !a->keys_out) return fail(CCG_ERR_INVALID, "keys_out is required");
+  if (!(a->order == 0 || (a->order >= 2 && a->order <= 4)))
+    return fail(CCG_ERR_UNSUPPORTED, "n-gram order %d: the engine supports 2..4", a->order);
   return check_logs(a->logs);
 }
 
@@ -939,8 +975,9 @@ static int sct_launch(ccg_ctx* ctx, const ccg_sct_climb_args* a, int64_t n) {
   if (n > kSctMaxLen)
     return fail(CCG_ERR_UNSUPPORTED, "ciphertext of %lld letters exceeds the engine limit %lld",
                 (long long)n, (long long)kSctMaxLen);
+  const int order = a->order == 0 ? 2 : a->order;
   SumPlan plan;
-  build_sum_plan(n - 1, &plan);
+  build_sum_plan(n >= order ? n - order + 1 : 0, &plan);
   if (plan.n_leaves > kSctMaxLeaves)
     return fail(CCG_ERR_UNSUPPORTED, "text length %lld needs %d pairwise leaves (limit %d)",
                 (long long)n, plan.n_leaves, kSctMaxLeaves);
@@ -958,6 +995,7 @@ static int sct_launch(ccg_ctx* ctx, const ccg_sct_climb_args* a, int64_t n) {
   p.p2 = a->p2;
   p.op1_hop = a->op1_hop;
   p.op2_hop = a->op2_hop;
+  p.order = order;
   p.logs = a->logs;
   p.scores = a->scores;
   p.keys_out = a->keys_out;
@@ -1018,7 +1056,9 @@ int ccg_sct_climb(ccg_ctx* ctx, const ccg_sct_climb_args* a) {
     if ((rc = upload(ctx, 4, a->skips, (size_t)nw * 8, &p))) return rc;
     d.skips = (const uint64_t*)p;
   }
-  if ((rc = upload(ctx, 5, a->logs, kAlpha * kAlpha * 8, &p))) return rc;
+  int64_t T = 1;
+  for (int q = 0; q < (a->order == 0 ? 2 : a->order); ++q) T *= kAlpha;
+  if ((rc = upload(ctx, 5, a->logs, (size_t)T * 8, &p))) return rc;
   d.logs = (const double*)p;
   if ((rc = ctx->buf(6, (size_t)nw * 8, &p))) return rc;
   d.scores = (double*)p;

@@ -98,6 +98,7 @@ struct SctLaunch {
   int32_t k;
   int64_t climbings;
   int32_t p1, p2, op1_hop, op2_hop;
+  int32_t order;  // n-gram order of the log table (2 = the reference's bigrams)
   const double* logs;
   double* scores;
   uint8_t* keys_out;
@@ -140,11 +141,11 @@ cudaError_t launch_group_best_f64(cudaStream_t s, const double* scores, int64_t 
                                   int32_t group_size, int64_t* out);
 cudaError_t launch_sct_score(cudaStream_t s, const uint8_t* ciphers, const int64_t* offsets,
                              const int32_t* cipher_of, const uint8_t* keys, int32_t k,
-                             int64_t n_keys, const double* logs, int64_t* n_of, double* out,
+                             int64_t n_keys, int order, const double* logs, double* out,
                              int32_t n_common, const SumPlan& plan);
 cudaError_t launch_sct_score_long(cudaStream_t s, const uint8_t* ciphers, const int64_t* offsets,
                                   const int32_t* cipher_of, const uint8_t* keys, int32_t k,
-                                  int64_t n_keys, const double* logs, double* out);
+                                  int64_t n_keys, int order, const double* logs, double* out);
 cudaError_t launch_sct_climb(cudaStream_t s, const SctLaunch& p, const SumPlan& plan,
                              int sm_count);
 

@@ -1,6 +1,7 @@
 // ccg_sct.cu -- single-columnar-transposition (SCT) kernels for sm_100a.
 //
-// Reference path: sct.py:148-170 sct_worker.  Start from permutation(k) (rng.py:91-97),
+// Reference path: sct.py:148-170 sct_worker.  n-gram extension: ORDER-letter windows
+// (trigram/quadgram log tables, BASELINE.json config 3); ORDER 2 is the reference.  Start from permutation(k) (rng.py:91-97),
 // then per try draw an operator (sct.py:69-79: element swaps, block swaps, block shift,
 // sct.py:82-135), decrypt the whole ciphertext with the candidate key
 // (ciphers.py:71-86 transposition_gather_map, irregular grid), score it as the float64
@@ -102,7 +103,7 @@ __device__ __forceinline__ void grid_pos(int t, int k, int& c, int& r) {
   c = t - r * k;
 }
 
-template <int SLOTS>
+template <int SLOTS, int ORDER>
 struct Evaluator {
   SlotPlan sp[SLOTS];
   int k, n, base, rem, q8, r8;
@@ -136,13 +137,17 @@ struct Evaluator {
     }
   }
 
+  // log-probability of the window of ORDER plaintext letters starting at grid (c, r)
   __device__ __forceinline__ double term(const uint8_t* txt, const uint16_t* colstart,
                                          const double* logs, int c, int r) const {
-    int c1 = c + 1, r1 = r;
-    if (c1 == k) { c1 = 0; ++r1; }
-    const int ch0 = txt[colstart[c] + r];
-    const int ch1 = txt[colstart[c1] + r1];
-    return logs[ch0 * kAlpha + ch1];
+    int idx = txt[colstart[c] + r];
+#pragma unroll
+    for (int j = 1; j < ORDER; ++j) {
+      if (++c == k) { c = 0; ++r; }
+      idx = idx * kAlpha + txt[colstart[c] + r];
+    }
+    if (ORDER == 2) return logs[idx];
+    return __ldg(logs + idx);  // trigram/quadgram tables are read through L1/L2
   }
 
   // Score of decrypting txt with the lane-distributed key.
@@ -218,9 +223,13 @@ __device__ __forceinline__ void stage_text(uint8_t* dst, const uint8_t* __restri
   __syncwarp();
 }
 
-__device__ __forceinline__ void stage_logs(double* logs, const double* __restrict__ g) {
+// the bigram table is staged in shared memory; higher orders stay in global memory
+template <int ORDER>
+__device__ __forceinline__ const double* stage_logs(double* logs, const double* __restrict__ g) {
+  if (ORDER != 2) return g;
   for (int i = threadIdx.x; i < kAlpha * kAlpha; i += blockDim.x) logs[i] = g[i];
   __syncthreads();
+  return logs;
 }
 
 __host__ __device__ __forceinline__ size_t text_stride(int n) { return ((size_t)n + 15) & ~(size_t)15; }
@@ -273,19 +282,18 @@ __device__ __forceinline__ void op_block_shift(Key& c, Draws& d, int k, int lane
   c = c.gather(src(lane), src(lane + 32), k > 32);
 }
 
-template <int SLOTS>
+template <int SLOTS, int ORDER>
 __global__ void __launch_bounds__(kSctWarps * 32)
     sct_climb_kernel(const SctLaunch p, const __grid_constant__ SumPlan plan) {
   extern __shared__ __align__(16) unsigned char smem[];
-  double* logs = reinterpret_cast<double*>(smem);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint16_t* colstart = reinterpret_cast<uint16_t*>(smem + kAlpha * kAlpha * sizeof(double)) +
                        warp * kSctMaxKey;
   uint8_t* txt = smem + kAlpha * kAlpha * sizeof(double) + kSctWarps * kSctMaxKey * 2 +
                  warp * text_stride(p.n);
-  stage_logs(logs, p.logs);
+  const double* logs = stage_logs<ORDER>(reinterpret_cast<double*>(smem), p.logs);
 
-  Evaluator<SLOTS> ev;
+  Evaluator<SLOTS, ORDER> ev;
   ev.init(plan, p.k, p.n, lane);
   const int k = p.k;
   const int64_t stride = (int64_t)gridDim.x * kSctWarps;
@@ -338,23 +346,22 @@ __global__ void __launch_bounds__(kSctWarps * 32)
 }
 
 // Score given (cipher, key) pairs with the same evaluator (sct.py:158-160).
-template <int SLOTS>
+template <int SLOTS, int ORDER>
 __global__ void __launch_bounds__(kSctWarps * 32)
     sct_score_kernel(const uint8_t* __restrict__ ciphers, const int64_t* __restrict__ offsets,
                      const int32_t* __restrict__ cipher_of, const uint8_t* __restrict__ keys,
                      int32_t k, int64_t n_keys, const double* __restrict__ glogs,
                      double* __restrict__ out, int32_t n, const __grid_constant__ SumPlan plan) {
   extern __shared__ __align__(16) unsigned char smem[];
-  double* logs = reinterpret_cast<double*>(smem);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint16_t* colstart = reinterpret_cast<uint16_t*>(smem + kAlpha * kAlpha * sizeof(double)) +
                        warp * kSctMaxKey;
   uint8_t* txt = smem + kAlpha * kAlpha * sizeof(double) + kSctWarps * kSctMaxKey * 2 +
                  warp * text_stride(n);
-  stage_logs(logs, glogs);
+  const double* logs = stage_logs<ORDER>(reinterpret_cast<double*>(smem), glogs);
   const int64_t w = (int64_t)blockIdx.x * kSctWarps + warp;
   if (w >= n_keys) return;
-  Evaluator<SLOTS> ev;
+  Evaluator<SLOTS, ORDER> ev;
   ev.init(plan, k, n, lane);
   stage_text(txt, ciphers + offsets[cipher_of[w]], n, lane);
   Key key;
@@ -372,12 +379,15 @@ struct LongText {
   const double* logs;
   const int32_t* colstart;
   int k;
+  int order;
   __device__ __forceinline__ int at(int64_t t) const {
     const int64_t r = t / k;
     return txt[colstart[t - r * k] + r];
   }
   __device__ __forceinline__ double term(int64_t t) const {
-    return logs[at(t) * kAlpha + at(t + 1)];
+    int64_t idx = 0;
+    for (int j = 0; j < order; ++j) idx = idx * kAlpha + at(t + j);
+    return logs[idx];
   }
 };
 
@@ -433,7 +443,8 @@ __global__ void sct_score_long_kernel(const uint8_t* __restrict__ ciphers,
                                       const int64_t* __restrict__ offsets,
                                       const int32_t* __restrict__ cipher_of,
                                       const uint8_t* __restrict__ keys, int32_t k, int64_t n_keys,
-                                      const double* __restrict__ logs, double* __restrict__ out) {
+                                      int order, const double* __restrict__ logs,
+                                      double* __restrict__ out) {
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= n_keys) return;
   const int32_t c = cipher_of[w];
@@ -446,8 +457,8 @@ __global__ void sct_score_long_kernel(const uint8_t* __restrict__ ciphers,
     colstart[col] = (int32_t)acc;
     acc += base + (col < rem ? 1 : 0);
   }
-  LongText L{ciphers + offsets[c], logs, colstart, k};
-  out[w] = n < 2 ? 0.0 : pairwise_iter(L, n - 1);
+  LongText L{ciphers + offsets[c], logs, colstart, k, order};
+  out[w] = n < order ? 0.0 : pairwise_iter(L, n - order + 1);
 }
 
 size_t sct_smem_bytes(int n) {
@@ -467,9 +478,9 @@ int slots_for(const SumPlan& plan) {
   return s <= 1 ? 1 : s <= 2 ? 2 : s <= 4 ? 4 : 8;
 }
 
-template <int SLOTS>
+template <int SLOTS, int ORDER>
 cudaError_t climb_slots(cudaStream_t s, const SctLaunch& p, const SumPlan& plan, int sm_count) {
-  auto kern = sct_climb_kernel<SLOTS>;
+  auto kern = sct_climb_kernel<SLOTS, ORDER>;
   const size_t bytes = sct_smem_bytes(p.n);
   cudaError_t e = prep_smem(kern, bytes);
   if (e != cudaSuccess) return e;
@@ -484,11 +495,11 @@ cudaError_t climb_slots(cudaStream_t s, const SctLaunch& p, const SumPlan& plan,
   return cudaGetLastError();
 }
 
-template <int SLOTS>
+template <int SLOTS, int ORDER>
 cudaError_t score_slots(cudaStream_t s, const uint8_t* ciphers, const int64_t* offsets,
                         const int32_t* cipher_of, const uint8_t* keys, int32_t k, int64_t n_keys,
                         const double* logs, double* out, int32_t n, const SumPlan& plan) {
-  auto kern = sct_score_kernel<SLOTS>;
+  auto kern = sct_score_kernel<SLOTS, ORDER>;
   const size_t bytes = sct_smem_bytes(n);
   cudaError_t e = prep_smem(kern, bytes);
   if (e != cudaSuccess) return e;
@@ -527,35 +538,59 @@ void build_sum_plan(int64_t n_terms, SumPlan* plan) {
 
 cudaError_t launch_sct_score_long(cudaStream_t s, const uint8_t* ciphers, const int64_t* offsets,
                                   const int32_t* cipher_of, const uint8_t* keys, int32_t k,
-                                  int64_t n_keys, const double* logs, double* out) {
+                                  int64_t n_keys, int order, const double* logs, double* out) {
   if (n_keys <= 0) return cudaSuccess;
   const int grid = (int)((n_keys + 127) / 128);
-  sct_score_long_kernel<<<grid, 128, 0, s>>>(ciphers, offsets, cipher_of, keys, k, n_keys, logs,
-                                              out);
+  sct_score_long_kernel<<<grid, 128, 0, s>>>(ciphers, offsets, cipher_of, keys, k, n_keys, order,
+                                              logs, out);
   return cudaGetLastError();
+}
+
+template <int ORDER>
+static cudaError_t climb_order(cudaStream_t s, const SctLaunch& p, const SumPlan& plan,
+                               int sm_count) {
+  switch (slots_for(plan)) {
+    case 1: return climb_slots<1, ORDER>(s, p, plan, sm_count);
+    case 2: return climb_slots<2, ORDER>(s, p, plan, sm_count);
+    case 4: return climb_slots<4, ORDER>(s, p, plan, sm_count);
+    default: return climb_slots<8, ORDER>(s, p, plan, sm_count);
+  }
 }
 
 cudaError_t launch_sct_climb(cudaStream_t s, const SctLaunch& p, const SumPlan& plan,
                              int sm_count) {
   if (p.n_workers <= 0) return cudaSuccess;
+  switch (p.order) {
+    case 2: return climb_order<2>(s, p, plan, sm_count);
+    case 3: return climb_order<3>(s, p, plan, sm_count);
+    case 4: return climb_order<4>(s, p, plan, sm_count);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int ORDER>
+static cudaError_t score_order(cudaStream_t s, const uint8_t* ciphers, const int64_t* offsets,
+                               const int32_t* cipher_of, const uint8_t* keys, int32_t k,
+                               int64_t n_keys, const double* logs, double* out, int32_t n_common,
+                               const SumPlan& plan) {
   switch (slots_for(plan)) {
-    case 1: return climb_slots<1>(s, p, plan, sm_count);
-    case 2: return climb_slots<2>(s, p, plan, sm_count);
-    case 4: return climb_slots<4>(s, p, plan, sm_count);
-    default: return climb_slots<8>(s, p, plan, sm_count);
+    case 1: return score_slots<1, ORDER>(s, ciphers, offsets, cipher_of, keys, k, n_keys, logs, out, n_common, plan);
+    case 2: return score_slots<2, ORDER>(s, ciphers, offsets, cipher_of, keys, k, n_keys, logs, out, n_common, plan);
+    case 4: return score_slots<4, ORDER>(s, ciphers, offsets, cipher_of, keys, k, n_keys, logs, out, n_common, plan);
+    default: return score_slots<8, ORDER>(s, ciphers, offsets, cipher_of, keys, k, n_keys, logs, out, n_common, plan);
   }
 }
 
 cudaError_t launch_sct_score(cudaStream_t s, const uint8_t* ciphers, const int64_t* offsets,
                              const int32_t* cipher_of, const uint8_t* keys, int32_t k,
-                             int64_t n_keys, const double* logs, int64_t* /*n_of*/, double* out,
+                             int64_t n_keys, int order, const double* logs, double* out,
                              int32_t n_common, const SumPlan& plan) {
   if (n_keys <= 0) return cudaSuccess;
-  switch (slots_for(plan)) {
-    case 1: return score_slots<1>(s, ciphers, offsets, cipher_of, keys, k, n_keys, logs, out, n_common, plan);
-    case 2: return score_slots<2>(s, ciphers, offsets, cipher_of, keys, k, n_keys, logs, out, n_common, plan);
-    case 4: return score_slots<4>(s, ciphers, offsets, cipher_of, keys, k, n_keys, logs, out, n_common, plan);
-    default: return score_slots<8>(s, ciphers, offsets, cipher_of, keys, k, n_keys, logs, out, n_common, plan);
+  switch (order) {
+    case 2: return score_order<2>(s, ciphers, offsets, cipher_of, keys, k, n_keys, logs, out, n_common, plan);
+    case 3: return score_order<3>(s, ciphers, offsets, cipher_of, keys, k, n_keys, logs, out, n_common, plan);
+    case 4: return score_order<4>(s, ciphers, offsets, cipher_of, keys, k, n_keys, logs, out, n_common, plan);
+    default: return cudaErrorInvalidValue;
   }
 }
 

@@ -162,13 +162,16 @@ def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, 
 
 def sct_climb(ciphers, cipher_of, keys, logs, key_length, climbings, *, p1=33, p2=66, op1_hop=3,
               op2_hop=3, skips=None, group_size=0, draws_used=False, last_accept=False,
-              tries_done=False, devices_=None) -> ClimbResult:
+              tries_done=False, order=2, devices_=None) -> ClimbResult:
     """Run sct_worker (sct.py:148-170) for every worker on the GPU(s).  All ciphertexts
-    referenced by one call must share a length (the numpy pairwise-sum plan is per length)."""
+    referenced by one call must share a length (the numpy pairwise-sum plan is per length).
+    logs: float64[26**order] (order 2 = the reference's bigram table)."""
     flat, off = _lib.ragged(ciphers)
     cof = np.ascontiguousarray(cipher_of, dtype=np.int32).reshape(-1)
     keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, 2)
-    lg = np.ascontiguousarray(logs, dtype=np.float64)
+    lg = np.ascontiguousarray(logs, dtype=np.float64).reshape(-1)
+    if lg.size != 26**int(order):
+        raise ValueError(f"expected {26**int(order)} log-table entries for order {order}")
     n = cof.size
     k = int(key_length)
     if keys.shape[0] != n:
@@ -201,6 +204,7 @@ def sct_climb(ciphers, cipher_of, keys, logs, key_length, climbings, *, p1=33, p
         a.draws_used, a.last_accept = _lib.ptr(out.draws_used), _lib.ptr(out.last_accept)
         a.tries_done = _lib.ptr(out.tries_done)
         a.group_size, a.group_best = int(group_size), _lib.ptr(out.group_best)
+        a.order = int(order)
         ctx = _lib.context(dev)
         with ctx.lock:
             before = ctx.launches()
@@ -245,21 +249,39 @@ def mas_delta_counts_batch(counts, pairs, score_matrix) -> np.ndarray:
     return out
 
 
-def sct_score_batch(ciphers, cipher_of, keys, logs) -> np.ndarray:
+def sct_score_batch(ciphers, cipher_of, keys, logs, order=2) -> np.ndarray:
     """candidate_score (sct.py:158-160) for many (ciphertext, key) pairs on the GPU."""
     flat, off = _lib.ragged(ciphers)
     cof = np.ascontiguousarray(cipher_of, dtype=np.int32).reshape(-1)
     kk = np.ascontiguousarray(keys, dtype=np.uint8)
     if kk.ndim != 2 or kk.shape[0] != cof.size:
         raise ValueError("keys must be [n_keys, key_length]")
-    lg = np.ascontiguousarray(logs, dtype=np.float64)
+    lg = np.ascontiguousarray(logs, dtype=np.float64).reshape(-1)
+    if lg.size != 26**int(order):
+        raise ValueError(f"expected {26**int(order)} log-table entries for order {order}")
     out = np.empty(cof.size, dtype=np.float64)
     ctx = _lib.context(default_device())
     with ctx.lock:
-        _lib.check(_lib.load().ccg_sct_score_batch(ctx.handle, _lib.ptr(flat), _lib.ptr(off),
-                                                   off.size - 1, _lib.ptr(cof), _lib.ptr(kk),
-                                                   kk.shape[1], cof.size, _lib.ptr(lg),
-                                                   _lib.ptr(out)), "sct_score")
+        _lib.check(_lib.load().ccg_sct_score_ngram_batch(ctx.handle, _lib.ptr(flat), _lib.ptr(off),
+                                                         off.size - 1, _lib.ptr(cof), _lib.ptr(kk),
+                                                         kk.shape[1], cof.size, int(order),
+                                                         _lib.ptr(lg), _lib.ptr(out)), "sct_score")
+    return out
+
+
+def ngram_log_score_batch(texts, order, logs) -> np.ndarray:
+    """log_score_text (ngrams.py:166-172) generalised to order-n windows, bit-exact numpy
+    pairwise order, on the GPU."""
+    flat, off = _lib.ragged(texts)
+    lg = np.ascontiguousarray(logs, dtype=np.float64).reshape(-1)
+    if lg.size != 26**int(order):
+        raise ValueError(f"expected {26**int(order)} log-table entries for order {order}")
+    out = np.empty(off.size - 1, dtype=np.float64)
+    ctx = _lib.context(default_device())
+    with ctx.lock:
+        _lib.check(_lib.load().ccg_ngram_log_score_batch(ctx.handle, _lib.ptr(flat), _lib.ptr(off),
+                                                         off.size - 1, int(order), _lib.ptr(lg),
+                                                         _lib.ptr(out)), "ngram_log_score")
     return out
 
 

@@ -312,3 +312,16 @@ def ngram_score_text_batch(texts, table) -> np.ndarray:
 def ngram_score_text(text: MappedText, table) -> int:
     """Sum of table entries over the text's windows (score_text generalised), on the GPU."""
     return int(ngram_score_text_batch([text], table)[0])
+
+
+def ngram_log_score_text_batch(texts, table) -> np.ndarray:
+    """Log-probability fitness of many texts (log_score_text generalised), bit-exact numpy
+    pairwise order, in one GPU call."""
+    t = as_log_ngram_table(table)
+    from .engine import ngram_log_score_batch
+
+    return ngram_log_score_batch(texts, t.order, t.logs)
+
+
+def ngram_log_score_text(text: MappedText, table) -> float:
+    return float(ngram_log_score_text_batch([text], table)[0])

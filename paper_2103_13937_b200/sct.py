@@ -4,6 +4,10 @@ sct_worker / solve_sct run on the GPU: one warp per worker, candidate keys mutat
 registers, decryption by index arithmetic, float64 scoring in numpy's pairwise order
 (csrc/ccg_sct.cu).  The operator functions below are the reference's host-side helpers,
 drawing from a (GPU-generated) WorkerRng stream; the climb itself never calls them.
+
+n-gram extension: sct_worker / solve_sct also accept an ngrams.LogNgramTable of order 3 or
+4 (BASELINE.json config 3: trigram scoring); the candidate score is then the pairwise sum of
+the window log-probabilities of that order.
 """
 from __future__ import annotations
 
@@ -15,7 +19,7 @@ import numpy as np
 from . import engine
 from .ciphers import sct_decrypt
 from .codec import MappedText
-from .ngrams import LogBigramTable
+from .ngrams import LogBigramTable, as_log_ngram_table
 from .rng import WorkerRng, philox_keys, worker_stream_index
 from .search import RestartSummary, SolveResult
 from .mas import _batched_restarts
@@ -110,9 +114,10 @@ def sct_worker(cipher: MappedText, logs: LogBigramTable, cfg: SctSolverConfig,
     text = np.asarray(cipher, dtype=np.int64)
     if text.size < cfg.key_length:
         raise ValueError("ciphertext shorter than the key")
-    res = engine.sct_climb([text], [0], [state.key], logs.logs, cfg.key_length, cfg.climbings,
+    lt = as_log_ngram_table(logs)
+    res = engine.sct_climb([text], [0], [state.key], lt.logs, cfg.key_length, cfg.climbings,
                            p1=cfg.p1, p2=cfg.p2, op1_hop=cfg.op1_hop, op2_hop=cfg.op2_hop,
-                           skips=[state.position], draws_used=True)
+                           skips=[state.position], draws_used=True, order=lt.order)
     state.advance(int(res.draws_used[0]))
     return res.keys[0].astype(np.int64), float(res.scores[0])
 
@@ -121,9 +126,10 @@ def _restart_batch(text, logs, cfg, restarts):
     W = cfg.workers
     streams = [worker_stream_index(r, w) for r in restarts for w in range(W)]
     keys = philox_keys([cfg.global_seed], streams)
-    res = engine.sct_climb([text], np.zeros(len(streams), np.int32), keys, logs.logs,
+    lt = as_log_ngram_table(logs)
+    res = engine.sct_climb([text], np.zeros(len(streams), np.int32), keys, lt.logs,
                            cfg.key_length, cfg.climbings, p1=cfg.p1, p2=cfg.p2,
-                           op1_hop=cfg.op1_hop, op2_hop=cfg.op2_hop, group_size=W)
+                           op1_hop=cfg.op1_hop, op2_hop=cfg.op2_hop, group_size=W, order=lt.order)
     out = []
     for i, _ in enumerate(restarts):
         sc = res.scores[i * W:(i + 1) * W]

@@ -532,3 +532,58 @@ def test_solve_stochastic_with_trigram_table():
                                   [(r << 32) | w for w in range(16)], 3, table.scores, 3000)
         assert summ[r].score == int(want.max())
     assert best.best_score == cc.ngram_score_text(best.best_text, table)
+
+
+@pytest.mark.parametrize("order", [2, 3, 4])
+def test_ngram_log_score_bit_exact_vs_oracle(order):
+    rng = np.random.default_rng(20 + order)
+    logs = -rng.random(26**order) * 20 - 1
+    lengths = [0, 1, order - 1, order, order + 1, 7, 8, 9, 127, 128, 129, 130, 400, 1000, 4096,
+               4100, 9000]
+    texts = [rng.integers(0, 26, L) for L in lengths]
+    got = cc.ngram_log_score_text_batch(texts, cc.LogNgramTable(order, logs, -21.0))
+    assert got.tolist() == [O.ngram_log_score_text(t, order, logs) for t in texts]
+
+
+@pytest.mark.parametrize("order", [3, 4])
+def test_sct_score_ngram_vs_oracle(order):
+    rng = np.random.default_rng(30 + order)
+    logs = -rng.random(26**order) * 20 - 1
+    ciphers, keys, cof = [], [], []
+    for i, (k, n) in enumerate([(5, 400), (10, 400), (20, 400), (7, 129), (40, 4096), (9, 5000)]):
+        ciphers.append(rng.integers(0, 26, n))
+        keys.append(rng.permutation(k))
+    for i, (c, kk) in enumerate(zip(ciphers, keys)):
+        got = engine.sct_score_batch([c], [0], kk[None, :].astype(np.uint8), logs, order=order)
+        assert float(got[0]) == O.sct_score(c, logs, kk, order=order)
+
+
+@pytest.mark.parametrize("order", [3, 4])
+def test_sct_climb_ngram_vs_oracle(order):
+    rng = np.random.default_rng(40 + order)
+    corpus = rng.integers(0, 26, 5000)
+    for k, n in [(5, 400), (10, 400), (20, 400), (15, 596), (33, 200), (6, order + 5)]:
+        logs = -rng.random(26**order) * 20 - 1
+        cipher = rng.integers(0, 26, n)
+        seeds, streams = [int(rng.integers(0, 2**63))] * 6, list(range(6))
+        keys = philox_keys(seeds[:1], streams)
+        res = engine.sct_climb([cipher], np.zeros(6, np.int32), keys, logs, k, 1200, order=order,
+                               group_size=6)
+        want_s, want_k = O.sct_workers([cipher], np.zeros(6, np.int32), seeds, streams, logs, k,
+                                       1200, order=order)
+        assert res.scores.tolist() == want_s.tolist(), (k, n)
+        assert np.array_equal(res.keys.astype(np.int64), want_k)
+
+
+def test_solve_sct_trigram_recovers_key(golden):
+    corpus = "".join(chr(97 + int(x)) for x in golden.corpus())
+    l3 = cc.build_log_ngram_table(cc.build_ngram_table_from_corpus(corpus, 3))
+    plain = golden.plain_sct(400)
+    key = cc.WorkerRng(1234, cc.KEYGEN_STREAM).permutation(8)
+    cipher = cc.sct_encrypt(plain, key)
+    cfg = cc.SctSolverConfig(key_length=8, workers=64, climbings=4000, global_seed=5)
+    best, _ = cc.solve_sct(cipher, l3, cfg)
+    assert np.array_equal(best.best_text, plain)
+    want_s, _ = O.sct_workers([cipher], np.zeros(64, np.int32), [5] * 64, list(range(64)), l3.logs,
+                              8, 4000, order=3)
+    assert best.per_worker_scores == want_s.tolist()
