@@ -35,20 +35,49 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kSctWarps = 8;
 
+// The worker's draw window: 128 consecutive raw draws of its stream in shared memory
+// (one Philox4x64-10 block per lane per refill, rng.py:68-75), so a scalar draw is one
+// broadcast 64-bit shared load.  Every SCT bound is < 2^11 (100, hops, k <= 64, ...), so
+// int(u*bound) uses the single-product exact conversion (ccg_rng.cuh int_below_small).
 struct Draws {
-  DrawWindow win;
-  uint64_t pos;
-  __device__ __forceinline__ uint64_t raw(int lane) {
-    if (pos >= win.base + 128) win.refill(pos, lane);
-    const uint32_t o = (uint32_t)(pos - win.base);
-    const uint32_t r = o >> 5;
-    const uint64_t w = r == 0 ? win.w[0] : r == 1 ? win.w[1] : r == 2 ? win.w[2] : win.w[3];
-    ++pos;
-    return shfl64(w, (int)(o & 31));
+  const uint64_t* key;  // &keys[2*w] (global; re-read at refill)
+  uint32_t win;         // shared address of the 128-slot window; slot j holds draw base+j >> 11
+  uint64_t base;        // stream index of window slot 0 (multiple of 4)
+  uint32_t o;           // window slot of the next draw
+
+  __device__ __forceinline__ void refill(int lane) {
+    base += o & ~3u;
+    o &= 3u;
+    uint64_t v0, v1, v2, v3;
+    philox4x64_10(__ldg(key), __ldg(key + 1), (base >> 2) + 1 + (uint64_t)lane, v0, v1, v2, v3);
+    __syncwarp();
+    const uint32_t a = win + 32u * (uint32_t)lane;
+    asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(a), "l"(v0 >> 11), "l"(v1 >> 11)
+                 : "memory");
+    asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(a + 16u), "l"(v2 >> 11), "l"(v3 >> 11)
+                 : "memory");
+    __syncwarp();
   }
-  // rng.py:77-79
+  __device__ __forceinline__ void start(uint64_t pos, int lane) {
+    base = pos & ~3ULL;
+    o = 0;
+    refill(lane);
+    o = (uint32_t)(pos & 3);
+  }
+  __device__ __forceinline__ uint64_t position() const { return base + o; }
+  // rng.py:77-79: int(u * bound) for the next draw, 1 <= bound < 2^11.  With m = x >> 11 and
+  // P = m * bound (< 2^64, exact), the double product rounds P * 2^-53 to 53 bits; truncation
+  // can differ from P >> 53 only when the fraction P mod 2^53 lies within 2^10 of 2^53 (the
+  // rounding step is at most 2^(bitlen(P) - 54) <= 2^10), so the exact test of
+  // int_below_small runs only then.
   __device__ __forceinline__ int below(uint32_t bound, int lane) {
-    return (int)int_below(raw(lane), bound);
+    if (o > 127u) refill(lane);
+    uint64_t m;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(m) : "r"(win + 8u * o));
+    ++o;
+    const uint64_t P = m * (uint64_t)bound;
+    if (((P >> 10) & ((1ULL << 43) - 1)) != ((1ULL << 43) - 1)) return (int)(P >> 53);
+    return (int)int_below_small(m << 11, bound);
   }
   // rng.py:81-89
   __device__ __forceinline__ void pair(uint32_t bound, int lane, int& a, int& b) {
@@ -94,19 +123,15 @@ struct SlotPlan {
   int leaf;       // leaf id handled by this lane's 8-lane group in this slot (-1: none)
   int count;      // strided terms per accumulator (len/8, 0 for a sequential leaf)
   int tail;       // terms added in order after the tree
-  int c0, r0;     // grid position of this lane's first strided term
-  int ct, rt;     // grid position of the first tail term
+  int p0;         // plaintext position of this lane's first strided term
+  int pt;         // position of the first tail term
 };
-
-__device__ __forceinline__ void grid_pos(int t, int k, int& c, int& r) {
-  r = t / k;
-  c = t - r * k;
-}
 
 template <int SLOTS, int ORDER>
 struct Evaluator {
   SlotPlan sp[SLOTS];
-  int k, n, base, rem, q8, r8;
+  int k, n, base, rem;
+  int c0, r0, q32, r32;  // grid position of plaintext position `lane`; 32 = q32*k + r32
   const SumPlan* plan;
 
   __device__ void init(const SumPlan& P, int k_, int n_, int lane) {
@@ -115,8 +140,10 @@ struct Evaluator {
     n = n_;
     base = n / k;
     rem = n - base * k;
-    q8 = 8 / k;
-    r8 = 8 - q8 * k;
+    q32 = 32 / k;
+    r32 = 32 - q32 * k;
+    r0 = lane / k;
+    c0 = lane - r0 * k;
 #pragma unroll
     for (int s = 0; s < SLOTS; ++s) {
       const int leaf = 4 * s + (lane >> 3);
@@ -126,33 +153,29 @@ struct Evaluator {
         q.leaf = leaf;
         q.count = len >= 8 ? len / 8 : 0;
         q.tail = len >= 8 ? len % 8 : len;
-        grid_pos(start + (lane & 7), k, q.c0, q.r0);
-        grid_pos(start + 8 * q.count, k, q.ct, q.rt);
+        q.p0 = start + (lane & 7);
+        q.pt = start + 8 * q.count;
       } else {
         q.leaf = -1;
         q.count = 0;
         q.tail = 0;
-        q.c0 = q.r0 = q.ct = q.rt = 0;
+        q.p0 = q.pt = 0;
       }
     }
   }
 
-  // log-probability of the window of ORDER plaintext letters starting at grid (c, r)
-  __device__ __forceinline__ double term(const uint8_t* txt, const uint16_t* colstart,
-                                         const double* logs, int c, int r) const {
-    int idx = txt[colstart[c] + r];
+  // log-probability of the window of ORDER plaintext letters starting at position t
+  __device__ __forceinline__ double term(const uint8_t* plain, const double* logs, int t) const {
+    int idx = plain[t];
 #pragma unroll
-    for (int j = 1; j < ORDER; ++j) {
-      if (++c == k) { c = 0; ++r; }
-      idx = idx * kAlpha + txt[colstart[c] + r];
-    }
+    for (int j = 1; j < ORDER; ++j) idx = idx * kAlpha + plain[t + j];
     if (ORDER == 2) return logs[idx];
     return __ldg(logs + idx);  // trigram/quadgram tables are read through L1/L2
   }
 
   // Score of decrypting txt with the lane-distributed key.
   __device__ double score(const Key& key, const uint8_t* txt, uint16_t* colstart,
-                          const double* logs, int lane) const {
+                          uint8_t* plain, const double* logs, int lane) const {
     // colstart[key[j]] = sum of segment lengths of key positions < j (ciphers.py:79-86)
     const bool wide = k > 32;
     const int len0 = lane < k ? base + (key.v0 < rem ? 1 : 0) : 0;
@@ -174,30 +197,37 @@ struct Evaluator {
       if (lane + 32 < k) colstart[key.v1] = (uint16_t)(tot0 + inc1 - len1);
     }
     __syncwarp();
+    // decrypt (ciphers.py:107-113): plain[t] = cipher[colstart[t % k] + t / k]
+    {
+      int c = c0, r = r0;
+      for (int t = lane; t < n; t += 32) {
+        plain[t] = txt[colstart[c] + r];
+        c += r32;
+        r += q32;
+        if (c >= k) {
+          c -= k;
+          ++r;
+        }
+      }
+    }
+    __syncwarp();
 
     double res[SLOTS];
 #pragma unroll
     for (int s = 0; s < SLOTS; ++s) {
       const SlotPlan& q = sp[s];
       double acc = 0.0;
-      int c = q.c0, r = q.r0;
-      for (int i = 0; i < q.count; ++i) {
-        const double v = term(txt, colstart, logs, c, r);
+      int t = q.p0;
+      for (int i = 0; i < q.count; ++i, t += 8) {
+        const double v = term(plain, logs, t);
         acc = i == 0 ? v : acc + v;
-        c += r8;
-        r += q8;
-        if (c >= k) { c -= k; ++r; }
       }
       // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) as an xor butterfly over the 8-lane group
       acc += __shfl_xor_sync(kFull, acc, 1);
       acc += __shfl_xor_sync(kFull, acc, 2);
       acc += __shfl_xor_sync(kFull, acc, 4);
-      c = q.ct;
-      r = q.rt;
-      for (int u = 0; u < q.tail; ++u) {
-        acc += term(txt, colstart, logs, c, r);
-        if (++c == k) { c = 0; ++r; }
-      }
+      t = q.pt;
+      for (int u = 0; u < q.tail; ++u, ++t) acc += term(plain, logs, t);
       res[s] = acc;
     }
     // replay the recursion's merges (post-order): leaf[dst] = leaf[dst] + leaf[src]
@@ -213,7 +243,9 @@ struct Evaluator {
       for (int s = 0; s < SLOTS; ++s)
         if (s == (d >> 2) && (lane >> 3) == (d & 3)) res[s] = res[s] + sv;
     }
-    return __shfl_sync(kFull, res[0], 0);
+    const double out = __shfl_sync(kFull, res[0], 0);
+    __syncwarp();  // plain / colstart are rewritten by the next candidate
+    return out;
   }
 };
 
@@ -233,6 +265,27 @@ __device__ __forceinline__ const double* stage_logs(double* logs, const double* 
 }
 
 __host__ __device__ __forceinline__ size_t text_stride(int n) { return ((size_t)n + 15) & ~(size_t)15; }
+
+// Shared layout: [bigram log table 676 x f64] then per warp
+// [draw window 128 x u64][colstart 64 x u16][ciphertext][decrypted candidate].
+constexpr size_t kLogsBytes = kAlpha * kAlpha * sizeof(double);
+constexpr size_t kWinBytes = 128 * sizeof(uint64_t);
+__host__ __device__ __forceinline__ size_t sct_warp_bytes(int n) {
+  return kWinBytes + kSctMaxKey * 2 + 2 * text_stride(n);
+}
+struct WarpSmem {
+  uint32_t win;
+  uint16_t* colstart;
+  uint8_t* txt;
+  uint8_t* plain;
+  __device__ WarpSmem(unsigned char* smem, int warp, int n) {
+    unsigned char* b = smem + kLogsBytes + (size_t)warp * sct_warp_bytes(n);
+    win = (uint32_t)__cvta_generic_to_shared(b);
+    colstart = reinterpret_cast<uint16_t*>(b + kWinBytes);
+    txt = b + kWinBytes + kSctMaxKey * 2;
+    plain = txt + text_stride(n);
+  }
+};
 
 // sct.py:82-89 apply_element_swaps
 __device__ __forceinline__ void op_element_swaps(Key& c, Draws& d, int k, int max_hops, int lane) {
@@ -283,14 +336,11 @@ __device__ __forceinline__ void op_block_shift(Key& c, Draws& d, int k, int lane
 }
 
 template <int SLOTS, int ORDER>
-__global__ void __launch_bounds__(kSctWarps * 32)
+__global__ void __launch_bounds__(kSctWarps * 32, 4)
     sct_climb_kernel(const SctLaunch p, const __grid_constant__ SumPlan plan) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint16_t* colstart = reinterpret_cast<uint16_t*>(smem + kAlpha * kAlpha * sizeof(double)) +
-                       warp * kSctMaxKey;
-  uint8_t* txt = smem + kAlpha * kAlpha * sizeof(double) + kSctWarps * kSctMaxKey * 2 +
-                 warp * text_stride(p.n);
+  const WarpSmem ws(smem, warp, p.n);
   const double* logs = stage_logs<ORDER>(reinterpret_cast<double*>(smem), p.logs);
 
   Evaluator<SLOTS, ORDER> ev;
@@ -300,12 +350,11 @@ __global__ void __launch_bounds__(kSctWarps * 32)
 
   for (int64_t w = (int64_t)blockIdx.x * kSctWarps + warp; w < p.n_workers; w += stride) {
     const int32_t cid = p.cipher_of[w];
-    stage_text(txt, p.ciphers + p.offsets[cid], p.n, lane);
+    stage_text(ws.txt, p.ciphers + p.offsets[cid], p.n, lane);
     Draws d;
-    d.win.k0 = p.keys[2 * w];
-    d.win.k1 = p.keys[2 * w + 1];
-    d.pos = p.skips ? p.skips[w] : 0;
-    d.win.refill(d.pos, lane);
+    d.key = p.keys + 2 * w;
+    d.win = ws.win;
+    d.start(p.skips ? p.skips[w] : 0, lane);
 
     // rng.py:91-97 permutation(k): Fisher-Yates from the top
     Key key;
@@ -315,7 +364,7 @@ __global__ void __launch_bounds__(kSctWarps * 32)
       const int j = d.below((uint32_t)(i + 1), lane);
       key.swap_pos(i, j, lane);
     }
-    double score = ev.score(key, txt, colstart, logs, lane);
+    double score = ev.score(key, ws.txt, ws.colstart, ws.plain, logs, lane);
     int64_t last = -1, t = 0;
     for (; t < p.climbings; ++t) {
       const int u = d.below(100u, lane);
@@ -326,7 +375,7 @@ __global__ void __launch_bounds__(kSctWarps * 32)
         op_block_swaps(cand, d, k, p.op2_hop, lane);
       else
         op_block_shift(cand, d, k, lane);
-      const double cs = ev.score(cand, txt, colstart, logs, lane);
+      const double cs = ev.score(cand, ws.txt, ws.colstart, ws.plain, logs, lane);
       if (cs > score) {
         key = cand;
         score = cs;
@@ -337,7 +386,7 @@ __global__ void __launch_bounds__(kSctWarps * 32)
     if (lane + 32 < k) p.keys_out[w * k + lane + 32] = (uint8_t)key.v1;
     if (lane == 0) {
       p.scores[w] = score;
-      if (p.draws_used) p.draws_used[w] = d.pos;
+      if (p.draws_used) p.draws_used[w] = d.position();
       if (p.last_accept) p.last_accept[w] = last;
       if (p.tries_done) p.tries_done[w] = t;
     }
@@ -354,20 +403,17 @@ __global__ void __launch_bounds__(kSctWarps * 32)
                      double* __restrict__ out, int32_t n, const __grid_constant__ SumPlan plan) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint16_t* colstart = reinterpret_cast<uint16_t*>(smem + kAlpha * kAlpha * sizeof(double)) +
-                       warp * kSctMaxKey;
-  uint8_t* txt = smem + kAlpha * kAlpha * sizeof(double) + kSctWarps * kSctMaxKey * 2 +
-                 warp * text_stride(n);
+  const WarpSmem ws(smem, warp, n);
   const double* logs = stage_logs<ORDER>(reinterpret_cast<double*>(smem), glogs);
   const int64_t w = (int64_t)blockIdx.x * kSctWarps + warp;
   if (w >= n_keys) return;
   Evaluator<SLOTS, ORDER> ev;
   ev.init(plan, k, n, lane);
-  stage_text(txt, ciphers + offsets[cipher_of[w]], n, lane);
+  stage_text(ws.txt, ciphers + offsets[cipher_of[w]], n, lane);
   Key key;
   key.v0 = lane < k ? keys[w * k + lane] : lane;
   key.v1 = lane + 32 < k ? keys[w * k + lane + 32] : lane + 32;
-  const double s = ev.score(key, txt, colstart, logs, lane);
+  const double s = ev.score(key, ws.txt, ws.colstart, ws.plain, logs, lane);
   if (lane == 0) out[w] = s;
 }
 
@@ -461,10 +507,7 @@ __global__ void sct_score_long_kernel(const uint8_t* __restrict__ ciphers,
   out[w] = n < order ? 0.0 : pairwise_iter(L, n - order + 1);
 }
 
-size_t sct_smem_bytes(int n) {
-  return kAlpha * kAlpha * sizeof(double) + kSctWarps * kSctMaxKey * 2 +
-         kSctWarps * text_stride(n);
-}
+size_t sct_smem_bytes(int n) { return kLogsBytes + kSctWarps * sct_warp_bytes(n); }
 
 template <typename K>
 cudaError_t prep_smem(K kern, size_t bytes) {

@@ -138,7 +138,7 @@ def c3(args):
     l3 = cc.build_log_ngram_table(cc.build_ngram_table_from_corpus(corpus_text(), 3))
     corpus = G.corpus()
     n_c = 1000
-    W, K = (8, 1000) if args.quick else (16, 3000)
+    W, K = (8, 1000) if args.quick else (32, 1000)
     total_evals, total_s, rec = 0, 0.0, 0
     rows = []
     ks = list(range(5, 21))
