@@ -36,8 +36,12 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 KEYGEN_STREAM = 2**32 - 2
-EXEC_LDS_BYTES_PER_EVAL = 2 * 26 * 8 + 4  # executed: two LDS.64 rows per active lane + K(a,b)
-                                          # (ccg_mas_tform.cu)
+# Algorithmic shared-memory bytes of the D-form kernel (ccg_mas_dform.cu):
+DFORM_BYTES_PER_TRY = 4          # one exact delta D[a][b] read per executed evaluation
+DFORM_BYTES_PER_ACCEPT = 20332   # N update 5408 + T row/column swap 416 + u,v 208 + S factors
+                                 # 416 + saved rows 208 + rebuild of D 13676
+DFORM_BYTES_PER_WORKER = 25844   # N from scratch 8112 + score 4056 + first D 13676 (+8 B per
+                                 # ciphertext bigram for the count matrix)
 REF_LOOKUP_BYTES_PER_EVAL = 208 * 4    # reference-equivalent: 208 table lookups
 
 
@@ -283,6 +287,7 @@ def main():
     d_scores = ctx.dev_alloc(n_workers * 8)
     d_maps = ctx.dev_alloc(n_workers * 26)
     d_best = ctx.dev_alloc(len(ciphers) * 8)
+    d_acc = ctx.dev_alloc(n_workers * 8)
     a = _lib.MasClimbArgs()
     a.ciphers, a.offsets, a.n_ciphers = d_flat, d_off, len(ciphers)
     a.cipher_of, a.keys, a.skips = d_cof, d_keys, None
@@ -291,6 +296,7 @@ def main():
     a.group_size, a.group_best = W, d_best
     a.max_len, a.table_max = int(lengths.max()), int(scores.max())
     a.flags = 0
+    a.accepts = d_acc
     ctx.synchronize()
 
     stream = torch.cuda.ExternalStream(ctx.stream(), device=f"cuda:{device}")
@@ -335,7 +341,15 @@ def main():
     # per-launch duration of the dominant kernel (mas_climb; the group argmax is ~us)
     kernel_s = float(np.mean(step_ms)) / 1e3
     smem_peak = smem_bw.value / 1e9
-    achieved = evals_per_step * EXEC_LDS_BYTES_PER_EVAL / kernel_s / 1e9
+    acc = np.empty(n_workers, dtype=np.int64)
+    ctx.d2h(acc, d_acc)
+    ctx.synchronize()
+    n_accepts = int(acc.sum())
+    worker_bytes = sum(W * (DFORM_BYTES_PER_WORKER + 8 * (int(L) - 1)) for L in lengths)
+    launch_bytes = (DFORM_BYTES_PER_TRY * evals_per_step + DFORM_BYTES_PER_ACCEPT * n_accepts
+                    + worker_bytes)
+    bytes_per_eval = launch_bytes / evals_per_step
+    achieved = launch_bytes / kernel_s / 1e9
     traffic = None
     tfile = ROOT / "profiles" / "ncu_traffic.json"
     if tfile.exists():
@@ -404,12 +418,16 @@ def main():
             "e2e": e2e,
             "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
                          "frac": achieved / smem_peak, "traffic": traffic,
-                         "kernel": "mas_climb_tform_kernel<false>",
-                         "bytes_per_eval": EXEC_LDS_BYTES_PER_EVAL,
+                         "kernel": "mas_climb_dform_kernel<false>",
+                         "bytes_per_eval": bytes_per_eval,
+                         "accepts_per_eval": n_accepts / evals_per_step,
                          "peak_source": "measured on this GPU by ccg_bench_smem_bandwidth "
                                         "(128-bit conflict-free LDS, full occupancy)",
                          "ref_equiv_achieved": evals_per_step * REF_LOOKUP_BYTES_PER_EVAL
-                         / kernel_s / 1e9},
+                         / kernel_s / 1e9,
+                         "note": "algorithmic shared-memory bytes of the D-form algorithm "
+                                 "(DESIGN.md 3.1); the kernel is issue-bound, see "
+                                 "profiles/*_ncu.txt"},
             "cpu_baseline": cpu,
             "clocks": clk,
             "gpu_launches": launches,

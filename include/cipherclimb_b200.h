@@ -65,6 +65,13 @@ enum {
 
 /* flags for ccg_*_climb_args.flags */
 #define CCG_FLAG_EARLY_EXIT 1u /* stop a worker once no proposal can ever be accepted again */
+/* MAS kernel selection (results are identical; for tests and benchmarks).  0 = automatic:
+ * the D-form kernel (maintained delta table) when its integer gate holds, else the T-form,
+ * else the packed / wide count-matrix kernels. */
+#define CCG_FLAG_KERNEL_MASK 0x30u
+#define CCG_FLAG_KERNEL_DFORM 0x10u
+#define CCG_FLAG_KERNEL_TFORM 0x20u
+#define CCG_FLAG_KERNEL_PACKED 0x30u
 
 typedef struct ccg_ctx ccg_ctx;
 
@@ -130,6 +137,7 @@ typedef struct {
   int64_t max_len;            /* longest ciphertext */
   int64_t table_max;          /* max(table) */
   uint32_t flags;             /* CCG_FLAG_* */
+  int64_t *accepts;           /* [n_workers] accepted interchanges, or NULL */
 } ccg_mas_climb_args;
 
 int ccg_mas_climb(ccg_ctx *ctx, const ccg_mas_climb_args *args);

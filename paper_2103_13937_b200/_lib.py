@@ -20,6 +20,7 @@ ALPHA = 26
 
 CCG_OK, CCG_ERR_INVALID, CCG_ERR_CUDA, CCG_ERR_NO_DEVICE, CCG_ERR_UNSUPPORTED = 0, -1, -2, -3, -4
 FLAG_EARLY_EXIT = 1
+KERNEL_FLAGS = {"auto": 0, "dform": 0x10, "tform": 0x20, "packed": 0x30}
 
 
 class EngineError(RuntimeError):
@@ -36,7 +37,7 @@ class MasClimbArgs(C.Structure):
         ("skips", _P), ("n_workers", _i64), ("climbings", _i64), ("table", _P),
         ("scores", _P), ("maps", _P), ("draws_used", _P), ("last_accept", _P),
         ("tries_done", _P), ("group_size", _i32), ("group_best", _P), ("max_len", _i64),
-        ("table_max", _i64), ("flags", _u32),
+        ("table_max", _i64), ("flags", _u32), ("accepts", _P),
     ]
 
 

@@ -532,10 +532,17 @@ static int mas_launch(ccg_ctx* ctx, const ccg_mas_climb_args* a, int64_t max_len
   p.last_accept = a->last_accept;
   p.tries_done = a->tries_done;
   p.flags = a->flags;
+  p.accepts = a->accepts;
   ctx->launches++;
-  cudaError_t e = mas_tform_ok(max_len, tmax)
-                      ? launch_mas_climb_tform(ctx->stream, p, ctx->sm_count)
-                      : launch_mas_climb(ctx->stream, p, mas_needs_wide(max_len, tmax), ctx->sm_count);
+  cudaError_t e;
+  const uint32_t kern = a->flags & CCG_FLAG_KERNEL_MASK;
+  if ((kern == 0 || kern == CCG_FLAG_KERNEL_DFORM) && mas_dform_ok(max_len, tmax))
+    e = launch_mas_climb_dform(ctx->stream, p, ctx->sm_count);
+  else if ((kern == 0 || kern == CCG_FLAG_KERNEL_DFORM || kern == CCG_FLAG_KERNEL_TFORM) &&
+           mas_tform_ok(max_len, tmax))
+    e = launch_mas_climb_tform(ctx->stream, p, ctx->sm_count);
+  else
+    e = launch_mas_climb(ctx->stream, p, mas_needs_wide(max_len, tmax), ctx->sm_count);
   if (e != cudaSuccess) return cuda_fail(e, "mas_climb kernel");
   if (a->group_size > 0 && a->group_best) {
     ctx->launches++;
@@ -608,10 +615,12 @@ int ccg_mas_climb(ccg_ctx* ctx, const ccg_mas_climb_args* a) {
   if (a->draws_used) { if ((rc = ctx->buf(8, (size_t)nw * 8, &p))) return rc; d.draws_used = (uint64_t*)p; }
   if (a->last_accept) { if ((rc = ctx->buf(9, (size_t)nw * 8, &p))) return rc; d.last_accept = (int64_t*)p; }
   if (a->tries_done) { if ((rc = ctx->buf(10, (size_t)nw * 8, &p))) return rc; d.tries_done = (int64_t*)p; }
+  if (a->accepts) { if ((rc = ctx->buf(12, (size_t)nw * 8, &p))) return rc; d.accepts = (int64_t*)p; }
   const int64_t ng = a->group_size > 0 ? nw / a->group_size : 0;
   if (a->group_best && ng) { if ((rc = ctx->buf(11, (size_t)ng * 8, &p))) return rc; d.group_best = (int64_t*)p; }
   else d.group_best = nullptr;
   if ((rc = mas_launch(ctx, &d, max_len, tmax))) return rc;
+  if (a->accepts && (rc = download(ctx, a->accepts, d.accepts, (size_t)nw * 8))) return rc;
   if ((rc = download(ctx, a->scores, d.scores, (size_t)nw * 8))) return rc;
   if (a->maps && (rc = download(ctx, a->maps, d.maps, (size_t)nw * kAlpha))) return rc;
   if (a->draws_used && (rc = download(ctx, a->draws_used, d.draws_used, (size_t)nw * 8))) return rc;

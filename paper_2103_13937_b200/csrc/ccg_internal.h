@@ -33,6 +33,7 @@ struct MasLaunch {
   int64_t* last_accept;
   int64_t* tries_done;
   uint32_t flags;
+  int64_t* accepts;
 };
 
 // MAS climb with an order-G n-gram table (ccg_mas_ngram.cu).
@@ -127,6 +128,10 @@ cudaError_t launch_mas_climb(cudaStream_t s, const MasLaunch& p, bool wide, int 
 // T-form climb (ccg_mas_tform.cu): the fast path whenever mas_tform_ok(max_len, max(S)).
 bool mas_tform_ok(int64_t max_len, int64_t table_max);
 cudaError_t launch_mas_climb_tform(cudaStream_t s, const MasLaunch& p, int sm_count);
+// D-form climb (ccg_mas_dform.cu): maintained table of all 325 exact swap deltas, 32
+// proposals per warp instruction; the fast path whenever mas_dform_ok(max_len, max(S)).
+bool mas_dform_ok(int64_t max_len, int64_t table_max);
+cudaError_t launch_mas_climb_dform(cudaStream_t s, const MasLaunch& p, int sm_count);
 size_t mas_ngram_smem_bytes(int order, int64_t max_len);
 cudaError_t launch_mas_ngram_climb(cudaStream_t s, const MasNgramLaunch& p, int sm_count);
 cudaError_t launch_ngram_score(cudaStream_t s, const uint8_t* texts, const int64_t* offsets,

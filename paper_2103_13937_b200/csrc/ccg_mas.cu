@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(kMasWarps * 32, 4)
     win.o = 0;
     win.refill(lane);
 
-    int last = -1;
+    int last = -1, nacc = 0;
     uint32_t t = 0;
     uint32_t since = 0, next_check = 256;
     // exact local-optimum test over all 325 interchanges (CCG_FLAG_EARLY_EXIT)
@@ -212,15 +212,18 @@ __global__ void __launch_bounds__(kMasWarps * 32, 4)
           if (d1 > 0) {
             accept(a1, b1, xa1, xb1, d1);
             last = (int)t;
+            ++nacc;
             const int ya = __shfl_sync(kFull, inv, a2), yb = __shfl_sync(kFull, inv, b2);
             d2 = eval(a2, b2, ya, yb);
             if (d2 > 0) {
               accept(a2, b2, ya, yb, d2);
               last = (int)t + 1;
+              ++nacc;
             }
           } else if (d2 > 0) {
             accept(a2, b2, xa2, xb2, d2);
             last = (int)t + 1;
+            ++nacc;
           }
           t += 2;
           if (EARLY) {
@@ -235,6 +238,7 @@ __global__ void __launch_bounds__(kMasWarps * 32, 4)
           if (d > 0) {
             accept(a, b, xa, xb, d);
             last = (int)t;
+            ++nacc;
             since = 0;
             next_check = 256;
           } else {
@@ -259,6 +263,7 @@ __global__ void __launch_bounds__(kMasWarps * 32, 4)
           pv = lane == xa ? b : (lane == xb ? a : pv);
           inv = lane == a ? xb : (lane == b ? xa : inv);
           last = (int)t;
+          ++nacc;
           since = 0;
           next_check = 256;
         } else if (EARLY && ++since >= next_check) {
@@ -276,6 +281,7 @@ __global__ void __launch_bounds__(kMasWarps * 32, 4)
       p.scores[w] = score;
       if (p.draws_used) p.draws_used[w] = win.position();
       if (p.last_accept) p.last_accept[w] = last;
+      if (p.accepts) p.accepts[w] = nacc;
       if (p.tries_done) p.tries_done[w] = t;
     }
     __syncwarp();

@@ -1,0 +1,323 @@
+// ccg_mas_dform.cu -- the MAS stochastic climb with a maintained table of exact swap deltas
+// ("D-form"): the sm_100a fast path of mas.py:218-244 stochastic_worker.
+//
+// Why.  A rejected proposal does not change the state, and ~99% of proposals are rejected
+// (the reference accepts ~70 of 10,000 tries, mas.py:237).  The reference recomputes
+// swap_delta (mas.py:181-210, 208 lookups) for every try; between two accepts the same
+// state is re-scored over and over.  Here the warp keeps ALL 325 exact deltas of the
+// current state in shared memory,
+//     D[a][b] = swap_delta(counts, a, b, S),
+// and rebuilds them only when a proposal is accepted.  Evaluating a proposal is one lookup,
+// so 32 proposals are evaluated by one warp instruction (lane j takes proposal t+j) and a
+// ballot finds the first accepted one -- exactly the sequential outcome, because proposals
+// never read the state (rng.py:81-89).
+//
+// Algebra (all exact integers).  With T the bigram counts of the current plaintext:
+//   D[a][b] = kt(a,b) * ks(a,b) - (N[a][a] + N[b][b] - N[a][b] - N[b][a])
+//   kt = T[a][a] + T[b][b] - T[a][b] - T[b][a],  ks = the same on S (static),
+//   N[x][y] = sum_q T[x][q] S[y][q] + T[q][x] S[q][y],
+// which is the T-form identity of ccg_mas_tform.cu expanded over rows/columns.  Accepting
+// the interchange sigma = (a b) maps T'[x][y] = T[sigma x][sigma y], and
+//   N'[x][y] = N[sigma x][y] + (T[sx][a] - T[sx][b]) (S[y][b] - S[y][a])
+//                             + (T[a][sx] - T[b][sx]) (S[b][y] - S[a][y]),   sx = sigma x,
+// an O(676) update; D is then rebuilt from N, T and ks (325 pairs).
+//
+// Proposal stream.  The letter window is the byte window of ccg_mas_common.cuh (one
+// Philox4x64-10 block per lane per refill, int(u*26) exact).  A pair with equal letters
+// needs a redraw (rng.py:85-86) and shifts the pairing by one draw, so each lane reads
+// three letters and a round covers the aligned pairs before the first redraw, the redraw
+// pair itself, and the shifted pairs up to the next redraw (two ballots) -- ~30 tries per
+// round; anything rarer (a double redraw) goes through the sequential path.
+//
+// Gate: max(S) <= 32767, n <= 32768 and (n-1)*max(S) < 2^27 keep every N and D entry in
+// int32 (|D| < 12 (n-1) max(S)); the host falls back to the T-form / packed kernels.
+#include "ccg_mas_common.cuh"
+
+namespace ccg {
+namespace {
+
+constexpr int kDWarps = 8;
+constexpr int kTS = 34;  // T row stride (int16): column walks are conflict-free (17 words/row)
+constexpr int kNS = 33;  // N row stride (int32)
+constexpr int kDS = 32;  // D row stride (int32): D[a][b] sits in bank b
+constexpr int kPairsP = 352;  // 325 pairs padded to 11 x 32
+
+struct DWarp {
+  int16_t T[kAlpha * kTS];
+  int N[kAlpha * kNS];
+  int D[kAlpha * kDS];
+};
+struct DBlock {
+  int S[kAlpha * kNS];
+  int KS[kAlpha * kDS];
+  uint16_t pair[kPairsP];  // (x << 8) | y for the 325 pairs x < y, padding = 0
+  DWarp w[kDWarps];
+};
+
+__device__ __forceinline__ int t_at(const DWarp& W, int x, int y) { return W.T[x * kTS + y]; }
+
+// T[x][y] += 1 via a 32-bit shared atomic on the containing word (no 16-bit atomics)
+__device__ __forceinline__ void t_inc(DWarp& W, int x, int y) {
+  const uint32_t idx = (uint32_t)(x * kTS + y);
+  uint32_t* word = reinterpret_cast<uint32_t*>(W.T) + (idx >> 1);
+  atomicAdd(word, 1u << (16u * (idx & 1u)));
+}
+
+// D[x][y] for all x != y from the current T, N (and the static ks).  Lane y builds column
+// y, so every shared access is either a broadcast (diagonals, via shuffles) or lands in a
+// distinct bank (row strides 17, 33 and 32 words): no bank conflicts.
+__device__ __forceinline__ void rebuild_D(const DBlock& B, DWarp& W, int lane) {
+  __syncwarp();
+  const int y = lane < kAlpha ? lane : 0;
+  const int tyy = t_at(W, y, y), nyy = W.N[y * kNS + y];
+#pragma unroll
+  for (int x = 0; x < kAlpha; ++x) {
+    const int txx = __shfl_sync(kFull, tyy, x), nxx = __shfl_sync(kFull, nyy, x);
+    const int kt = txx + tyy - t_at(W, x, y) - t_at(W, y, x);
+    const int dv = kt * B.KS[x * kDS + y] - nxx - nyy + W.N[x * kNS + y] + W.N[y * kNS + x];
+    if (lane < kAlpha) W.D[x * kDS + y] = dv;
+  }
+  __syncwarp();
+}
+
+// max over the 325 deltas (exact local-optimum test)
+__device__ __forceinline__ int max_D(const DBlock& B, const DWarp& W, int lane) {
+  int m = (int)0x80000000;
+#pragma unroll
+  for (int i = 0; i < kPairsP / 32; ++i) {
+    const int e = lane + 32 * i;
+    if (e < 325) {
+      const int pr = B.pair[e];
+      m = max(m, W.D[(pr >> 8) * kDS + (pr & 0xff)]);
+    }
+  }
+  return __reduce_max_sync(kFull, m);
+}
+
+template <bool EARLY>
+__global__ void __launch_bounds__(kDWarps * 32, 3) mas_climb_dform_kernel(const MasLaunch p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  DBlock& B = *reinterpret_cast<DBlock*>(smem_raw);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  DWarp& W = B.w[warp];
+
+  for (int i = threadIdx.x; i < kAlpha * kAlpha; i += blockDim.x) {
+    const int x = i / kAlpha, y = i - x * kAlpha;
+    B.S[x * kNS + y] = (int)p.table[i];
+  }
+  for (int i = threadIdx.x; i < kPairsP; i += blockDim.x) {
+    int x = 0, rem = i;
+    while (x < kAlpha - 1 && rem >= kAlpha - 1 - x) {
+      rem -= kAlpha - 1 - x;
+      ++x;
+    }
+    B.pair[i] = i < 325 ? (uint16_t)((x << 8) | (x + 1 + rem)) : (uint16_t)0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kAlpha * kAlpha; i += blockDim.x) {
+    const int x = i / kAlpha, y = i - x * kAlpha;
+    B.KS[x * kDS + y] =
+        B.S[x * kNS + x] + B.S[y * kNS + y] - B.S[x * kNS + y] - B.S[y * kNS + x];
+  }
+  __syncthreads();
+
+  const int64_t stride = (int64_t)gridDim.x * kDWarps;
+  const uint32_t climbings = (uint32_t)p.climbings;
+  const int y = lane < kAlpha ? lane : 0;  // the column this lane owns in N updates
+
+  for (int64_t w = (int64_t)blockIdx.x * kDWarps + warp; w < p.n_workers; w += stride) {
+    const int32_t cid = p.cipher_of[w];
+    const int64_t off = p.offsets[cid], n = p.offsets[cid + 1] - off;
+    const uint8_t* text = p.ciphers + off;
+
+    // T = bigram counts of the ciphertext (the worker starts at the ciphertext, mas.py:229-230)
+    for (int i = lane; i < kAlpha * kTS / 2; i += 32) reinterpret_cast<uint32_t*>(W.T)[i] = 0u;
+    __syncwarp();
+    for (int64_t i = lane; i + 1 < n; i += 32) t_inc(W, text[i], text[i + 1]);
+    __syncwarp();
+    // N from scratch (lane y owns column y) and the score (mas.py:232)
+    int part = 0;
+    if (lane < kAlpha) {
+      for (int x = 0; x < kAlpha; ++x) {
+        int acc = 0;
+        for (int q = 0; q < kAlpha; ++q)
+          acc += t_at(W, x, q) * B.S[y * kNS + q] + t_at(W, q, x) * B.S[q * kNS + y];
+        W.N[x * kNS + y] = acc;
+        part += t_at(W, x, y) * B.S[x * kNS + y];
+      }
+    }
+    int64_t score = (int64_t)(int)__reduce_add_sync(kFull, (uint32_t)part);
+    rebuild_D(B, W, lane);
+
+    int pv = lane < kAlpha ? lane : 0;  // pi(lane): cipher letter -> plaintext letter
+    ByteWindow win;
+    win.key = p.keys + 2 * w;
+    win.base = p.skips ? p.skips[w] : 0;
+    win.o = 0;
+    win.refill(lane);
+
+    // commit the interchange a<->b (mas.py:237-243)
+    auto accept = [&](int a, int b, int d) {
+      score += d;
+      pv = pv == a ? b : (pv == b ? a : pv);
+      // lane x: u_x = T[sx][a] - T[sx][b], v_x = T[a][sx] - T[b][sx] (old T, sx = sigma x)
+      const int x = lane < kAlpha ? lane : 0;
+      const int sx = x == a ? b : (x == b ? a : x);
+      const int u = t_at(W, sx, a) - t_at(W, sx, b);
+      const int v = t_at(W, a, sx) - t_at(W, b, sx);
+      // lane y: S-column factors of its N column
+      const int sb = B.S[y * kNS + b] - B.S[y * kNS + a];
+      const int sc = B.S[b * kNS + y] - B.S[a * kNS + y];
+      const int na = W.N[a * kNS + y], nb = W.N[b * kNS + y];
+      const int ua = __shfl_sync(kFull, u, a), va = __shfl_sync(kFull, v, a);
+      const int ub = __shfl_sync(kFull, u, b), vb = __shfl_sync(kFull, v, b);
+      __syncwarp();
+      // N'[x][y] = N[sigma x][y] + u_x sb_y + v_x sc_y: rows other than a, b in place,
+      // rows a, b from the saved old rows
+#pragma unroll
+      for (int xx = 0; xx < kAlpha; ++xx) {
+        const int ux = __shfl_sync(kFull, u, xx), vx = __shfl_sync(kFull, v, xx);
+        if (lane < kAlpha) W.N[xx * kNS + y] += ux * sb + vx * sc;
+      }
+      if (lane < kAlpha) {
+        W.N[a * kNS + y] = nb + ua * sb + va * sc;
+        W.N[b * kNS + y] = na + ub * sb + vb * sc;
+      }
+      // swap rows a, b then columns a, b of T
+      int16_t ra = 0, rb = 0;
+      if (lane < kAlpha) {
+        ra = W.T[a * kTS + lane];
+        rb = W.T[b * kTS + lane];
+      }
+      __syncwarp();
+      if (lane < kAlpha) {
+        W.T[a * kTS + lane] = rb;
+        W.T[b * kTS + lane] = ra;
+      }
+      __syncwarp();
+      if (lane < kAlpha) {
+        ra = W.T[lane * kTS + a];
+        rb = W.T[lane * kTS + b];
+      }
+      __syncwarp();
+      if (lane < kAlpha) {
+        W.T[lane * kTS + a] = rb;
+        W.T[lane * kTS + b] = ra;
+      }
+      rebuild_D(B, W, lane);
+    };
+
+    int last = -1, nacc = 0;
+    uint32_t t = 0;
+    bool done = EARLY && max_D(B, W, lane) <= 0;
+    while (!done && t < climbings) {
+      if (win.o > 120u) win.refill(lane);
+      const uint32_t o = win.o;
+      // Lane j reads letters c0, c1, c2 = L[o+2j], L[o+2j+1], L[o+2j+2].  Pairs j < r0 are
+      // aligned (c0, c1); r0 is the first pair needing a redraw (c0 == c1); its partner is
+      // c2 of lane r0 unless that equals c0 too; the pairs after it are shifted by one draw
+      // (c1, c2) up to the next redraw.  rng.py:81-89 exactly.
+      const uint32_t pos = o + 2u * (uint32_t)lane;
+      const int src = (int)((pos >> 2) & 31u);
+      const uint32_t x0 = __shfl_sync(kFull, win.lo, src), x1 = __shfl_sync(kFull, win.hi, src);
+      const uint32_t wd = __funnelshift_r(x0, x1, (pos & 3u) * 8u);
+      const int c0 = (int)(wd & 0xffu), c1 = (int)((wd >> 8) & 0xffu), c2 = (int)((wd >> 16) & 0xffu);
+      const uint32_t nA = (128u - o) >> 1;  // pairs whose two letters are in the window
+      const uint32_t nB = (127u - o) >> 1;  // shifted pairs / redraw partners in the window
+      const uint32_t eqA = __ballot_sync(kFull, c0 == c1);
+      const uint32_t r0 = eqA ? (uint32_t)(__ffs(eqA) - 1) : 32u;
+      uint32_t R;          // pairs in this round
+      bool seq = false;    // the round stopped at a pair that needs the sequential path
+      if (r0 >= nA) {
+        R = min(nA, 32u);
+      } else {
+        const int c2r = __shfl_sync(kFull, c2, (int)r0), c0r = __shfl_sync(kFull, c0, (int)r0);
+        if (r0 >= nB || c2r == c0r) {
+          R = r0;
+          seq = true;
+        } else {
+          const uint32_t eqB = __ballot_sync(kFull, c1 == c2) & ~((2u << r0) - 1u);
+          R = eqB ? (uint32_t)(__ffs(eqB) - 1) : 32u;
+          R = min(R, nB);
+          seq = R < 32u && R < nB;
+        }
+      }
+      if (R > climbings - t) {
+        R = climbings - t;
+        seq = false;
+      }
+      const uint32_t j = (uint32_t)lane;
+      const int pa = j <= r0 ? c0 : c1;
+      const int pb = j < r0 ? c1 : c2;
+      const int d = j < R ? W.D[pa * kDS + pb] : 0;
+      const uint32_t acc = __ballot_sync(kFull, d > 0);
+      if (acc == 0) {  // the common case: R rejections
+        t += R;
+        win.o += 2u * R + (R > r0 ? 1u : 0u);
+        if (seq && t < climbings) {  // one try through the sequential redraw path
+          int a2, b2;
+          win.pair(lane, a2, b2);
+          const int d2 = W.D[a2 * kDS + b2];
+          if (d2 > 0) {
+            accept(a2, b2, d2);
+            last = (int)t;
+            ++nacc;
+            if (EARLY) done = max_D(B, W, lane) <= 0;
+          }
+          ++t;
+        }
+        continue;
+      }
+      const uint32_t k = (uint32_t)(__ffs(acc) - 1);  // the first accepted proposal
+      const int ak = __shfl_sync(kFull, pa, (int)k), bk = __shfl_sync(kFull, pb, (int)k);
+      const int dk = __shfl_sync(kFull, d, (int)k);
+      t += k;
+      win.o += 2u * (k + 1u) + (k + 1u > r0 ? 1u : 0u);
+      accept(ak, bk, dk);
+      last = (int)t;
+      ++nacc;
+      ++t;
+      if (EARLY) done = max_D(B, W, lane) <= 0;
+    }
+
+    if (lane < kAlpha && p.maps) p.maps[w * kAlpha + lane] = (uint8_t)pv;
+    if (lane == 0) {
+      p.scores[w] = score;
+      if (p.draws_used) p.draws_used[w] = win.position();
+      if (p.last_accept) p.last_accept[w] = last;
+      if (p.accepts) p.accepts[w] = nacc;
+      if (p.tries_done) p.tries_done[w] = t;
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
+bool mas_dform_ok(int64_t max_len, int64_t table_max) {
+  if (table_max > 32767 || max_len > 32768) return false;
+  const int64_t n1 = max_len > 0 ? max_len - 1 : 0;
+  return n1 * table_max < (int64_t(1) << 27);
+}
+
+cudaError_t launch_mas_climb_dform(cudaStream_t s, const MasLaunch& p, int sm_count) {
+  if (p.n_workers <= 0) return cudaSuccess;
+  auto kern = (p.flags & CCG_FLAG_EARLY_EXIT) ? mas_climb_dform_kernel<true>
+                                              : mas_climb_dform_kernel<false>;
+  const int smem = (int)sizeof(DBlock);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDWarps * 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t need = (p.n_workers + kDWarps - 1) / kDWarps;
+  const int64_t resident = (int64_t)per_sm * sm_count;
+  const int grid = (int)(need < resident ? need : resident);
+  kern<<<grid, kDWarps * 32, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace ccg

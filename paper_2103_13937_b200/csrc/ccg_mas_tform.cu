@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kTWarps * 32) mas_climb_tform_kernel(const Mas
       return false;
     };
 
-    int last = -1;
+    int last = -1, nacc = 0;
     uint32_t t = 0;
     uint32_t since = 0, next_check = 256;
     // Four proposals per iteration.  Proposals never depend on the state (rng.py:81-89
@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(kTWarps * 32) mas_climb_tform_kernel(const Mas
       if (d > 0) {
         accept((int)a, (int)b, d);
         last = (int)t;
+        ++nacc;
         dirty = true;
         since = 0;
         next_check = 256;
@@ -211,6 +212,7 @@ __global__ void __launch_bounds__(kTWarps * 32) mas_climb_tform_kernel(const Mas
         if (d > 0) {
           accept(a, b, d);
           last = (int)t;
+          ++nacc;
           since = 0;
           next_check = 256;
         } else {
@@ -232,6 +234,7 @@ __global__ void __launch_bounds__(kTWarps * 32) mas_climb_tform_kernel(const Mas
       if (d > 0) {
         accept(a, b, d);
         last = (int)t;
+        ++nacc;
       }
       ++t;
     }
@@ -241,6 +244,7 @@ __global__ void __launch_bounds__(kTWarps * 32) mas_climb_tform_kernel(const Mas
       p.scores[w] = score;
       if (p.draws_used) p.draws_used[w] = win.position();
       if (p.last_accept) p.last_accept[w] = last;
+      if (p.accepts) p.accepts[w] = nacc;
       if (p.tries_done) p.tries_done[w] = t;
     }
     __syncwarp();

@@ -70,6 +70,7 @@ class ClimbResult:
     last_accept: np.ndarray | None
     tries_done: np.ndarray | None
     launches: int
+    accepts: np.ndarray | None = None   # accepted interchanges per worker (bigram MAS kernels)
 
 
 def _run_sharded(n_workers, group_size, devs, fn):
@@ -90,13 +91,15 @@ def _concat(parts, name):
 
 def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, group_size=0,
               draws_used=False, last_accept=False, tries_done=False, early_exit=False,
-              order=2, ngram_kernel=False, devices_=None) -> ClimbResult:
+              order=2, ngram_kernel=False, kernel="auto", accepts=False,
+              devices_=None) -> ClimbResult:
     """Run stochastic_worker (mas.py:218-244) for every worker on the GPU(s).
 
     ciphers: list of letter arrays; cipher_of: int per worker; keys: uint64[n, 2] Philox
     keys (rng.philox_keys); table_scores: int64[26**order].  order 2 runs the bigram kernels
     (ccg_mas_climb); order 3/4 -- or ngram_kernel=True at order 2 -- the position-based
-    n-gram kernel (ccg_mas_ngram_climb, entries must fit uint16)."""
+    n-gram kernel (ccg_mas_ngram_climb, entries must fit uint16).  `kernel` selects the
+    bigram kernel ("auto", "dform", "tform", "packed"); results are identical."""
     flat, off = _lib.ragged(ciphers)
     cof = np.ascontiguousarray(cipher_of, dtype=np.int32).reshape(-1)
     keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, 2)
@@ -126,6 +129,7 @@ def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, 
             last_accept=np.empty(m, dtype=np.int64) if last_accept else None,
             tries_done=np.empty(m, dtype=np.int64) if tries_done else None,
             launches=0,
+            accepts=np.empty(m, dtype=np.int64) if (accepts and not use_ng) else None,
         )
         if m == 0:
             return out
@@ -133,6 +137,8 @@ def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, 
         k = np.ascontiguousarray(keys[lo:hi])
         s = None if sk is None else np.ascontiguousarray(sk[lo:hi])
         a = _lib.MasNgramArgs() if use_ng else _lib.MasClimbArgs()
+        if not use_ng:
+            a.accepts = _lib.ptr(out.accepts)
         a.ciphers, a.offsets, a.n_ciphers = _lib.ptr(flat), _lib.ptr(off), off.size - 1
         a.cipher_of, a.keys, a.skips = _lib.ptr(c_of), _lib.ptr(k), _lib.ptr(s)
         a.n_workers, a.climbings, a.table = m, int(climbings), _lib.ptr(table)
@@ -140,7 +146,7 @@ def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, 
         a.draws_used, a.last_accept = _lib.ptr(out.draws_used), _lib.ptr(out.last_accept)
         a.tries_done = _lib.ptr(out.tries_done)
         a.group_size, a.group_best = int(group_size), _lib.ptr(out.group_best)
-        a.flags = _lib.FLAG_EARLY_EXIT if early_exit else 0
+        a.flags = (_lib.FLAG_EARLY_EXIT if early_exit else 0) | _lib.KERNEL_FLAGS[kernel]
         if use_ng:
             a.order = order
         ctx = _lib.context(dev)
@@ -156,7 +162,7 @@ def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, 
         scores=_concat(parts, "scores"), keys=_concat(parts, "keys"),
         group_best=_concat(parts, "group_best"), draws_used=_concat(parts, "draws_used"),
         last_accept=_concat(parts, "last_accept"), tries_done=_concat(parts, "tries_done"),
-        launches=sum(p.launches for p in parts),
+        launches=sum(p.launches for p in parts), accepts=_concat(parts, "accepts"),
     )
 
 

@@ -587,3 +587,50 @@ def test_solve_sct_trigram_recovers_key(golden):
     want_s, _ = O.sct_workers([cipher], np.zeros(64, np.int32), [5] * 64, list(range(64)), l3.logs,
                               8, 4000, order=3)
     assert best.per_worker_scores == want_s.tolist()
+
+
+# ------------------------------------------------------------------ MAS kernel variants
+@pytest.mark.parametrize("early", [False, True])
+def test_mas_kernels_agree_with_oracle(early):
+    # the D-form (maintained delta table), T-form and packed count-matrix kernels must give
+    # the same per-worker outputs, equal to the oracle's stochastic_worker
+    rng = np.random.default_rng(77 + early)
+    ciphers = []
+    for L in [2, 3, 5, 26, 60, 100, 300, 471, 1000, 2000]:
+        c = rng.integers(0, int(rng.choice([2, 5, 26])), L)
+        ciphers.append(c)
+    table = rng.integers(0, 1000, 676)
+    cof = np.repeat(np.arange(len(ciphers), dtype=np.int32), 6)
+    streams = [int(rng.integers(0, 2**40)) for _ in cof]
+    keys = philox_keys([2024], streams)
+    outs = {}
+    for kern in ("dform", "tform", "packed"):
+        outs[kern] = engine.mas_climb(ciphers, cof, keys, table, 5000, kernel=kern, draws_used=True,
+                                      last_accept=True, tries_done=True, early_exit=early,
+                                      group_size=6, accepts=True)
+    want_s, want_m = O.mas_workers(ciphers, cof, [2024] * cof.size, streams, table, 5000)
+    for kern, r in outs.items():
+        assert r.scores.tolist() == want_s.tolist(), kern
+        for i, c in enumerate(cof):
+            assert np.array_equal(r.keys[i].astype(np.int64)[ciphers[c]], want_m[i][ciphers[c]]), kern
+        # the early-exit point is kernel-specific (each stops once it has proven that no
+        # proposal can be accepted); everything the reference defines must agree
+        fields = ("last_accept", "group_best", "accepts") if early else (
+            "draws_used", "last_accept", "tries_done", "group_best", "accepts")
+        for f in fields:
+            assert np.array_equal(getattr(r, f), getattr(outs["packed"], f)), (kern, f)
+    if not early:
+        assert (outs["dform"].tries_done == 5000).all()
+
+
+def test_dform_draw_position_continues_stream():
+    rng = np.random.default_rng(3)
+    table = rng.integers(0, 700, 676)
+    c = rng.integers(0, 26, 333)
+    key = philox_key(5, 17)
+    a = engine.mas_climb([c], [0], [key], table, 2345, kernel="dform", draws_used=True)
+    b = engine.mas_climb([c], [0], [key], table, 777, kernel="dform", skips=a.draws_used)
+    _, s_o, _, _ = O.stochastic_worker(c, table, 777, 5, 17, skip=int(a.draws_used[0]))
+    assert int(b.scores[0]) == s_o
+    assert int(a.draws_used[0]) == int(engine.mas_climb([c], [0], [key], table, 2345, kernel="packed",
+                                                        draws_used=True).draws_used[0])
