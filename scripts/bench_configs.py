@@ -213,7 +213,7 @@ def c5(args):
         tabs[o] = cc.quantize_log_table(cc.build_log_ngram_table(cc.build_ngram_table_from_corpus(corpus, o))).scores
     plain = G.plain_mas(300)
     cipher = np.random.default_rng(1).permutation(26)[plain]
-    K = 2000
+    K = 10_000
     sizes = [1000, 10_000, 100_000] + ([] if args.quick else [1_000_000])
     for order in (2, 3, 4):
         for n in sizes:
