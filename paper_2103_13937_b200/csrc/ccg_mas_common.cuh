@@ -60,15 +60,20 @@ struct ByteWindow {
   uint64_t base;  // stream index of window draw 0 (multiple of 4)
   uint32_t lo, hi;
   uint32_t o;     // window offset of the next draw
+  uint32_t rk = 0;  // shared address of precomputed round keys (philox_round_keys), or 0
 
   __device__ __forceinline__ void refill(int lane) {
     const uint64_t pos = base + o;
     base = pos & ~3ULL;
     o = (uint32_t)(pos & 3);
     uint64_t v0, v1, v2, v3;
-    philox4x64_10(__ldg(key), __ldg(key + 1), (base >> 2) + 1 + (uint64_t)lane, v0, v1, v2, v3);
-    lo = int_below_small(v0, 26) | (int_below_small(v1, 26) << 8) |
-         (int_below_small(v2, 26) << 16) | (int_below_small(v3, 26) << 24);
+    const uint64_t ctr = (base >> 2) + 1 + (uint64_t)lane;
+    if (rk)
+      philox4x64_10_rk(rk, ctr, v0, v1, v2, v3);
+    else
+      philox4x64_10(__ldg(key), __ldg(key + 1), ctr, v0, v1, v2, v3);
+    lo = int_below_tiny(v0, 26) | (int_below_tiny(v1, 26) << 8) |
+         (int_below_tiny(v2, 26) << 16) | (int_below_tiny(v3, 26) << 24);
     hi = __shfl_down_sync(kFull, lo, 1);
   }
   // letters of draws o .. o+3, one per byte; valid when o <= 124

@@ -40,9 +40,9 @@ constexpr int kDWarps = 8;
 constexpr int kTS = 34;  // T row stride (int16): column walks are conflict-free (17 words/row)
 constexpr int kNS = 33;  // N row stride (int32)
 constexpr int kDS = 32;  // D row stride (int32): D[a][b] sits in bank b
-constexpr int kPairsP = 352;  // 325 pairs padded to 11 x 32
 
-struct DWarp {
+struct alignas(16) DWarp {
+  uint64_t rk[20];  // Philox round keys of the current worker's stream
   int16_t T[kAlpha * kTS];
   int N[kAlpha * kNS];
   int D[kAlpha * kDS];
@@ -50,7 +50,6 @@ struct DWarp {
 struct DBlock {
   int S[kAlpha * kNS];
   int KS[kAlpha * kDS];
-  uint16_t pair[kPairsP];  // (x << 8) | y for the 325 pairs x < y, padding = 0
   DWarp w[kDWarps];
 };
 
@@ -80,17 +79,12 @@ __device__ __forceinline__ void rebuild_D(const DBlock& B, DWarp& W, int lane) {
   __syncwarp();
 }
 
-// max over the 325 deltas (exact local-optimum test)
-__device__ __forceinline__ int max_D(const DBlock& B, const DWarp& W, int lane) {
+// max over the 325 deltas (exact local-optimum test); lane y scans column y
+__device__ __forceinline__ int max_D(const DWarp& W, int lane) {
   int m = (int)0x80000000;
-#pragma unroll
-  for (int i = 0; i < kPairsP / 32; ++i) {
-    const int e = lane + 32 * i;
-    if (e < 325) {
-      const int pr = B.pair[e];
-      m = max(m, W.D[(pr >> 8) * kDS + (pr & 0xff)]);
-    }
-  }
+  if (lane < kAlpha)
+    for (int x = 0; x < kAlpha; ++x)
+      if (x != lane) m = max(m, W.D[x * kDS + lane]);
   return __reduce_max_sync(kFull, m);
 }
 
@@ -104,14 +98,6 @@ __global__ void __launch_bounds__(kDWarps * 32, 3) mas_climb_dform_kernel(const 
   for (int i = threadIdx.x; i < kAlpha * kAlpha; i += blockDim.x) {
     const int x = i / kAlpha, y = i - x * kAlpha;
     B.S[x * kNS + y] = (int)p.table[i];
-  }
-  for (int i = threadIdx.x; i < kPairsP; i += blockDim.x) {
-    int x = 0, rem = i;
-    while (x < kAlpha - 1 && rem >= kAlpha - 1 - x) {
-      rem -= kAlpha - 1 - x;
-      ++x;
-    }
-    B.pair[i] = i < 325 ? (uint16_t)((x << 8) | (x + 1 + rem)) : (uint16_t)0;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kAlpha * kAlpha; i += blockDim.x) {
@@ -152,6 +138,9 @@ __global__ void __launch_bounds__(kDWarps * 32, 3) mas_climb_dform_kernel(const 
     int pv = lane < kAlpha ? lane : 0;  // pi(lane): cipher letter -> plaintext letter
     ByteWindow win;
     win.key = p.keys + 2 * w;
+    philox_round_keys(W.rk, __ldg(win.key), __ldg(win.key + 1), lane);
+    __syncwarp();
+    win.rk = smem_addr(W.rk);
     win.base = p.skips ? p.skips[w] : 0;
     win.o = 0;
     win.refill(lane);
@@ -209,7 +198,7 @@ __global__ void __launch_bounds__(kDWarps * 32, 3) mas_climb_dform_kernel(const 
 
     int last = -1, nacc = 0;
     uint32_t t = 0;
-    bool done = EARLY && max_D(B, W, lane) <= 0;
+    bool done = EARLY && max_D(W, lane) <= 0;
     while (!done && t < climbings) {
       if (win.o > 120u) win.refill(lane);
       const uint32_t o = win.o;
@@ -262,7 +251,7 @@ __global__ void __launch_bounds__(kDWarps * 32, 3) mas_climb_dform_kernel(const 
             accept(a2, b2, d2);
             last = (int)t;
             ++nacc;
-            if (EARLY) done = max_D(B, W, lane) <= 0;
+            if (EARLY) done = max_D(W, lane) <= 0;
           }
           ++t;
         }
@@ -277,7 +266,7 @@ __global__ void __launch_bounds__(kDWarps * 32, 3) mas_climb_dform_kernel(const 
       last = (int)t;
       ++nacc;
       ++t;
-      if (EARLY) done = max_D(B, W, lane) <= 0;
+      if (EARLY) done = max_D(W, lane) <= 0;
     }
 
     if (lane < kAlpha && p.maps) p.maps[w * kAlpha + lane] = (uint8_t)pv;

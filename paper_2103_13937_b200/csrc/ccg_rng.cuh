@@ -72,6 +72,43 @@ __device__ __forceinline__ uint32_t int_below_small(uint64_t x, uint32_t bound) 
   return q;
 }
 
+// Same for 1 <= bound < 2^11 from the top 32 bits: with A = (x >> 32) * bound, the product
+// m * bound (m = x >> 11) lies in [A, A + bound) * 2^21, so int(u*bound) = A >> 32 exactly --
+// including the float rounding, whose carry needs a fraction within 2^10 of 1 -- unless the
+// low word of A is within `bound` of wrapping (probability bound / 2^32), where the exact
+// test above decides.
+__device__ __forceinline__ uint32_t int_below_tiny(uint64_t x, uint32_t bound) {
+  const uint64_t A = (uint64_t)(uint32_t)(x >> 32) * bound;
+  if ((uint32_t)A < 0u - bound) return (uint32_t)(A >> 32);
+  return int_below_small(x, bound);
+}
+
+// Philox4x64-10 with the ten round keys (k0 + r*W0, k1 + r*W1) precomputed in shared memory
+// at `rk` (20 x u64, see philox_round_keys): one broadcast LDS.128 per round instead of two
+// 64-bit key additions.
+__device__ __forceinline__ void philox_round_keys(uint64_t* rk, uint64_t k0, uint64_t k1,
+                                                  int lane) {
+  if (lane < 10) {
+    rk[2 * lane] = k0 + (uint64_t)lane * kPhiloxW0;
+    rk[2 * lane + 1] = k1 + (uint64_t)lane * kPhiloxW1;
+  }
+}
+__device__ __forceinline__ void philox4x64_10_rk(uint32_t rk, uint64_t c0, uint64_t& o0,
+                                                 uint64_t& o1, uint64_t& o2, uint64_t& o3) {
+  uint64_t x0 = c0, x1 = 0, x2 = 0, x3 = 0;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint64_t k0, k1;
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(k0), "=l"(k1) : "r"(rk + 16u * r));
+    const uint64_t lo0 = kPhiloxM0 * x0, hi0 = __umul64hi(kPhiloxM0, x0);
+    const uint64_t lo1 = kPhiloxM1 * x2, hi1 = __umul64hi(kPhiloxM1, x2);
+    const uint64_t n0 = hi1 ^ x1 ^ k0;
+    const uint64_t n2 = hi0 ^ x3 ^ k1;
+    x0 = n0; x1 = lo1; x2 = n2; x3 = lo0;
+  }
+  o0 = x0; o1 = x1; o2 = x2; o3 = x3;
+}
+
 // u in [0,1) exactly as numpy: (x >> 11) * 2^-53.
 __device__ __forceinline__ double to_uniform(uint64_t x) {
   return (double)(x >> 11) * (1.0 / 9007199254740992.0);
