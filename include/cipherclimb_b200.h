@@ -68,10 +68,11 @@ enum {
 /* MAS kernel selection (results are identical; for tests and benchmarks).  0 = automatic:
  * the D-form kernel (maintained delta table) when its integer gate holds, else the T-form,
  * else the packed / wide count-matrix kernels. */
-#define CCG_FLAG_KERNEL_MASK 0x30u
-#define CCG_FLAG_KERNEL_DFORM 0x10u
+#define CCG_FLAG_KERNEL_MASK 0x70u
+#define CCG_FLAG_KERNEL_DFORM 0x10u  /* deltas computed on demand from the maintained N, T */
 #define CCG_FLAG_KERNEL_TFORM 0x20u
 #define CCG_FLAG_KERNEL_PACKED 0x30u
+#define CCG_FLAG_KERNEL_DTABLE 0x40u /* D-form with the full delta table kept in smem */
 
 typedef struct ccg_ctx ccg_ctx;
 

@@ -536,10 +536,10 @@ static int mas_launch(ccg_ctx* ctx, const ccg_mas_climb_args* a, int64_t max_len
   ctx->launches++;
   cudaError_t e;
   const uint32_t kern = a->flags & CCG_FLAG_KERNEL_MASK;
-  if ((kern == 0 || kern == CCG_FLAG_KERNEL_DFORM) && mas_dform_ok(max_len, tmax))
+  const bool dform = kern == 0 || kern == CCG_FLAG_KERNEL_DFORM || kern == CCG_FLAG_KERNEL_DTABLE;
+  if (dform && mas_dform_ok(max_len, tmax))
     e = launch_mas_climb_dform(ctx->stream, p, ctx->sm_count);
-  else if ((kern == 0 || kern == CCG_FLAG_KERNEL_DFORM || kern == CCG_FLAG_KERNEL_TFORM) &&
-           mas_tform_ok(max_len, tmax))
+  else if ((dform || kern == CCG_FLAG_KERNEL_TFORM) && mas_tform_ok(max_len, tmax))
     e = launch_mas_climb_tform(ctx->stream, p, ctx->sm_count);
   else
     e = launch_mas_climb(ctx->stream, p, mas_needs_wide(max_len, tmax), ctx->sm_count);

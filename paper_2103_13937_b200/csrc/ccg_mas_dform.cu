@@ -41,22 +41,28 @@ constexpr int kTS = 34;  // T row stride (int16): column walks are conflict-free
 constexpr int kNS = 33;  // N row stride (int32)
 constexpr int kDS = 32;  // D row stride (int32): D[a][b] sits in bank b
 
+// TABLE = true keeps D in shared memory (rebuilt on every accept); TABLE = false computes
+// each looked-up delta from T, N and ks on demand (no rebuild, 3.3 KB less per warp).
+template <bool TABLE>
 struct alignas(16) DWarp {
   uint64_t rk[20];  // Philox round keys of the current worker's stream
   int16_t T[kAlpha * kTS];
   int N[kAlpha * kNS];
-  int D[kAlpha * kDS];
+  int D[TABLE ? kAlpha * kDS : 4];
 };
+template <bool TABLE>
 struct DBlock {
   int S[kAlpha * kNS];
   int KS[kAlpha * kDS];
-  DWarp w[kDWarps];
+  DWarp<TABLE> w[kDWarps];
 };
 
-__device__ __forceinline__ int t_at(const DWarp& W, int x, int y) { return W.T[x * kTS + y]; }
+template <class WT>
+__device__ __forceinline__ int t_at(const WT& W, int x, int y) { return W.T[x * kTS + y]; }
 
 // T[x][y] += 1 via a 32-bit shared atomic on the containing word (no 16-bit atomics)
-__device__ __forceinline__ void t_inc(DWarp& W, int x, int y) {
+template <class WT>
+__device__ __forceinline__ void t_inc(WT& W, int x, int y) {
   const uint32_t idx = (uint32_t)(x * kTS + y);
   uint32_t* word = reinterpret_cast<uint32_t*>(W.T) + (idx >> 1);
   atomicAdd(word, 1u << (16u * (idx & 1u)));
@@ -65,7 +71,8 @@ __device__ __forceinline__ void t_inc(DWarp& W, int x, int y) {
 // D[x][y] for all x != y from the current T, N (and the static ks).  Lane y builds column
 // y, so every shared access is either a broadcast (diagonals, via shuffles) or lands in a
 // distinct bank (row strides 17, 33 and 32 words): no bank conflicts.
-__device__ __forceinline__ void rebuild_D(const DBlock& B, DWarp& W, int lane) {
+template <class BT, class WT>
+__device__ __forceinline__ void rebuild_D(const BT& B, WT& W, int lane) {
   __syncwarp();
   const int y = lane < kAlpha ? lane : 0;
   const int tyy = t_at(W, y, y), nyy = W.N[y * kNS + y];
@@ -79,8 +86,30 @@ __device__ __forceinline__ void rebuild_D(const DBlock& B, DWarp& W, int lane) {
   __syncwarp();
 }
 
+// D[a][b] from T, N and ks; tdg / ndg hold T[lane][lane] / N[lane][lane] (all lanes call)
+template <class BT, class WT>
+__device__ __forceinline__ int delta_at(const BT& B, const WT& W, int tdg, int ndg, int a, int b) {
+  const int ta = __shfl_sync(kFull, tdg, a), tb = __shfl_sync(kFull, tdg, b);
+  const int na = __shfl_sync(kFull, ndg, a), nb = __shfl_sync(kFull, ndg, b);
+  const int kt = ta + tb - t_at(W, a, b) - t_at(W, b, a);
+  return kt * B.KS[a * kDS + b] - na - nb + W.N[a * kNS + b] + W.N[b * kNS + a];
+}
+
+// max over the 325 on-demand deltas; lane y scans column y
+template <class BT, class WT>
+__device__ __forceinline__ int max_delta(const BT& B, const WT& W, int tdg, int ndg, int lane) {
+  int m = (int)0x80000000;
+  const int y = lane < kAlpha ? lane : 0;
+  for (int x = 0; x < kAlpha; ++x) {
+    const int dv = delta_at(B, W, tdg, ndg, x, y);
+    if (lane < kAlpha && x != lane) m = max(m, dv);
+  }
+  return __reduce_max_sync(kFull, m);
+}
+
 // max over the 325 deltas (exact local-optimum test); lane y scans column y
-__device__ __forceinline__ int max_D(const DWarp& W, int lane) {
+template <class WT>
+__device__ __forceinline__ int max_D(const WT& W, int lane) {
   int m = (int)0x80000000;
   if (lane < kAlpha)
     for (int x = 0; x < kAlpha; ++x)
@@ -88,12 +117,12 @@ __device__ __forceinline__ int max_D(const DWarp& W, int lane) {
   return __reduce_max_sync(kFull, m);
 }
 
-template <bool EARLY>
-__global__ void __launch_bounds__(kDWarps * 32, 3) mas_climb_dform_kernel(const MasLaunch p) {
+template <bool EARLY, bool TABLE>
+__global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_kernel(const MasLaunch p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  DBlock& B = *reinterpret_cast<DBlock*>(smem_raw);
+  DBlock<TABLE>& B = *reinterpret_cast<DBlock<TABLE>*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  DWarp& W = B.w[warp];
+  DWarp<TABLE>& W = B.w[warp];
 
   for (int i = threadIdx.x; i < kAlpha * kAlpha; i += blockDim.x) {
     const int x = i / kAlpha, y = i - x * kAlpha;
@@ -133,7 +162,14 @@ __global__ void __launch_bounds__(kDWarps * 32, 3) mas_climb_dform_kernel(const 
       }
     }
     int64_t score = (int64_t)(int)__reduce_add_sync(kFull, (uint32_t)part);
-    rebuild_D(B, W, lane);
+    int tdg = 0, ndg = 0;  // T[lane][lane], N[lane][lane] (on-demand deltas)
+    if (TABLE) {
+      rebuild_D(B, W, lane);
+    } else {
+      __syncwarp();
+      tdg = t_at(W, y, y);
+      ndg = W.N[y * kNS + y];
+    }
 
     int pv = lane < kAlpha ? lane : 0;  // pi(lane): cipher letter -> plaintext letter
     ByteWindow win;
@@ -193,12 +229,21 @@ __global__ void __launch_bounds__(kDWarps * 32, 3) mas_climb_dform_kernel(const 
         W.T[lane * kTS + a] = rb;
         W.T[lane * kTS + b] = ra;
       }
-      rebuild_D(B, W, lane);
+      if (TABLE) {
+        rebuild_D(B, W, lane);
+      } else {
+        __syncwarp();
+        tdg = t_at(W, y, y);
+        ndg = W.N[y * kNS + y];
+      }
+    };
+    auto optimum = [&]() {
+      return TABLE ? max_D(W, lane) <= 0 : max_delta(B, W, tdg, ndg, lane) <= 0;
     };
 
     int last = -1, nacc = 0;
     uint32_t t = 0;
-    bool done = EARLY && max_D(W, lane) <= 0;
+    bool done = EARLY && optimum();
     while (!done && t < climbings) {
       if (win.o > 120u) win.refill(lane);
       const uint32_t o = win.o;
@@ -238,7 +283,13 @@ __global__ void __launch_bounds__(kDWarps * 32, 3) mas_climb_dform_kernel(const 
       const uint32_t j = (uint32_t)lane;
       const int pa = j <= r0 ? c0 : c1;
       const int pb = j < r0 ? c1 : c2;
-      const int d = j < R ? W.D[pa * kDS + pb] : 0;
+      int d;
+      if (TABLE) {
+        d = j < R ? W.D[pa * kDS + pb] : 0;
+      } else {
+        d = delta_at(B, W, tdg, ndg, pa, pb);
+        d = j < R ? d : 0;
+      }
       const uint32_t acc = __ballot_sync(kFull, d > 0);
       if (acc == 0) {  // the common case: R rejections
         t += R;
@@ -246,12 +297,12 @@ __global__ void __launch_bounds__(kDWarps * 32, 3) mas_climb_dform_kernel(const 
         if (seq && t < climbings) {  // one try through the sequential redraw path
           int a2, b2;
           win.pair(lane, a2, b2);
-          const int d2 = W.D[a2 * kDS + b2];
+          const int d2 = TABLE ? W.D[a2 * kDS + b2] : delta_at(B, W, tdg, ndg, a2, b2);
           if (d2 > 0) {
             accept(a2, b2, d2);
             last = (int)t;
             ++nacc;
-            if (EARLY) done = max_D(W, lane) <= 0;
+            if (EARLY) done = optimum();
           }
           ++t;
         }
@@ -266,7 +317,7 @@ __global__ void __launch_bounds__(kDWarps * 32, 3) mas_climb_dform_kernel(const 
       last = (int)t;
       ++nacc;
       ++t;
-      if (EARLY) done = max_D(W, lane) <= 0;
+      if (EARLY) done = optimum();
     }
 
     if (lane < kAlpha && p.maps) p.maps[w * kAlpha + lane] = (uint8_t)pv;
@@ -291,9 +342,11 @@ bool mas_dform_ok(int64_t max_len, int64_t table_max) {
 
 cudaError_t launch_mas_climb_dform(cudaStream_t s, const MasLaunch& p, int sm_count) {
   if (p.n_workers <= 0) return cudaSuccess;
-  auto kern = (p.flags & CCG_FLAG_EARLY_EXIT) ? mas_climb_dform_kernel<true>
-                                              : mas_climb_dform_kernel<false>;
-  const int smem = (int)sizeof(DBlock);
+  const bool table = (p.flags & CCG_FLAG_KERNEL_MASK) == CCG_FLAG_KERNEL_DTABLE;
+  auto kern = (p.flags & CCG_FLAG_EARLY_EXIT)
+                  ? (table ? mas_climb_dform_kernel<true, true> : mas_climb_dform_kernel<true, false>)
+                  : (table ? mas_climb_dform_kernel<false, true> : mas_climb_dform_kernel<false, false>);
+  const int smem = table ? (int)sizeof(DBlock<true>) : (int)sizeof(DBlock<false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);

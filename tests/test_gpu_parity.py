@@ -604,7 +604,7 @@ def test_mas_kernels_agree_with_oracle(early):
     streams = [int(rng.integers(0, 2**40)) for _ in cof]
     keys = philox_keys([2024], streams)
     outs = {}
-    for kern in ("dform", "tform", "packed"):
+    for kern in ("dform", "dtable", "tform", "packed"):
         outs[kern] = engine.mas_climb(ciphers, cof, keys, table, 5000, kernel=kern, draws_used=True,
                                       last_accept=True, tries_done=True, early_exit=early,
                                       group_size=6, accepts=True)
