@@ -37,10 +37,11 @@ sys.path.insert(0, str(ROOT))
 
 KEYGEN_STREAM = 2**32 - 2
 # Algorithmic shared-memory bytes of the D-form kernel (ccg_mas_dform.cu):
-DFORM_BYTES_PER_TRY = 4          # one exact delta D[a][b] read per executed evaluation
-DFORM_BYTES_PER_ACCEPT = 20332   # N update 5408 + T row/column swap 416 + u,v 208 + S factors
-                                 # 416 + saved rows 208 + rebuild of D 13676
-DFORM_BYTES_PER_WORKER = 25844   # N from scratch 8112 + score 4056 + first D 13676 (+8 B per
+DFORM_BYTES_PER_TRY = 16         # exact delta of the proposal: T[a][b], T[b][a] (2 B each),
+                                 # N[a][b], N[b][a], ks[a][b] (4 B each)
+DFORM_BYTES_PER_ACCEPT = 6812    # N update 5408 + T row/column swap 416 + u,v 208 + S factors
+                                 # 416 + saved rows 208 + diagonal refresh 156
+DFORM_BYTES_PER_WORKER = 12324   # N from scratch 8112 + score 4056 + diagonals 156 (+8 B per
                                  # ciphertext bigram for the count matrix)
 REF_LOOKUP_BYTES_PER_EVAL = 208 * 4    # reference-equivalent: 208 table lookups
 
@@ -426,8 +427,9 @@ def main():
                          "ref_equiv_achieved": evals_per_step * REF_LOOKUP_BYTES_PER_EVAL
                          / kernel_s / 1e9,
                          "note": "algorithmic shared-memory bytes of the D-form algorithm "
-                                 "(DESIGN.md 3.1); the kernel is issue-bound, see "
-                                 "profiles/*_ncu.txt"},
+                                 "(DESIGN.md 3.1); the kernel is issue-bound (ncu: ~67% of "
+                                 "issue slots, 12.5 warp instructions per evaluation, "
+                                 "profiles/r1d_ncu.txt)"},
             "cpu_baseline": cpu,
             "clocks": clk,
             "gpu_launches": launches,
