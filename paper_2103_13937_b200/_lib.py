@@ -230,13 +230,46 @@ def context(device: int = 0) -> Context:
     return ctx
 
 
+class Packed:
+    """A pre-packed ragged batch of letter arrays: uint8 letters + int64 offsets[n+1]
+    (what every batch entry point hands to the C ABI).  Pass it instead of a list to skip
+    the per-call packing."""
+
+    def __init__(self, flat, offsets):
+        self.flat = np.ascontiguousarray(flat, dtype=np.uint8)
+        self.offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+        if self.offsets.ndim != 1 or self.offsets.size < 1 or self.offsets[0] != 0:
+            raise ValueError("offsets must be int64[n+1] starting at 0")
+        if self.offsets[-1] != self.flat.size or (np.diff(self.offsets) < 0).any():
+            raise ValueError("offsets must be non-decreasing and end at len(flat)")
+        if self.flat.size and self.flat.max() >= ALPHA:
+            raise ValueError("letter indices must lie in 0..25")
+
+    def __len__(self):
+        return self.offsets.size - 1
+
+    def __getitem__(self, i):
+        return self.flat[self.offsets[i]:self.offsets[i + 1]]
+
+    @classmethod
+    def of(cls, texts) -> "Packed":
+        flat, off = ragged(texts)
+        p = cls.__new__(cls)
+        p.flat, p.offsets = flat, off
+        return p
+
+
 def ragged(texts) -> tuple[np.ndarray, np.ndarray]:
     """Concatenate letter arrays into (uint8 flat, int64 offsets[n+1])."""
-    arrs = [np.asarray(t, dtype=np.int64) for t in texts]
-    offsets = np.zeros(len(arrs) + 1, dtype=np.int64)
-    if arrs:
-        offsets[1:] = np.cumsum([a.size for a in arrs])
-    flat = np.concatenate(arrs) if arrs else np.zeros(0, dtype=np.int64)
+    if isinstance(texts, Packed):
+        return texts.flat, texts.offsets
+    n = len(texts)
+    offsets = np.zeros(n + 1, dtype=np.int64)
+    if n == 0:
+        return np.zeros(0, dtype=np.uint8), offsets
+    arrs = [t if isinstance(t, np.ndarray) else np.asarray(t, dtype=np.int64) for t in texts]
+    offsets[1:] = np.cumsum(np.fromiter((a.size for a in arrs), dtype=np.int64, count=n))
+    flat = np.concatenate([a.reshape(-1) for a in arrs]) if offsets[-1] else np.zeros(0, np.int64)
     if flat.size and (flat.min() < 0 or flat.max() >= ALPHA):
         raise ValueError("letter indices must lie in 0..25")
     return np.ascontiguousarray(flat, dtype=np.uint8), offsets

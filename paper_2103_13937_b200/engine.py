@@ -92,14 +92,16 @@ def _concat(parts, name):
 def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, group_size=0,
               draws_used=False, last_accept=False, tries_done=False, early_exit=False,
               order=2, ngram_kernel=False, kernel="auto", accepts=False,
-              devices_=None) -> ClimbResult:
+              out: ClimbResult | None = None, devices_=None) -> ClimbResult:
     """Run stochastic_worker (mas.py:218-244) for every worker on the GPU(s).
 
     ciphers: list of letter arrays; cipher_of: int per worker; keys: uint64[n, 2] Philox
     keys (rng.philox_keys); table_scores: int64[26**order].  order 2 runs the bigram kernels
     (ccg_mas_climb); order 3/4 -- or ngram_kernel=True at order 2 -- the position-based
     n-gram kernel (ccg_mas_ngram_climb, entries must fit uint16).  `kernel` selects the
-    bigram kernel ("auto", "dform", "tform", "packed"); results are identical."""
+    bigram kernel ("auto", "dform", "dtable", "tform", "packed"); results are identical.
+    `ciphers` may be a list of letter arrays or a pre-packed _lib.Packed batch; `out` may
+    supply the result arrays (e.g. in pinned host memory) for the whole batch."""
     flat, off = _lib.ragged(ciphers)
     cof = np.ascontiguousarray(cipher_of, dtype=np.int32).reshape(-1)
     keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, 2)
@@ -119,18 +121,32 @@ def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, 
     sk = None if skips is None else np.ascontiguousarray(skips, dtype=np.uint64).reshape(-1)
     devs = devices_ or devices()
 
+    given = out
+
+    def view(arr, lo_, hi_):
+        return None if arr is None else arr[lo_:hi_]
+
     def run(dev, lo, hi):
         m = hi - lo
-        out = ClimbResult(
-            scores=np.empty(m, dtype=np.int64),
-            keys=np.empty((m, 26), dtype=np.uint8),
-            group_best=np.empty(m // group_size, dtype=np.int64) if group_size > 0 else None,
-            draws_used=np.empty(m, dtype=np.uint64) if draws_used else None,
-            last_accept=np.empty(m, dtype=np.int64) if last_accept else None,
-            tries_done=np.empty(m, dtype=np.int64) if tries_done else None,
-            launches=0,
-            accepts=np.empty(m, dtype=np.int64) if (accepts and not use_ng) else None,
-        )
+        if given is not None:
+            g0, g1 = (lo // group_size, hi // group_size) if group_size > 0 else (0, 0)
+            out = ClimbResult(
+                scores=given.scores[lo:hi], keys=given.keys[lo:hi],
+                group_best=view(given.group_best, g0, g1) if group_size > 0 else None,
+                draws_used=view(given.draws_used, lo, hi), last_accept=view(given.last_accept, lo, hi),
+                tries_done=view(given.tries_done, lo, hi), launches=0,
+                accepts=view(given.accepts, lo, hi) if not use_ng else None)
+        else:
+            out = ClimbResult(
+                scores=np.empty(m, dtype=np.int64),
+                keys=np.empty((m, 26), dtype=np.uint8),
+                group_best=np.empty(m // group_size, dtype=np.int64) if group_size > 0 else None,
+                draws_used=np.empty(m, dtype=np.uint64) if draws_used else None,
+                last_accept=np.empty(m, dtype=np.int64) if last_accept else None,
+                tries_done=np.empty(m, dtype=np.int64) if tries_done else None,
+                launches=0,
+                accepts=np.empty(m, dtype=np.int64) if (accepts and not use_ng) else None,
+            )
         if m == 0:
             return out
         c_of = np.ascontiguousarray(cof[lo:hi])
@@ -158,6 +174,9 @@ def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, 
         return out
 
     parts = _run_sharded(n, group_size, devs, run)
+    if given is not None:
+        given.launches = sum(p.launches for p in parts)
+        return given
     return ClimbResult(
         scores=_concat(parts, "scores"), keys=_concat(parts, "keys"),
         group_best=_concat(parts, "group_best"), draws_used=_concat(parts, "draws_used"),

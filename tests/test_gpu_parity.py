@@ -634,3 +634,23 @@ def test_dform_draw_position_continues_stream():
     assert int(b.scores[0]) == s_o
     assert int(a.draws_used[0]) == int(engine.mas_climb([c], [0], [key], table, 2345, kernel="packed",
                                                         draws_used=True).draws_used[0])
+
+
+def test_packed_batch_and_out_buffers_match_list_api():
+    from paper_2103_13937_b200 import _lib
+
+    rng = np.random.default_rng(9)
+    ciphers = [rng.integers(0, 26, int(L)) for L in rng.integers(2, 400, 30)]
+    table = rng.integers(0, 800, 676)
+    cof = np.repeat(np.arange(30, dtype=np.int32), 4)
+    keys = philox_keys([3], list(range(cof.size)))
+    want = engine.mas_climb(ciphers, cof, keys, table, 3000, group_size=4)
+    out = engine.ClimbResult(scores=np.zeros(cof.size, np.int64), keys=np.zeros((cof.size, 26), np.uint8),
+                             group_best=np.zeros(30, np.int64), draws_used=None, last_accept=None,
+                             tries_done=None, launches=0)
+    got = engine.mas_climb(_lib.Packed.of(ciphers), cof, keys, table, 3000, group_size=4, out=out)
+    assert got is out
+    assert np.array_equal(out.scores, want.scores) and np.array_equal(out.keys, want.keys)
+    assert np.array_equal(out.group_best, want.group_best)
+    with pytest.raises(ValueError):
+        _lib.Packed(np.array([1, 2, 30], np.uint8), np.array([0, 3]))
