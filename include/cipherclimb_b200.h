@@ -233,6 +233,9 @@ typedef struct {
   uint32_t flags;
   int32_t order;              /* n-gram order of `logs` ([26^order]): 0 or 2 = bigram (reference),
                                  3 = trigram, 4 = quadgram (extension) */
+  const int32_t *key_lengths; /* [n_workers] per-worker key length in 2..key_length (a ragged
+                                 batch in one launch), or NULL: every worker uses key_length.
+                                 keys_out keeps the stride key_length. */
 } ccg_sct_climb_args;
 
 /* n-gram extension of the two scoring entry points above: logs float64[26^order], windows of

@@ -48,7 +48,7 @@ class SctClimbArgs(C.Structure):
         ("p1", _i32), ("p2", _i32), ("op1_hop", _i32), ("op2_hop", _i32), ("logs", _P),
         ("scores", _P), ("keys_out", _P), ("draws_used", _P), ("last_accept", _P),
         ("tries_done", _P), ("group_size", _i32), ("group_best", _P), ("text_len", _i64),
-        ("flags", _u32), ("order", _i32),
+        ("flags", _u32), ("order", _i32), ("key_lengths", _P),
     ]
 
 

@@ -980,7 +980,8 @@ static int sct_check(const ccg_sct_climb_args* a) {
 }
 
 static int sct_launch(ccg_ctx* ctx, const ccg_sct_climb_args* a, int64_t n) {
-  if (n < a->key_length) return fail(CCG_ERR_INVALID, "ciphertext shorter than the key");
+  if (n < a->key_length && !a->key_lengths)
+    return fail(CCG_ERR_INVALID, "ciphertext shorter than the key");
   if (n > kSctMaxLen)
     return fail(CCG_ERR_UNSUPPORTED, "ciphertext of %lld letters exceeds the engine limit %lld",
                 (long long)n, (long long)kSctMaxLen);
@@ -1005,6 +1006,7 @@ static int sct_launch(ccg_ctx* ctx, const ccg_sct_climb_args* a, int64_t n) {
   p.op1_hop = a->op1_hop;
   p.op2_hop = a->op2_hop;
   p.order = order;
+  p.key_lengths = a->key_lengths;
   p.logs = a->logs;
   p.scores = a->scores;
   p.keys_out = a->keys_out;
@@ -1049,6 +1051,13 @@ int ccg_sct_climb(ccg_ctx* ctx, const ccg_sct_climb_args* a) {
     if (n < 0) n = L;
     if (L != n)
       return fail(CCG_ERR_INVALID, "all ciphertexts of one sct_climb call must have the same length");
+    if (a->key_lengths) {
+      const int32_t kw = a->key_lengths[i];
+      if (kw < 2) return fail(CCG_ERR_INVALID, "key_length must be at least 2");
+      if (kw > a->key_length)
+        return fail(CCG_ERR_INVALID, "key_lengths[%lld] exceeds key_length", (long long)i);
+      if (kw > L) return fail(CCG_ERR_INVALID, "ciphertext shorter than the key");
+    }
   }
   ccg_sct_climb_args d = *a;
   void* p;
@@ -1073,6 +1082,10 @@ int ccg_sct_climb(ccg_ctx* ctx, const ccg_sct_climb_args* a) {
   d.scores = (double*)p;
   if ((rc = ctx->buf(7, (size_t)nw * k, &p))) return rc;
   d.keys_out = (uint8_t*)p;
+  if (a->key_lengths) {
+    if ((rc = upload(ctx, 12, a->key_lengths, (size_t)nw * 4, &p))) return rc;
+    d.key_lengths = (const int32_t*)p;
+  }
   if (a->draws_used) { if ((rc = ctx->buf(8, (size_t)nw * 8, &p))) return rc; d.draws_used = (uint64_t*)p; }
   if (a->last_accept) { if ((rc = ctx->buf(9, (size_t)nw * 8, &p))) return rc; d.last_accept = (int64_t*)p; }
   if (a->tries_done) { if ((rc = ctx->buf(10, (size_t)nw * 8, &p))) return rc; d.tries_done = (int64_t*)p; }

@@ -100,6 +100,7 @@ struct SctLaunch {
   int64_t climbings;
   int32_t p1, p2, op1_hop, op2_hop;
   int32_t order;  // n-gram order of the log table (2 = the reference's bigrams)
+  const int32_t* key_lengths;  // per-worker key length (<= k), or NULL for k
   const double* logs;
   double* scores;
   uint8_t* keys_out;

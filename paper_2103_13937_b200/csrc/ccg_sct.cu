@@ -134,16 +134,21 @@ struct Evaluator {
   int c0, r0, q32, r32;  // grid position of plaintext position `lane`; 32 = q32*k + r32
   const SumPlan* plan;
 
-  __device__ void init(const SumPlan& P, int k_, int n_, int lane) {
-    plan = &P;
+  // the key length may change per worker (ragged SCT batches)
+  __device__ __forceinline__ void set_k(int k_, int lane) {
     k = k_;
-    n = n_;
     base = n / k;
     rem = n - base * k;
     q32 = 32 / k;
     r32 = 32 - q32 * k;
     r0 = lane / k;
     c0 = lane - r0 * k;
+  }
+
+  __device__ void init(const SumPlan& P, int k_, int n_, int lane) {
+    plan = &P;
+    n = n_;
+    set_k(k_, lane);
 #pragma unroll
     for (int s = 0; s < SLOTS; ++s) {
       const int leaf = 4 * s + (lane >> 3);
@@ -345,11 +350,13 @@ __global__ void __launch_bounds__(kSctWarps * 32, 4)
 
   Evaluator<SLOTS, ORDER> ev;
   ev.init(plan, p.k, p.n, lane);
-  const int k = p.k;
+  const int kmax = p.k;  // keys_out stride
   const int64_t stride = (int64_t)gridDim.x * kSctWarps;
 
   for (int64_t w = (int64_t)blockIdx.x * kSctWarps + warp; w < p.n_workers; w += stride) {
     const int32_t cid = p.cipher_of[w];
+    const int k = p.key_lengths ? p.key_lengths[w] : kmax;
+    if (p.key_lengths) ev.set_k(k, lane);
     stage_text(ws.txt, p.ciphers + p.offsets[cid], p.n, lane);
     Draws d;
     d.key = p.keys + 2 * w;
@@ -382,8 +389,8 @@ __global__ void __launch_bounds__(kSctWarps * 32, 4)
         last = t;
       }
     }
-    if (lane < k) p.keys_out[w * k + lane] = (uint8_t)key.v0;
-    if (lane + 32 < k) p.keys_out[w * k + lane + 32] = (uint8_t)key.v1;
+    if (lane < k) p.keys_out[w * kmax + lane] = (uint8_t)key.v0;
+    if (lane + 32 < k) p.keys_out[w * kmax + lane + 32] = (uint8_t)key.v1;
     if (lane == 0) {
       p.scores[w] = score;
       if (p.draws_used) p.draws_used[w] = d.position();

@@ -190,7 +190,9 @@ def sct_climb(ciphers, cipher_of, keys, logs, key_length, climbings, *, p1=33, p
               tries_done=False, order=2, devices_=None) -> ClimbResult:
     """Run sct_worker (sct.py:148-170) for every worker on the GPU(s).  All ciphertexts
     referenced by one call must share a length (the numpy pairwise-sum plan is per length).
-    logs: float64[26**order] (order 2 = the reference's bigram table)."""
+    logs: float64[26**order] (order 2 = the reference's bigram table).  key_length may be an
+    int or one length per worker (a ragged batch in one launch); keys come back as
+    uint8[n, max key length], row i valid in its first key_length[i] entries."""
     flat, off = _lib.ragged(ciphers)
     cof = np.ascontiguousarray(cipher_of, dtype=np.int32).reshape(-1)
     keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, 2)
@@ -198,7 +200,14 @@ def sct_climb(ciphers, cipher_of, keys, logs, key_length, climbings, *, p1=33, p
     if lg.size != 26**int(order):
         raise ValueError(f"expected {26**int(order)} log-table entries for order {order}")
     n = cof.size
-    k = int(key_length)
+    klens = None
+    if np.ndim(key_length):
+        klens = np.ascontiguousarray(key_length, dtype=np.int32).reshape(-1)
+        if klens.size != n:
+            raise ValueError("one key length per worker required")
+        k = int(klens.max()) if n else 2
+    else:
+        k = int(key_length)
     if keys.shape[0] != n:
         raise ValueError("one Philox key per worker required")
     sk = None if skips is None else np.ascontiguousarray(skips, dtype=np.uint64).reshape(-1)
@@ -230,6 +239,8 @@ def sct_climb(ciphers, cipher_of, keys, logs, key_length, climbings, *, p1=33, p
         a.tries_done = _lib.ptr(out.tries_done)
         a.group_size, a.group_best = int(group_size), _lib.ptr(out.group_best)
         a.order = int(order)
+        kl = None if klens is None else np.ascontiguousarray(klens[lo:hi])
+        a.key_lengths = _lib.ptr(kl)
         ctx = _lib.context(dev)
         with ctx.lock:
             before = ctx.launches()

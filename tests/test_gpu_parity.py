@@ -654,3 +654,26 @@ def test_packed_batch_and_out_buffers_match_list_api():
     assert np.array_equal(out.group_best, want.group_best)
     with pytest.raises(ValueError):
         _lib.Packed(np.array([1, 2, 30], np.uint8), np.array([0, 3]))
+
+
+@pytest.mark.parametrize("order", [2, 3])
+def test_sct_ragged_key_lengths_one_launch(order):
+    rng = np.random.default_rng(60 + order)
+    logs = -rng.random(26**order) * 20 - 1
+    ciphers = [rng.integers(0, 26, 400) for _ in range(12)]
+    ks = [5, 6, 7, 9, 10, 12, 15, 17, 20, 33, 40, 64]
+    cof = np.repeat(np.arange(12, dtype=np.int32), 3)
+    klens = np.repeat(np.array(ks, dtype=np.int32), 3)
+    streams = list(range(cof.size))
+    keys = philox_keys([77], streams)
+    res = engine.sct_climb(ciphers, cof, keys, logs, klens, 600, order=order, group_size=3,
+                           draws_used=True)
+    for i in range(cof.size):
+        c, k = int(cof[i]), int(klens[i])
+        key, score, _ = O.sct_worker(ciphers[c], logs, k, 600, 77, streams[i], order=order)
+        assert float(res.scores[i]) == score, (i, k)
+        assert np.array_equal(res.keys[i, :k].astype(np.int64), key)
+    one = engine.sct_climb([ciphers[3]], np.zeros(3, np.int32), keys[9:12], logs, 9, 600, order=order,
+                           draws_used=True)
+    assert np.array_equal(one.scores, res.scores[9:12])
+    assert np.array_equal(one.draws_used, res.draws_used[9:12])
