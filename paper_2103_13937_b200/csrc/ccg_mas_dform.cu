@@ -87,21 +87,23 @@ __device__ __forceinline__ void rebuild_D(const BT& B, WT& W, int lane) {
 }
 
 // D[a][b] from T, N and ks; tdg / ndg hold T[lane][lane] / N[lane][lane] (all lanes call)
-template <class BT, class WT>
-__device__ __forceinline__ int delta_at(const BT& B, const WT& W, int tdg, int ndg, int a, int b) {
+template <class WT>
+__device__ __forceinline__ int delta_at(uint32_t ks_s, const WT& W, int tdg, int ndg, int a, int b) {
   const int ta = __shfl_sync(kFull, tdg, a), tb = __shfl_sync(kFull, tdg, b);
   const int na = __shfl_sync(kFull, ndg, a), nb = __shfl_sync(kFull, ndg, b);
   const int kt = ta + tb - t_at(W, a, b) - t_at(W, b, a);
-  return kt * B.KS[a * kDS + b] - na - nb + W.N[a * kNS + b] + W.N[b * kNS + a];
+  // ks through a 32-bit shared address (a generic B.KS access recomputes the window base)
+  const int ks = (int)lds_u32(ks_s + 4u * (uint32_t)(a * kDS + b));
+  return kt * ks - na - nb + W.N[a * kNS + b] + W.N[b * kNS + a];
 }
 
 // max over the 325 on-demand deltas; lane y scans column y
-template <class BT, class WT>
-__device__ __forceinline__ int max_delta(const BT& B, const WT& W, int tdg, int ndg, int lane) {
+template <class WT>
+__device__ __forceinline__ int max_delta(uint32_t ks_s, const WT& W, int tdg, int ndg, int lane) {
   int m = (int)0x80000000;
   const int y = lane < kAlpha ? lane : 0;
   for (int x = 0; x < kAlpha; ++x) {
-    const int dv = delta_at(B, W, tdg, ndg, x, y);
+    const int dv = delta_at(ks_s, W, tdg, ndg, x, y);
     if (lane < kAlpha && x != lane) m = max(m, dv);
   }
   return __reduce_max_sync(kFull, m);
@@ -139,6 +141,7 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
   const int64_t stride = (int64_t)gridDim.x * kDWarps;
   const uint32_t climbings = (uint32_t)p.climbings;
   const int y = lane < kAlpha ? lane : 0;  // the column this lane owns in N updates
+  const uint32_t ks_s = smem_addr(B.KS);
 
   for (int64_t w = (int64_t)blockIdx.x * kDWarps + warp; w < p.n_workers; w += stride) {
     const int32_t cid = p.cipher_of[w];
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
       }
     };
     auto optimum = [&]() {
-      return TABLE ? max_D(W, lane) <= 0 : max_delta(B, W, tdg, ndg, lane) <= 0;
+      return TABLE ? max_D(W, lane) <= 0 : max_delta(ks_s, W, tdg, ndg, lane) <= 0;
     };
 
     int last = -1, nacc = 0;
@@ -287,7 +290,7 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
       if (TABLE) {
         d = j < R ? W.D[pa * kDS + pb] : 0;
       } else {
-        d = delta_at(B, W, tdg, ndg, pa, pb);
+        d = delta_at(ks_s, W, tdg, ndg, pa, pb);
         d = j < R ? d : 0;
       }
       const uint32_t acc = __ballot_sync(kFull, d > 0);
@@ -297,7 +300,7 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
         if (seq && t < climbings) {  // one try through the sequential redraw path
           int a2, b2;
           win.pair(lane, a2, b2);
-          const int d2 = TABLE ? W.D[a2 * kDS + b2] : delta_at(B, W, tdg, ndg, a2, b2);
+          const int d2 = TABLE ? W.D[a2 * kDS + b2] : delta_at(ks_s, W, tdg, ndg, a2, b2);
           if (d2 > 0) {
             accept(a2, b2, d2);
             last = (int)t;

@@ -677,3 +677,18 @@ def test_sct_ragged_key_lengths_one_launch(order):
                            draws_used=True)
     assert np.array_equal(one.scores, res.scores[9:12])
     assert np.array_equal(one.draws_used, res.draws_used[9:12])
+
+
+@pytest.mark.parametrize("L,tmax", [(5000, 32_767), (40_000, 700), (3000, 100_000)])
+def test_mas_kernel_gates_fall_back_exactly(L, tmax):
+    """Inputs past the D-form gate ((n-1) max S >= 2^27), the T-form gate (n > 32768) and the
+    16-bit table gate (max S > 65535) take the next kernel; results equal the oracle."""
+    rng = np.random.default_rng(L)
+    c = rng.integers(0, 26, L)
+    table = rng.integers(0, tmax + 1, 676)
+    table[7] = tmax
+    keys = philox_keys([1], [0, 1])
+    res = engine.mas_climb([c], np.zeros(2, np.int32), keys, table, 1200, draws_used=True)
+    want_s, want_m = O.mas_workers([c], np.zeros(2, np.int32), [1, 1], [0, 1], table, 1200)
+    assert res.scores.tolist() == want_s.tolist()
+    assert np.array_equal(res.keys.astype(np.int64), want_m)
