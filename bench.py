@@ -120,7 +120,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200", "-i", str(self.device)],
+                 "-lms", "50", "-i", str(self.device)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -203,14 +203,17 @@ def cpu_sample(ciphers, scores, workers, climbings, seconds, rank=0):
         seeds = [7000 + rank * len(ciphers) + i for i in range(m) for _ in range(workers)]
         streams = [w for _ in range(m) for w in range(workers)]
         t0 = time.perf_counter()
-        O.mas_workers(ciphers[:m], cof, seeds, streams, scores, climbings, threads=threads)
+        sc, maps = O.mas_workers(ciphers[:m], cof, seeds, streams, scores, climbings,
+                                 threads=threads)
         dt = time.perf_counter() - t0
         if dt >= seconds or m >= len(ciphers):
             evals = n * climbings
+            best = [int(np.argmax(sc[i * workers:(i + 1) * workers])) for i in range(m)]
             return {"value": evals / dt, "unit": "evals/s", "cores": threads, "kind": "port",
                     "sample": f"{m} ciphertexts x {workers} workers x {climbings} climbings "
                               f"({evals:.3g} evals, {dt:.1f} s) of the bench workload, "
-                              "C oracle (oracle/cc_oracle.c), one pthread per core"}
+                              "C oracle (oracle/cc_oracle.c), one pthread per core",
+                    "best_maps": [maps[i * workers + b] for i, b in enumerate(best)]}
         m = min(len(ciphers), max(m + 1, int(m * max(2.0, 1.3 * seconds / max(dt, 1e-3)))))
 
 
@@ -226,6 +229,13 @@ def run_reference(args):
         if s >= args.warmup:
             samples.append(r)
     value = float(np.mean([r["value"] for r in samples]))
+    # success rate vs length over the reference arm's own sample (same seeds as our arm)
+    maps = samples[-1].pop("best_maps")
+    for r in samples[:-1]:
+        r.pop("best_maps", None)
+    m = len(maps)
+    rec = np.array([np.array_equal(maps[i][ciphers[i]], plains[i]) for i in range(m)])
+    bins = (lengths[:m] // 50) * 50
     line = {
         "impl": "reference", "metric": "key-candidate fitness evals/sec", "value": value,
         "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -235,6 +245,9 @@ def run_reference(args):
         "cpu_baseline": {**samples[-1], "value": value},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "success_by_len": {f"{b}-{b + 49}": round(float(rec[bins == b].mean()), 4)
+                           for b in sorted(set(bins.tolist()))},
+        "success_sample": f"first {m} ciphertexts of the workload",
     }
     print(json.dumps(line), flush=True)
 
@@ -416,6 +429,12 @@ def main():
     cpu = None
     if rank == 0 and not args.no_cpu:
         cpu = cpu_sample(ciphers, scores, W, K, args.cpu_seconds)
+        cpu_maps = cpu.pop("best_maps")
+        # the same per-ciphertext outcome as the CPU port on its whole sample (bit-exact parity)
+        if e2e is not None:
+            cpu["agrees_with_gpu"] = all(
+                np.array_equal(res.keys[i * W + int(res.group_best[i])].astype(np.int64)[ciphers[i]],
+                               cpu_maps[i][ciphers[i]]) for i in range(len(cpu_maps)))
 
     if rank == 0:
         line = {
