@@ -30,7 +30,7 @@
 namespace ccg {
 namespace {
 
-constexpr int kNgWarps = 8;
+
 
 __host__ __device__ constexpr int pow26(int g) { return g == 0 ? 1 : 26 * pow26(g - 1); }
 
@@ -116,7 +116,7 @@ struct NgState {
   }
 };
 
-template <int G, bool SMEM_TAB>
+template <int G, bool SMEM_TAB, int kNgWarps>
 __global__ void __launch_bounds__(kNgWarps * 32) mas_ngram_kernel(const MasNgramLaunch p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -328,9 +328,9 @@ __global__ void __launch_bounds__(kNgWarps * 32) mas_ngram_kernel(const MasNgram
   }
 }
 
-template <int G, bool SMEM_TAB>
-cudaError_t launch_ng(cudaStream_t s, const MasNgramLaunch& p, int sm_count) {
-  auto kern = mas_ngram_kernel<G, SMEM_TAB>;
+template <int G, bool SMEM_TAB, int kNgWarps>
+cudaError_t launch_ng_w(cudaStream_t s, const MasNgramLaunch& p, int sm_count) {
+  auto kern = mas_ngram_kernel<G, SMEM_TAB, kNgWarps>;
   const size_t tab = SMEM_TAB ? (((size_t)pow26(G) * 2 + 15) & ~(size_t)15) : 0;
   const size_t bytes = tab + (size_t)kNgWarps * ng_warp_bytes((int)p.max_len);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -344,6 +344,16 @@ cudaError_t launch_ng(cudaStream_t s, const MasNgramLaunch& p, int sm_count) {
   const int grid = (int)(need < resident ? need : resident);
   kern<<<grid, kNgWarps * 32, bytes, s>>>(p);
   return cudaGetLastError();
+}
+
+// 16 warps per block when the shared-memory layout fits (more latency hiding for the
+// table lookups), else 8.
+template <int G, bool SMEM_TAB>
+cudaError_t launch_ng(cudaStream_t s, const MasNgramLaunch& p, int sm_count) {
+  const size_t tab = SMEM_TAB ? (((size_t)pow26(G) * 2 + 15) & ~(size_t)15) : 0;
+  if (tab + 16 * (size_t)ng_warp_bytes((int)p.max_len) <= 200 * 1024)
+    return launch_ng_w<G, SMEM_TAB, 16>(s, p, sm_count);
+  return launch_ng_w<G, SMEM_TAB, 8>(s, p, sm_count);
 }
 
 // ngrams.py:134-140 generalised to order G: one warp per text, int64 sum.
@@ -369,7 +379,7 @@ __global__ void ngram_score_kernel(const uint8_t* __restrict__ texts, const int6
 
 size_t mas_ngram_smem_bytes(int order, int64_t max_len) {
   const size_t tab = order <= 3 ? (((size_t)pow26(order) * 2 + 15) & ~(size_t)15) : 0;
-  return tab + (size_t)kNgWarps * ng_warp_bytes((int)max_len);
+  return tab + (size_t)8 * ng_warp_bytes((int)max_len);
 }
 
 cudaError_t launch_mas_ngram_climb(cudaStream_t s, const MasNgramLaunch& p, int sm_count) {
