@@ -325,3 +325,52 @@ def ngram_log_score_text_batch(texts, table) -> np.ndarray:
 
 def ngram_log_score_text(text: MappedText, table) -> float:
     return float(ngram_log_score_text_batch([text], table)[0])
+
+
+def parse_ngram_file(lines, order: int) -> NgramTable:
+    """`<ngram> <integer>` per line (parse_bigram_file, ngrams.py:76-108, generalised to
+    windows of `order` letters): blank lines skipped, missing n-grams are 0, a repeated
+    n-gram keeps its last value with a warning."""
+    order = _check_order(order)
+    if isinstance(lines, str):
+        lines = lines.splitlines()
+    scores = np.zeros(ALPHABET_SIZE**order, dtype=np.int64)
+    seen = set()
+    for lineno, line in enumerate(lines, start=1):
+        fields = line.split()
+        if not fields:
+            continue
+        if len(fields) != 2:
+            raise ValueError(f"line {lineno}: expected '<ngram> <score>', got {line!r}")
+        gram, value_text = fields
+        if len(gram) != order or any(not ("a" <= ch <= "z") for ch in gram):
+            raise ValueError(f"line {lineno}: bad {order}-gram {gram!r}")
+        try:
+            value = int(value_text)
+        except ValueError:
+            raise ValueError(f"line {lineno}: bad score {value_text!r}") from None
+        if value < 0:
+            raise ValueError(f"line {lineno}: negative score {value}")
+        idx = ngram_index(ord(ch) - 97 for ch in gram)
+        if idx in seen:
+            warnings.warn(f"duplicate {order}-gram {gram!r}; keeping the later value")
+        seen.add(idx)
+        scores[idx] = value
+    return NgramTable(order, scores)
+
+
+def format_ngram_file(table, nonzero_only: bool = False) -> str:
+    """All 26**order records in lexicographic order (format_bigram_file generalised; at
+    order 2 the output is identical).  nonzero_only drops zero entries, which
+    parse_ngram_file restores as 0."""
+    t = as_ngram_table(table)
+    out = []
+    for i, v in enumerate(t.scores):
+        if nonzero_only and not v:
+            continue
+        letters, x = [], i
+        for _ in range(t.order):
+            letters.append(chr(97 + x % ALPHABET_SIZE))
+            x //= ALPHABET_SIZE
+        out.append(f"{''.join(reversed(letters))} {int(v)}")
+    return "\n".join(out) + "\n"

@@ -196,3 +196,24 @@ def test_bench_workload_keys_match_oracle():
     for s in (100000, 100001, 100777):
         assert np.array_equal(bench.reference_permutation(s, bench.KEYGEN_STREAM, 26),
                               O.permutation(s, bench.KEYGEN_STREAM, 26))
+
+
+def test_ngram_file_formats_round_trip(golden):
+    import paper_2103_13937_b200 as cc
+
+    eng = cc.BigramTable(golden.english_scores())
+    # order 2 is byte-identical to the reference's bigram format
+    assert cc.format_ngram_file(eng) == cc.format_bigram_file(eng)
+    assert np.array_equal(cc.parse_ngram_file(cc.format_bigram_file(eng), 2).scores, eng.scores)
+    corpus = "".join(chr(97 + int(x)) for x in golden.corpus())
+    for order in (3, 4):
+        t = cc.build_ngram_table_from_corpus(corpus, order)
+        txt = cc.format_ngram_file(t, nonzero_only=True)
+        assert np.array_equal(cc.parse_ngram_file(txt, order).scores, t.scores)
+        assert t.scores.sum() == len(corpus) - order + 1
+    with pytest.raises(ValueError):
+        cc.parse_ngram_file("abc 1\nab 2\n", 3)
+    with pytest.raises(ValueError):
+        cc.parse_ngram_file("abc -1\n", 3)
+    with pytest.warns(UserWarning):
+        cc.parse_ngram_file("abc 1\nabc 2\n", 3)
