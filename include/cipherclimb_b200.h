@@ -24,6 +24,8 @@
  *   ccg_sct_score_batch                          sct.py:158-160 candidate_score (ciphers.py:71-86,107-113)
  *   ccg_ngram_log_score_batch                    ngrams.py:166-172 generalised to order-n windows
  *   ccg_sct_score_ngram_batch                    sct.py:158-160 with an order-n log table
+ *   ccg_encrypt_batch                            ciphers.py:46-49,89-104 mas_encrypt / sct_encrypt with keys
+ *                                                rng.py:91-97 permutation(k) on KEYGEN streams (test sets)
  *   ccg_sct_climb[_dev]                          sct.py:173-176 _sct_task -> sct.py:148-170 sct_worker,
  *                                                for a whole batch (sct.py:194-200) + max_element
  *
@@ -249,6 +251,16 @@ int ccg_sct_score_ngram_batch(ccg_ctx *ctx, const uint8_t *ciphers, const int64_
 
 int ccg_sct_climb(ccg_ctx *ctx, const ccg_sct_climb_args *args);
 int ccg_sct_climb_dev(ccg_ctx *ctx, const ccg_sct_climb_args *args);
+
+/* Device-side test-set generation for a ragged batch of plaintexts:
+ * kind 0 = MAS (ciphers.py:46-49 mas_encrypt), 1 = SCT (ciphers.py:89-104 sct_encrypt,
+ * irregular grid).  With keygen (2 * n_texts Philox keys of WorkerRng(seed_i, KEYGEN_STREAM))
+ * the key of text i is drawn on the device as permutation(k_i) (rng.py:91-97) and written to
+ * keys[i * kmax ...]; with keygen NULL the keys are read from `keys`.  k_i = 26 for MAS,
+ * key_lengths[i] in 1..min(kmax, 64) for SCT.  out receives the ciphertexts (same offsets). */
+int ccg_encrypt_batch(ccg_ctx *ctx, int32_t kind, const uint8_t *texts, const int64_t *offsets,
+                      int64_t n_texts, const uint64_t *keygen, const int32_t *key_lengths,
+                      int32_t kmax, uint8_t *keys, uint8_t *out);
 
 /* Roofline denominator: measured shared-memory (LDS) bandwidth of this device, bytes/s. */
 int ccg_bench_smem_bandwidth(ccg_ctx *ctx, double *out_bytes_per_s);

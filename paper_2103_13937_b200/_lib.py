@@ -108,6 +108,7 @@ EXPORTS = {
     "ccg_sct_score_ngram_batch": (C.c_int, [_P, _P, _P, _i64, _P, _P, _i32, _i64, _i32, _P, _P]),
     "ccg_sct_climb": (C.c_int, [_P, C.POINTER(SctClimbArgs)]),
     "ccg_sct_climb_dev": (C.c_int, [_P, C.POINTER(SctClimbArgs)]),
+    "ccg_encrypt_batch": (C.c_int, [_P, _i32, _P, _P, _i64, _P, _P, _i32, _P, _P]),
     "ccg_bench_smem_bandwidth": (C.c_int, [_P, _P]),
 }
 

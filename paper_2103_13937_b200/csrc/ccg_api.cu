@@ -1102,6 +1102,55 @@ int ccg_sct_climb(ccg_ctx* ctx, const ccg_sct_climb_args* a) {
   return finish(ctx, cudaSuccess, "sct_climb");
 }
 
+// ------------------------------------------------------------------ test-set generation
+int ccg_encrypt_batch(ccg_ctx* ctx, int32_t kind, const uint8_t* texts, const int64_t* offsets,
+                      int64_t n_texts, const uint64_t* keygen, const int32_t* key_lengths,
+                      int32_t kmax, uint8_t* keys, uint8_t* out) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (kind != 0 && kind != 1) return fail(CCG_ERR_INVALID, "kind must be 0 (MAS) or 1 (SCT)");
+  if ((rc = check_ragged(texts, offsets, n_texts, "encrypt", nullptr))) return rc;
+  if (n_texts == 0) return CCG_OK;
+  if (!keys || !out) return fail(CCG_ERR_INVALID, "null keys / out");
+  if (kind == 0 && kmax < kAlpha) return fail(CCG_ERR_INVALID, "kmax must be >= 26 for MAS");
+  if (kind == 1 && !key_lengths) return fail(CCG_ERR_INVALID, "key_lengths required for SCT");
+  for (int64_t i = 0; i < n_texts; ++i) {
+    const int k = kind == 0 ? kAlpha : key_lengths[i];
+    if (k < 1 || k > kmax || k > kSctMaxKey)
+      return fail(CCG_ERR_INVALID, "key length %d of text %lld out of range", k, (long long)i);
+    if (!keygen) {
+      uint64_t seen = 0;
+      for (int q = 0; q < k; ++q) {
+        const int v = keys[i * kmax + q];
+        if (v >= k || (seen >> v) & 1)
+          return fail(CCG_ERR_INVALID, kind == 0 ? "substitution key must be a permutation of 0..25"
+                                                 : "transposition key must be a permutation of 0..k-1");
+        seen |= 1ULL << v;
+      }
+    }
+  }
+  const size_t total = (size_t)offsets[n_texts];
+  void *dt, *doff, *dkg = nullptr, *dkl = nullptr, *dkeys, *dout;
+  if ((rc = upload(ctx, 0, texts, total, &dt))) return rc;
+  if ((rc = upload(ctx, 1, offsets, (size_t)(n_texts + 1) * 8, &doff))) return rc;
+  if (keygen && (rc = upload(ctx, 2, keygen, (size_t)n_texts * 16, &dkg))) return rc;
+  if (key_lengths && (rc = upload(ctx, 3, key_lengths, (size_t)n_texts * 4, &dkl))) return rc;
+  if (keygen) {
+    if ((rc = ctx->buf(4, (size_t)n_texts * kmax, &dkeys))) return rc;
+  } else if ((rc = upload(ctx, 4, keys, (size_t)n_texts * kmax, &dkeys))) {
+    return rc;
+  }
+  if ((rc = ctx->buf(5, total ? total : 1, &dout))) return rc;
+  ctx->launches++;
+  cudaError_t e = launch_encrypt(ctx->stream, kind, (const uint8_t*)dt, (const int64_t*)doff,
+                                 n_texts, (const uint64_t*)dkg, (const int32_t*)dkl,
+                                 (uint8_t*)dkeys, kmax, (uint8_t*)dout);
+  if (e != cudaSuccess) return cuda_fail(e, "encrypt kernel");
+  if (keygen && (rc = download(ctx, keys, dkeys, (size_t)n_texts * kmax))) return rc;
+  if ((rc = download(ctx, out, dout, total))) return rc;
+  return finish(ctx, cudaSuccess, "encrypt");
+}
+
 int ccg_bench_smem_bandwidth(ccg_ctx* ctx, double* out_bytes_per_s) {
   int rc = enter(ctx);
   if (rc) return rc;

@@ -155,6 +155,10 @@ cudaError_t launch_sct_score_long(cudaStream_t s, const uint8_t* ciphers, const 
 cudaError_t launch_sct_climb(cudaStream_t s, const SctLaunch& p, const SumPlan& plan,
                              int sm_count);
 
+cudaError_t launch_encrypt(cudaStream_t s, int kind, const uint8_t* texts, const int64_t* offsets,
+                           int64_t n, const uint64_t* keygen, const int32_t* key_lengths,
+                           uint8_t* keys, int kmax, uint8_t* out);
+
 cudaError_t bench_smem_bandwidth(cudaStream_t s, int sm_count, double* bytes_per_s);
 
 }  // namespace ccg

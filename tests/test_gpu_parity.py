@@ -692,3 +692,31 @@ def test_mas_kernel_gates_fall_back_exactly(L, tmax):
     want_s, want_m = O.mas_workers([c], np.zeros(2, np.int32), [1, 1], [0, 1], table, 1200)
     assert res.scores.tolist() == want_s.tolist()
     assert np.array_equal(res.keys.astype(np.int64), want_m)
+
+
+# ------------------------------------------------------------------ device-side test sets
+def test_encrypt_batch_reference_recipe(golden):
+    """WorkerRng(seed, KEYGEN).permutation(k) keys and mas/sct encryption on the GPU equal
+    the host functions (pinned to the reference) for a ragged batch."""
+    corpus = golden.corpus()
+    rng = np.random.default_rng(5)
+    lengths = [0, 1, 3, 26, 100, 400, 501] + [int(v) for v in rng.integers(2, 600, 25)]
+    plains = [corpus[o:o + L] for o, L in zip(rng.integers(0, corpus.size - 700, len(lengths)), lengths)]
+    seeds = [100000 + i for i in range(len(plains))]
+    c_mas, k_mas = cc.encrypt_batch(plains, "mas", key_seeds=seeds)
+    for p, s, c, k in zip(plains, seeds, c_mas, k_mas):
+        want_k = O.permutation(s, 2**32 - 2, 26)
+        assert np.array_equal(k, want_k)
+        assert np.array_equal(c, cc.mas_encrypt(p, want_k))
+    klens = [int(v) for v in rng.integers(1, 65, len(plains))]
+    c_sct, k_sct = cc.encrypt_batch(plains, "sct", key_seeds=seeds, key_lengths=klens)
+    for p, s, kl, c, k in zip(plains, seeds, klens, c_sct, k_sct):
+        want_k = O.permutation(s, 2**32 - 2, kl)
+        assert np.array_equal(k, want_k)
+        assert np.array_equal(c, cc.sct_encrypt(p, want_k))
+    # explicit keys
+    keys = [rng.permutation(26) for _ in plains]
+    c2, _ = cc.encrypt_batch(plains, "mas", keys=keys)
+    assert all(np.array_equal(c, cc.mas_encrypt(p, k)) for p, c, k in zip(plains, c2, keys))
+    with pytest.raises(ValueError):
+        cc.encrypt_batch(plains[:1], "mas", keys=[np.zeros(26, int)])
