@@ -177,7 +177,8 @@ def barrier_max(value: float, world: int, device: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([value], dtype=torch.float64, device=f"cuda:{device}")
+    on_gpu = dist.get_backend() == "nccl"
+    t = torch.tensor([value], dtype=torch.float64, device=f"cuda:{device}" if on_gpu else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -278,6 +279,10 @@ def main():
     from paper_2103_13937_b200 import _lib, engine
 
     device = local if world > 1 else 0
+    # CCG_BENCH_SHARE_GPU=1 (testing only, with CCG_BENCH_BACKEND=gloo): ranks share the
+    # visible GPUs round-robin, so the multi-rank path can be exercised on a 1-GPU box
+    if os.environ.get("CCG_BENCH_SHARE_GPU") == "1":
+        device = local % torch.cuda.device_count()
     torch.cuda.set_device(device)
     engine.set_devices([device])
     ctx = _lib.context(device)
