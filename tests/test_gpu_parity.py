@@ -720,3 +720,67 @@ def test_encrypt_batch_reference_recipe(golden):
     assert all(np.array_equal(c, cc.mas_encrypt(p, k)) for p, c, k in zip(plains, c2, keys))
     with pytest.raises(ValueError):
         cc.encrypt_batch(plains[:1], "mas", keys=[np.zeros(26, int)])
+
+
+# ------------------------------------------------------------------ randomized parity sweeps
+def test_fuzz_mas_kernels_vs_oracle():
+    """3,000 random workers: lengths 2..3000, alphabets of 2..26 letters, tables of many
+    magnitudes (including the D-form / T-form gate edges), random budgets and stream skips."""
+    rng = np.random.default_rng(2024)
+    for trial in range(16):
+        tmax = int(rng.choice([1, 5, 700, 32_767, 65_535, 2**20]))
+        table = rng.integers(0, tmax + 1, 676)
+        ciphers = []
+        for _ in range(60):
+            L = int(rng.choice([2, 3, 10, 100, 500, 1500, 3000]))
+            ciphers.append(rng.integers(0, int(rng.integers(2, 27)), L))
+        n = 500
+        cof = rng.integers(0, len(ciphers), n).astype(np.int32)
+        seeds = rng.integers(0, 2**63, n).tolist()
+        streams = rng.integers(0, 2**48, n).tolist()
+        keys = philox_keys(seeds, streams)
+        climb = int(rng.choice([1, 33, 1000, 3000]))
+        res = engine.mas_climb(ciphers, cof, keys, table, climb, last_accept=True)
+        want_s, want_m = O.mas_workers(ciphers, cof, seeds, streams, table, climb)
+        assert res.scores.tolist() == want_s.tolist(), (trial, tmax, climb)
+        assert np.array_equal(res.keys.astype(np.int64), want_m), (trial, tmax, climb)
+
+
+@pytest.mark.parametrize("order", [3, 4])
+def test_fuzz_ngram_vs_oracle(order):
+    rng = np.random.default_rng(300 + order)
+    for trial in range(6):
+        table = rng.integers(0, int(rng.choice([2, 300, 65_536])), 26**order)
+        ciphers = [rng.integers(0, int(rng.integers(2, 27)), int(rng.choice([2, 5, 40, 90, 300, 1000])))
+                   for _ in range(40)]
+        n = 300
+        cof = rng.integers(0, len(ciphers), n).astype(np.int32)
+        seeds = rng.integers(0, 2**63, n).tolist()
+        streams = rng.integers(0, 2**48, n).tolist()
+        keys = philox_keys(seeds, streams)
+        res = engine.mas_climb(ciphers, cof, keys, table, 800, order=order)
+        want_s, _ = O.ngram_workers(ciphers, cof, seeds, streams, order, table, 800)
+        assert res.scores.tolist() == want_s.tolist(), trial
+
+
+def test_fuzz_sct_vs_oracle():
+    rng = np.random.default_rng(77)
+    for trial in range(10):
+        n = int(rng.choice([8, 129, 400, 1000]))
+        logs = -rng.random(676) * 20 - 1
+        ciphers = [rng.integers(0, 26, n) for _ in range(4)]
+        m = 64
+        cof = rng.integers(0, 4, m).astype(np.int32)
+        klens = rng.integers(2, min(n, 64) + 1, m).astype(np.int32)
+        seeds = rng.integers(0, 2**63, m).tolist()
+        streams = rng.integers(0, 2**48, m).tolist()
+        keys = philox_keys(seeds, streams)
+        p1, p2 = sorted(int(v) for v in rng.integers(0, 101, 2))
+        res = engine.sct_climb(ciphers, cof, keys, logs, klens, 300, p1=p1, p2=p2, op1_hop=2,
+                               op2_hop=4)
+        for i in range(m):
+            k = int(klens[i])
+            key, score, _ = O.sct_worker(ciphers[cof[i]], logs, k, 300, seeds[i], streams[i],
+                                         p1=p1, p2=p2, op1_hop=2, op2_hop=4)
+            assert float(res.scores[i]) == score, (trial, i)
+            assert np.array_equal(res.keys[i, :k].astype(np.int64), key)
