@@ -87,20 +87,26 @@ def full(tag: str, tries: float) -> str:
     if "smsp__inst_executed.sum" in h:
         inst = float(v[h.index("smsp__inst_executed.sum")].replace(",", ""))
         out += ["", f"derived: warp instructions per try = {inst / tries:.2f}"]
-    # hottest SASS by execution count (source page)
+    # hottest SASS by warp-stall samples (source page; one section per function)
     try:
         src = ncu_csv(rep, "source", ["--print-source", "sass"])
-        hh = src[1]
-        ie, isrc = hh.index("Instructions Executed"), hh.index("Source")
-        iss = hh.index("Warp Stall Sampling (All Samples)")
-        body = [r for r in src[2:] if len(r) > ie and (r[ie] or "0") != "0"]
-        tot_samples = sum(int(r[iss] or 0) for r in body) or 1
-        body.sort(key=lambda r: -int(r[iss] or 0))
+        rows, hh = [], None
+        for r in src:
+            if r and r[0] == "Kernel Name":
+                hh = None
+            elif r and r[0] == "Address":
+                hh = r
+            elif hh:
+                rows.append(dict(zip(hh, r)))
+        body = [r for r in rows if int(r.get("Instructions Executed") or 0)]
+        tot_samples = sum(int(r.get("Warp Stall Sampling (All Samples)") or 0) for r in body) or 1
+        body.sort(key=lambda r: -int(r.get("Warp Stall Sampling (All Samples)") or 0))
         out += ["", "top 25 SASS instructions by warp-stall samples "
-                "(execs per try, share of samples, instruction):"]
+                "(execs per unit, share of samples, instruction):"]
         for r in body[:25]:
-            out.append(f"  {int(r[ie]) / tries:8.4f} {100 * int(r[iss] or 0) / tot_samples:6.2f}%  "
-                       f"{r[isrc].strip()[:80]}")
+            out.append(f"  {int(r['Instructions Executed']) / tries:8.4f} "
+                       f"{100 * int(r.get('Warp Stall Sampling (All Samples)') or 0) / tot_samples:6.2f}%  "
+                       f"{r['Source'].strip()[:80]}")
     except Exception as e:  # noqa: BLE001
         out.append(f"(source page unavailable: {e})")
     return "\n".join(out) + "\n"
@@ -109,16 +115,17 @@ def full(tag: str, tries: float) -> str:
 def main():
     tag = sys.argv[1]
     tries = float(sys.argv[2]) if len(sys.argv) > 2 else 2000 * 64 * 10_000
+    name = sys.argv[3] if len(sys.argv) > 3 else tag
     PROF.mkdir(exist_ok=True)
     b = OUT / f"bench_{tag}.json"
     if b.exists() and b.stat().st_size:
         line = json.loads(b.read_text().strip().splitlines()[-1])
-        (PROF / f"{tag}_bench.json").write_text(json.dumps(line, indent=1) + "\n")
+        (PROF / f"{name}_bench.json").write_text(json.dumps(line, indent=1) + "\n")
     if (OUT / f"launches_{tag}.csv").exists():
-        (PROF / f"{tag}_launches.txt").write_text(launches(tag))
+        (PROF / f"{name}_launches.txt").write_text(launches(tag))
     if (OUT / f"prof_{tag}.ncu-rep").exists():
-        (PROF / f"{tag}_ncu.txt").write_text(full(tag, tries))
-    print("wrote", sorted(p.name for p in PROF.glob(f"{tag}_*")))
+        (PROF / f"{name}_ncu.txt").write_text(full(tag, tries))
+    print("wrote", sorted(p.name for p in PROF.glob(f"{name}_*")))
 
 
 if __name__ == "__main__":
