@@ -276,7 +276,8 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
           const uint32_t eqB = __ballot_sync(kFull, c1 == c2) & ~((2u << r0) - 1u);
           R = eqB ? (uint32_t)(__ffs(eqB) - 1) : 32u;
           R = min(R, nB);
-          seq = R < 32u && R < nB;
+          // a second redraw ends the round; the next round starts at that pair, which it
+          // handles as its first-segment redraw (no sequential try needed)
         }
       }
       if (R > climbings - t) {
