@@ -41,8 +41,9 @@ DFORM_BYTES_PER_TRY = 16         # exact delta of the proposal: T[a][b], T[b][a]
                                  # N[a][b], N[b][a], ks[a][b] (4 B each)
 DFORM_BYTES_PER_ACCEPT = 6812    # N update 5408 + T row/column swap 416 + u,v 208 + S factors
                                  # 416 + saved rows 208 + diagonal refresh 156
-DFORM_BYTES_PER_WORKER = 12324   # N from scratch 8112 + score 4056 + diagonals 156 (+8 B per
-                                 # ciphertext bigram for the count matrix)
+DFORM_BYTES_PER_CIPHER = 12168   # once per ciphertext (dform_init_kernel): N from scratch 8112
+                                 # + score 4056 (+8 B per bigram for the count matrix)
+DFORM_BYTES_PER_WORKER = 5356    # each worker copies the ciphertext's T, N (5200) + diagonals 156
 REF_LOOKUP_BYTES_PER_EVAL = 208 * 4    # reference-equivalent: 208 table lookups
 
 
@@ -364,7 +365,8 @@ def main():
     ctx.d2h(acc, d_acc)
     ctx.synchronize()
     n_accepts = int(acc.sum())
-    worker_bytes = sum(W * (DFORM_BYTES_PER_WORKER + 8 * (int(L) - 1)) for L in lengths)
+    worker_bytes = sum(W * DFORM_BYTES_PER_WORKER + DFORM_BYTES_PER_CIPHER + 8 * (int(L) - 1)
+                       for L in lengths)
     launch_bytes = (DFORM_BYTES_PER_TRY * evals_per_step + DFORM_BYTES_PER_ACCEPT * n_accepts
                     + worker_bytes)
     bytes_per_eval = launch_bytes / evals_per_step

@@ -537,8 +537,20 @@ static int mas_launch(ccg_ctx* ctx, const ccg_mas_climb_args* a, int64_t max_len
   cudaError_t e;
   const uint32_t kern = a->flags & CCG_FLAG_KERNEL_MASK;
   const bool dform = kern == 0 || kern == CCG_FLAG_KERNEL_DFORM || kern == CCG_FLAG_KERNEL_DTABLE;
-  if (dform && mas_dform_ok(max_len, tmax))
+  p.init = nullptr;
+  if (dform && mas_dform_ok(max_len, tmax)) {
+    // workers of a ciphertext share their initial state: compute it once per ciphertext
+    if (a->n_ciphers > 0 && a->n_workers >= 4 * a->n_ciphers) {
+      void* init = nullptr;
+      int rc = ctx->buf(14, dform_init_bytes(a->n_ciphers), &init);
+      if (rc) return rc;
+      ctx->launches++;
+      e = launch_dform_init(ctx->stream, p, a->n_ciphers, init, ctx->sm_count);
+      if (e != cudaSuccess) return cuda_fail(e, "dform_init kernel");
+      p.init = init;
+    }
     e = launch_mas_climb_dform(ctx->stream, p, ctx->sm_count);
+  }
   else if ((dform || kern == CCG_FLAG_KERNEL_TFORM) && mas_tform_ok(max_len, tmax))
     e = launch_mas_climb_tform(ctx->stream, p, ctx->sm_count);
   else

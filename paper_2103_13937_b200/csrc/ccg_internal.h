@@ -34,6 +34,7 @@ struct MasLaunch {
   int64_t* tries_done;
   uint32_t flags;
   int64_t* accepts;
+  const void* init;  // D-form: per-ciphertext initial states (dform_init_kernel), or NULL
 };
 
 // MAS climb with an order-G n-gram table (ccg_mas_ngram.cu).
@@ -133,6 +134,9 @@ cudaError_t launch_mas_climb_tform(cudaStream_t s, const MasLaunch& p, int sm_co
 // proposals per warp instruction; the fast path whenever mas_dform_ok(max_len, max(S)).
 bool mas_dform_ok(int64_t max_len, int64_t table_max);
 cudaError_t launch_mas_climb_dform(cudaStream_t s, const MasLaunch& p, int sm_count);
+size_t dform_init_bytes(int64_t n_ciphers);
+cudaError_t launch_dform_init(cudaStream_t s, const MasLaunch& p, int64_t n_ciphers, void* out,
+                              int sm_count);
 size_t mas_ngram_smem_bytes(int order, int64_t max_len);
 cudaError_t launch_mas_ngram_climb(cudaStream_t s, const MasNgramLaunch& p, int sm_count);
 cudaError_t launch_ngram_score(cudaStream_t s, const uint8_t* texts, const int64_t* offsets,

@@ -57,6 +57,17 @@ struct DBlock {
   DWarp<TABLE> w[kDWarps];
 };
 
+// Initial state of a ciphertext's workers (identical for all of them: they start at the
+// ciphertext), computed once per ciphertext by dform_init_kernel when several workers share
+// a ciphertext: T and N in the shared-memory layout, and the score.
+struct alignas(16) CipherInit {
+  int16_t T[kAlpha * kTS];
+  int N[kAlpha * kNS];
+  int score;
+  int pad_[3];
+};
+constexpr int kInitVec = (int)(sizeof(CipherInit) / 16);
+
 template <class WT>
 __device__ __forceinline__ int t_at(const WT& W, int x, int y) { return W.T[x * kTS + y]; }
 
@@ -119,16 +130,35 @@ __device__ __forceinline__ int max_D(const WT& W, int lane) {
   return __reduce_max_sync(kFull, m);
 }
 
-template <bool EARLY, bool TABLE>
-__global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_kernel(const MasLaunch p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  DBlock<TABLE>& B = *reinterpret_cast<DBlock<TABLE>*>(smem_raw);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  DWarp<TABLE>& W = B.w[warp];
+// T = bigram counts of the ciphertext (the worker starts at the ciphertext, mas.py:229-230),
+// N from scratch (lane y owns column y), returns the score (mas.py:232)
+template <class BT, class WT>
+__device__ __forceinline__ int64_t initial_state(const BT& B, WT& W, const uint8_t* text,
+                                                 int64_t n, int lane, int y) {
+  for (int i = lane; i < kAlpha * kTS / 2; i += 32) reinterpret_cast<uint32_t*>(W.T)[i] = 0u;
+  __syncwarp();
+  for (int64_t i = lane; i + 1 < n; i += 32) t_inc(W, text[i], text[i + 1]);
+  __syncwarp();
+  int part = 0;
+  if (lane < kAlpha) {
+    for (int x = 0; x < kAlpha; ++x) {
+      int acc = 0;
+      for (int q = 0; q < kAlpha; ++q)
+        acc += t_at(W, x, q) * B.S[y * kNS + q] + t_at(W, q, x) * B.S[q * kNS + y];
+      W.N[x * kNS + y] = acc;
+      part += t_at(W, x, y) * B.S[x * kNS + y];
+    }
+  }
+  const int64_t score = (int64_t)(int)__reduce_add_sync(kFull, (uint32_t)part);
+  __syncwarp();
+  return score;
+}
 
+template <bool TABLE>
+__device__ __forceinline__ void stage_block_tables(DBlock<TABLE>& B, const int64_t* table) {
   for (int i = threadIdx.x; i < kAlpha * kAlpha; i += blockDim.x) {
     const int x = i / kAlpha, y = i - x * kAlpha;
-    B.S[x * kNS + y] = (int)p.table[i];
+    B.S[x * kNS + y] = (int)table[i];
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kAlpha * kAlpha; i += blockDim.x) {
@@ -137,6 +167,37 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
         B.S[x * kNS + x] + B.S[y * kNS + y] - B.S[x * kNS + y] - B.S[y * kNS + x];
   }
   __syncthreads();
+}
+
+// One warp per ciphertext: its workers' common initial state.
+__global__ void __launch_bounds__(kDWarps * 32) dform_init_kernel(const MasLaunch p, int64_t n_ciphers,
+                                                                  CipherInit* out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  DBlock<false>& B = *reinterpret_cast<DBlock<false>*>(smem_raw);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  DWarp<false>& W = B.w[warp];
+  stage_block_tables(B, p.table);
+  const int y = lane < kAlpha ? lane : 0;
+  for (int64_t c = (int64_t)blockIdx.x * kDWarps + warp; c < n_ciphers;
+       c += (int64_t)gridDim.x * kDWarps) {
+    const int64_t off = p.offsets[c], n = p.offsets[c + 1] - off;
+    const int64_t score = initial_state(B, W, p.ciphers + off, n, lane, y);
+    const uint4* src = reinterpret_cast<const uint4*>(W.T);
+    uint4* dst = reinterpret_cast<uint4*>(out + c);
+    for (int i = lane; i < kInitVec - 1; i += 32) dst[i] = src[i];
+    if (lane == 0) out[c].score = (int)score;
+    __syncwarp();
+  }
+}
+
+template <bool EARLY, bool TABLE>
+__global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_kernel(const MasLaunch p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  DBlock<TABLE>& B = *reinterpret_cast<DBlock<TABLE>*>(smem_raw);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  DWarp<TABLE>& W = B.w[warp];
+
+  stage_block_tables(B, p.table);
 
   const int64_t stride = (int64_t)gridDim.x * kDWarps;
   const uint32_t climbings = (uint32_t)p.climbings;
@@ -148,23 +209,16 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
     const int64_t off = p.offsets[cid], n = p.offsets[cid + 1] - off;
     const uint8_t* text = p.ciphers + off;
 
-    // T = bigram counts of the ciphertext (the worker starts at the ciphertext, mas.py:229-230)
-    for (int i = lane; i < kAlpha * kTS / 2; i += 32) reinterpret_cast<uint32_t*>(W.T)[i] = 0u;
-    __syncwarp();
-    for (int64_t i = lane; i + 1 < n; i += 32) t_inc(W, text[i], text[i + 1]);
-    __syncwarp();
-    // N from scratch (lane y owns column y) and the score (mas.py:232)
-    int part = 0;
-    if (lane < kAlpha) {
-      for (int x = 0; x < kAlpha; ++x) {
-        int acc = 0;
-        for (int q = 0; q < kAlpha; ++q)
-          acc += t_at(W, x, q) * B.S[y * kNS + q] + t_at(W, q, x) * B.S[q * kNS + y];
-        W.N[x * kNS + y] = acc;
-        part += t_at(W, x, y) * B.S[x * kNS + y];
-      }
+    int64_t score;
+    if (p.init) {  // the ciphertext's initial state, computed once by dform_init_kernel
+      const uint4* src = reinterpret_cast<const uint4*>(p.init) + (int64_t)cid * kInitVec;
+      uint4* dst = reinterpret_cast<uint4*>(W.T);  // T, N are contiguous like CipherInit
+      for (int i = lane; i < kInitVec - 1; i += 32) dst[i] = src[i];
+      score = reinterpret_cast<const CipherInit*>(p.init)[cid].score;
+      __syncwarp();
+    } else {
+      score = initial_state(B, W, text, n, lane, y);
     }
-    int64_t score = (int64_t)(int)__reduce_add_sync(kFull, (uint32_t)part);
     int tdg = 0, ndg = 0;  // T[lane][lane], N[lane][lane] (on-demand deltas)
     if (TABLE) {
       rebuild_D(B, W, lane);
@@ -342,6 +396,20 @@ bool mas_dform_ok(int64_t max_len, int64_t table_max) {
   if (table_max > 32767 || max_len > 32768) return false;
   const int64_t n1 = max_len > 0 ? max_len - 1 : 0;
   return n1 * table_max < (int64_t(1) << 27);
+}
+
+size_t dform_init_bytes(int64_t n_ciphers) { return (size_t)n_ciphers * sizeof(CipherInit); }
+
+cudaError_t launch_dform_init(cudaStream_t s, const MasLaunch& p, int64_t n_ciphers, void* out,
+                              int sm_count) {
+  if (n_ciphers <= 0) return cudaSuccess;
+  const int smem = (int)sizeof(DBlock<false>);
+  cudaError_t e = cudaFuncSetAttribute(dform_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int64_t need = (n_ciphers + kDWarps - 1) / kDWarps;
+  const int grid = (int)(need < 4 * (int64_t)sm_count ? need : 4 * (int64_t)sm_count);
+  dform_init_kernel<<<grid, kDWarps * 32, smem, s>>>(p, n_ciphers, (CipherInit*)out);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_mas_climb_dform(cudaStream_t s, const MasLaunch& p, int sm_count) {
