@@ -464,8 +464,8 @@ def main():
                          / kernel_s / 1e9,
                          "note": "algorithmic shared-memory bytes of the D-form algorithm "
                                  "(DESIGN.md 3.1); the kernel is issue-bound (ncu: ~67% of "
-                                 "issue slots, 12.5 warp instructions per evaluation, "
-                                 "profiles/r1d_ncu.txt)"},
+                                 "issue slots, 11.8 warp instructions per evaluation, "
+                                 "profiles/r1e_ncu.txt)"},
             "cpu_baseline": cpu,
             "clocks": clk,
             "gpu_launches": launches,
