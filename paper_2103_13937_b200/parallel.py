@@ -9,8 +9,9 @@ all-gather of the per-worker scores the reference's SolveResult reports
 (per_worker_scores, mas.py:273-278).  Payloads are a few bytes per worker, so this is
 latency-bound; NCCL (or gloo on CPU) all_gather is used as is.
 
-For one ciphertext, `solve_stochastic_sharded` returns the same SolveResult as
-mas.solve_stochastic on one GPU, for any world size.
+For one ciphertext, `solve_stochastic_sharded` / `solve_sct_sharded` return the same
+SolveResult as mas.solve_stochastic / one restart of sct.solve_sct on one GPU, for any world
+size.
 """
 from __future__ import annotations
 
@@ -108,15 +109,18 @@ def solve_stochastic_sharded(cipher, table, cfg, restart: int = 0, climb=None) -
     `climb` defaults to engine.mas_climb (this rank's GPU); tests substitute the oracle."""
     from . import engine
     from .mas import _check_cipher
+    from .ngrams import as_ngram_table
 
     climb = climb or engine.mas_climb
     text = _check_cipher(cipher)
+    t = as_ngram_table(table)
     W = cfg.workers
     lo, hi = rank_slice(W)
     streams = [worker_stream_index(restart, w) for w in range(lo, hi)]
     if hi > lo:
+        extra = {} if t.order == 2 else {"order": t.order}
         res = climb([text], np.zeros(hi - lo, np.int32), philox_keys([cfg.global_seed], streams),
-                    table.scores, cfg.climbings, group_size=hi - lo)
+                    t.scores, cfg.climbings, group_size=hi - lo, **extra)
         local_scores = np.asarray(res.scores, dtype=np.int64)
         b = int(res.group_best[0])
         best_local = (int(local_scores[b]), lo + b, np.asarray(res.keys[b], dtype=np.int64))
@@ -127,3 +131,37 @@ def solve_stochastic_sharded(cipher, table, cfg, restart: int = 0, climb=None) -
     score, idx, mapping = best_over_ranks(best_local[0], best_local[1], best_local[2])
     return SolveResult(best_text=mapping[text], best_score=int(score),
                        per_worker_scores=[int(v) for v in per_worker], history=[])
+
+
+def solve_sct_sharded(cipher, logs, cfg, restart: int = 0, climb=None) -> SolveResult:
+    """One restart of sct.solve_sct (sct.py:179-210) with the cfg.workers workers split over
+    ranks: per-worker float64 scores gathered in worker order, best key = first maximum.
+
+    `climb` defaults to engine.sct_climb (this rank's GPU); tests substitute the oracle."""
+    from . import engine
+    from .ciphers import sct_decrypt
+    from .ngrams import as_log_ngram_table
+
+    climb = climb or engine.sct_climb
+    text = np.asarray(cipher, dtype=np.int64)
+    if text.size < cfg.key_length:
+        raise ValueError("ciphertext shorter than the key")
+    lt = as_log_ngram_table(logs)
+    W, k = cfg.workers, cfg.key_length
+    lo, hi = rank_slice(W)
+    streams = [worker_stream_index(restart, w) for w in range(lo, hi)]
+    if hi > lo:
+        res = climb([text], np.zeros(hi - lo, np.int32), philox_keys([cfg.global_seed], streams),
+                    lt.logs, k, cfg.climbings, p1=cfg.p1, p2=cfg.p2, op1_hop=cfg.op1_hop,
+                    op2_hop=cfg.op2_hop, group_size=hi - lo, order=lt.order)
+        local_scores = np.asarray(res.scores, dtype=np.float64)
+        b = int(res.group_best[0])
+        best_local = (float(local_scores[b]), lo + b, np.asarray(res.keys[b], dtype=np.int64)[:k])
+    else:
+        local_scores = np.zeros(0, dtype=np.float64)
+        best_local = (-np.inf, np.iinfo(np.int64).max, np.zeros(k, np.int64))
+    per_worker = all_gather_array(local_scores)
+    score, idx, key = best_over_ranks(best_local[0], best_local[1], best_local[2])
+    return SolveResult(best_text=sct_decrypt(text, key), best_score=float(score),
+                       per_worker_scores=[float(v) for v in per_worker], history=[],
+                       best_key=key)

@@ -48,6 +48,31 @@ def oracle_climb(ciphers, cipher_of, keys, table, climbings, group_size=0, **_):
                        last_accept=None, tries_done=None, launches=0)
 
 
+def oracle_sct_climb(ciphers, cipher_of, keys, logs, key_length, climbings, p1=33, p2=66,
+                     op1_hop=3, op2_hop=3, group_size=0, order=2, **_):
+    """engine.sct_climb stand-in: the oracle on raw Philox keys."""
+    from oracle import oracle as O
+    from paper_2103_13937_b200.engine import ClimbResult
+
+    keys = np.asarray(keys, dtype=np.uint64).reshape(-1, 2)
+    flat, off = O.ragged(ciphers)
+    cfg = O._cfgv(key_length, climbings, p1, p2, op1_hop, op2_hop, order)
+    lg = np.ascontiguousarray(logs, dtype=np.float64)
+    scores, outk = [], []
+    for c, (k0, k1) in zip(cipher_of, keys):
+        t = flat[off[c]:off[c + 1]]
+        kk = np.empty(key_length, np.int64)
+        s = O.lib().cco_sct_worker(O._p(t), t.size, O._p(lg), O._p(cfg), int(k0), int(k1), 0,
+                                   O._p(kk), None)
+        scores.append(s)
+        outk.append(kk)
+    scores = np.array(scores, dtype=np.float64)
+    gb = np.array([int(np.argmax(scores[i:i + group_size]))
+                   for i in range(0, scores.size, group_size)], dtype=np.int64)
+    return ClimbResult(scores=scores, keys=np.array(outk), group_best=gb, draws_used=None,
+                       last_accept=None, tries_done=None, launches=0)
+
+
 def _worker(rank, world, port, q):
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "tests"))
@@ -70,6 +95,13 @@ def _worker(rank, world, port, q):
             res = parallel.solve_stochastic_sharded(cipher, table, cfg, restart=1,
                                                     climb=oracle_climb)
             out[W] = (res.best_score, res.per_worker_scores, res.best_text.tolist())
+        logs = cc.build_log_table(cc.BigramTable(rng.integers(1, 500, 676)))
+        sc = rng.integers(0, 26, 150)
+        for W in (5, 2):
+            scfg = cc.SctSolverConfig(key_length=6, workers=W, climbings=300, global_seed=17)
+            res = parallel.solve_sct_sharded(sc, logs, scfg, restart=2, climb=oracle_sct_climb)
+            out[("sct", W)] = (res.best_score, res.per_worker_scores, res.best_key.tolist(),
+                               res.best_text.tolist())
         # tie-break: equal scores on both ranks -> lowest global index wins
         s, i, p = parallel.best_over_ranks(10, 7 - rank, np.full(3, rank))
         out["tie"] = (s, i, p.tolist())
@@ -106,6 +138,15 @@ def test_sharded_solve_matches_single_process():
         best = int(ref.group_best[0])
         want = (int(ref.scores[best]), ref.scores.tolist(), ref.keys[best][cipher].tolist())
         assert results[0][W] == want and results[1][W] == want, W
+    logs = cc.build_log_table(cc.BigramTable(rng.integers(1, 500, 676)))
+    sc = rng.integers(0, 26, 150)
+    for W in (5, 2):
+        keys = philox_keys([17], [worker_stream_index(2, w) for w in range(W)])
+        ref = oracle_sct_climb([sc], np.zeros(W, np.int32), keys, logs.logs, 6, 300, group_size=W)
+        best = int(ref.group_best[0])
+        want = (float(ref.scores[best]), ref.scores.tolist(), ref.keys[best].tolist(),
+                cc.sct_decrypt(sc, ref.keys[best]).tolist())
+        assert results[0][("sct", W)] == want and results[1][("sct", W)] == want, W
     assert results[0]["tie"] == results[1]["tie"] == (10, 6, [1, 1, 1])
     assert results[0]["float"] == results[1]["float"] == (3.5, 1, [1, 1])
     assert results[0]["gather"] == results[1]["gather"] == [10, 11, 12]
