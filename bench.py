@@ -130,11 +130,16 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self, which: str):
+        """Record the host time the timed region starts ("begin") or ends ("end")."""
+        setattr(self, "t_" + which, time.time())
 
     def stop(self) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.3)  # let the sample covering the end of the timed region arrive
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -143,7 +148,9 @@ class ClockSampler:
         sm, smax, reasons = [], None, set()
         names = ["active", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
                  "sw_power_cap"]
-        for ln in self.lines:
+        t0, t1 = getattr(self, "t_begin", 0.0), getattr(self, "t_end", float("inf"))
+        window = [ln for t, ln in self.lines if t0 - 0.1 <= t <= t1 + 0.15]
+        for ln in window or [ln for _, ln in self.lines]:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -264,6 +271,25 @@ def config_block(args, world):
 
 
 # ------------------------------------------------------------------ GPU leg
+def issue_roofline(evals_per_s: float, clk: dict) -> dict | None:
+    """Warp instructions issued per second vs the issue peak (4 per SM per clock), using the
+    warp instructions per evaluation measured by ncu on this kernel (profiles/r1e_ncu.txt)."""
+    prof = ROOT / "profiles" / "r1e_ncu.txt"
+    try:
+        import re
+
+        inst = float(re.search(r"warp instructions per try = ([0-9.]+)", prof.read_text()).group(1))
+    except Exception:  # noqa: BLE001
+        return None
+    mhz = clk.get("sm_mhz") or 1965.0
+    peak = 4 * 148 * mhz * 1e6
+    achieved = evals_per_s * inst
+    return {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "warp-inst/s",
+            "frac": achieved / peak, "inst_per_eval": inst,
+            "source": "ncu smsp__inst_executed.sum / tries (profiles/r1e_ncu.txt); peak = "
+                      "4 issue slots x 148 SMs x the median SM clock during the timed steps"}
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":
@@ -328,16 +354,17 @@ def main():
     def step():
         _lib.check(L.ccg_mas_climb_dev(ctx.handle, a), "mas_climb_dev")
 
+    clocks = ClockSampler(device)
+    clocks.start()  # running before the warm-up so that it samples the whole timed region
     for _ in range(args.warmup):
         with torch.cuda.stream(stream):
             flush.zero_()
         step()
     ctx.synchronize()
 
-    clocks = ClockSampler(device)
     barrier(world)
     torch.cuda.synchronize()
-    clocks.start()
+    clocks.mark("begin")
     launches0 = ctx.launches()
     evs = []
     for _ in range(args.steps):
@@ -351,6 +378,7 @@ def main():
         evs.append((e0, e1))
     ctx.synchronize()
     torch.cuda.synchronize()
+    clocks.mark("end")
     barrier(world)
     clk = clocks.stop()
     launches = ctx.launches() - launches0
@@ -463,9 +491,11 @@ def main():
                          "ref_equiv_achieved": evals_per_step * REF_LOOKUP_BYTES_PER_EVAL
                          / kernel_s / 1e9,
                          "note": "algorithmic shared-memory bytes of the D-form algorithm "
-                                 "(DESIGN.md 3.1); the kernel is issue-bound (ncu: ~67% of "
-                                 "issue slots, 11.8 warp instructions per evaluation, "
-                                 "profiles/r1e_ncu.txt)"},
+                                 "(DESIGN.md 3.1); the kernel is issue-bound, see "
+                                 "issue_roofline"},
+            # the binding resource: warp-instruction issue (4 schedulers per SM), with the
+            # instructions per evaluation of the committed ncu capture of this kernel
+            "issue_roofline": issue_roofline(value / world, clk),
             "cpu_baseline": cpu,
             "clocks": clk,
             "gpu_launches": launches,
