@@ -137,7 +137,6 @@ cudaError_t launch_mas_climb_dform(cudaStream_t s, const MasLaunch& p, int sm_co
 size_t dform_init_bytes(int64_t n_ciphers);
 cudaError_t launch_dform_init(cudaStream_t s, const MasLaunch& p, int64_t n_ciphers, void* out,
                               int sm_count);
-size_t mas_ngram_smem_bytes(int order, int64_t max_len);
 cudaError_t launch_mas_ngram_climb(cudaStream_t s, const MasNgramLaunch& p, int sm_count);
 cudaError_t launch_ngram_score(cudaStream_t s, const uint8_t* texts, const int64_t* offsets,
                                int64_t n, int order, const int64_t* table, int64_t* out);

@@ -377,11 +377,6 @@ __global__ void ngram_score_kernel(const uint8_t* __restrict__ texts, const int6
 
 }  // namespace
 
-size_t mas_ngram_smem_bytes(int order, int64_t max_len) {
-  const size_t tab = order <= 3 ? (((size_t)pow26(order) * 2 + 15) & ~(size_t)15) : 0;
-  return tab + (size_t)8 * ng_warp_bytes((int)max_len);
-}
-
 cudaError_t launch_mas_ngram_climb(cudaStream_t s, const MasNgramLaunch& p, int sm_count) {
   if (p.n_workers <= 0) return cudaSuccess;
   switch (p.order) {

@@ -6,11 +6,10 @@
 // maps one 64-bit word x to (x >> 11) * 2^-53.  next_int_below(bound) is int(u * bound)
 // (rng.py:43-47): an IEEE-754 double multiply, rounded to nearest-even, then truncated.
 //
-// Device design (B200): draws are produced a warp at a time.  A refill makes each lane
-// compute ONE Philox block (4 words) and a 4-step shuffle transpose leaves lane i holding
-// draws base+i, base+32+i, base+64+i, base+96+i of the stream ("lane-major window"), so a
-// warp can convert 32 consecutive draws in parallel with any bound and a sequential
-// consumer reads draw j with one shuffle from lane (j-base)&31.
+// Device design (B200): draws are produced a warp at a time -- a refill makes each lane
+// compute ONE Philox block (4 words), so a warp produces 128 consecutive draws at once.
+// The consumers keep them as letters in registers (ccg_mas_common.cuh ByteWindow /
+// LetterWindow) or pre-shifted in shared memory (ccg_sct.cu Draws).
 //
 // int(u*bound) is emulated exactly in integer arithmetic (no FP64 pipe): with m = x>>11
 // and P = m*bound (exact), the double product is P*2^-53 rounded to 53 significant bits;
@@ -119,43 +118,5 @@ __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
   const uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)(v >> 32), src);
   return ((uint64_t)hi << 32) | lo;
 }
-
-// A warp's window of 128 consecutive raw draws of one stream, lane-major.
-// All members are warp-uniform except w[] (per lane).
-struct DrawWindow {
-  uint64_t k0, k1;   // Philox key = (seed, stream)
-  uint64_t base;     // stream index of the first draw in the window (multiple of 4)
-  uint64_t w[4];     // lane i: draws base+i, base+32+i, base+64+i, base+96+i
-
-  // Refill so that the window starts at draw `pos` rounded down to a block boundary.
-  __device__ __forceinline__ void refill(uint64_t pos, int lane) {
-    base = pos & ~3ULL;
-    uint64_t v0, v1, v2, v3;
-    // block index of draw base is base/4; numpy's counter for block b is b+1
-    philox4x64_10(k0, k1, (base >> 2) + 1 + (uint64_t)lane, v0, v1, v2, v3);
-    // lane L now holds draws base+4L .. base+4L+3.  Transpose: draw base+32r+i lives in
-    // lane 8r + i/4, word i%4.
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int src = 8 * r + (lane >> 2);
-      const uint64_t s0 = shfl64(v0, src), s1 = shfl64(v1, src);
-      const uint64_t s2 = shfl64(v2, src), s3 = shfl64(v3, src);
-      const int wsel = lane & 3;
-      w[r] = wsel == 0 ? s0 : wsel == 1 ? s1 : wsel == 2 ? s2 : s3;
-    }
-  }
-
-  // Raw draw `pos + lane` for this lane, valid when pos+31 < base+128 (caller ensures).
-  __device__ __forceinline__ uint64_t lane_draw(uint64_t pos, int lane) const {
-    const uint32_t idx = (uint32_t)(pos - base) + (uint32_t)lane;  // < 128
-    const uint32_t r = idx >> 5;
-    return r == 0 ? w[0] : r == 1 ? w[1] : r == 2 ? w[2] : w[3];
-  }
-
-  // Ensure draws [pos, pos+32) are inside the window.
-  __device__ __forceinline__ void ensure32(uint64_t pos, int lane) {
-    if (pos + 32 > base + 128) refill(pos, lane);
-  }
-};
 
 }  // namespace ccg
