@@ -202,3 +202,32 @@ def solve_deterministic(cipher: MappedText, table: BigramTable, cfg: MasSolverCo
     loop in one GPU launch (one CTA, 325 pair-workers)."""
     text = _check_cipher(cipher)
     return _det_batch(text, table, cfg, [restart])[0]
+
+
+# ------------------------------------------------------------------ many ciphertexts
+def solve_stochastic_batch(ciphers, table, cfg: MasSolverConfig, restart: int = 0,
+                           seeds=None) -> list[SolveResult]:
+    """solve_stochastic (mas.py:253-278) for many ciphertexts in one GPU launch: ciphertext i
+    gets cfg.workers workers on the streams (restart << 32) | w of seed `seeds[i]` (default
+    cfg.global_seed for all), exactly as separate solve_stochastic calls would.  The batch
+    form of BASELINE.json configs 2 and 4."""
+    texts = [_check_cipher(c) for c in ciphers]
+    n, W = len(texts), cfg.workers
+    if n == 0:
+        return []
+    seeds = [cfg.global_seed] * n if seeds is None else list(seeds)
+    if len(seeds) != n:
+        raise ValueError("one seed per ciphertext required")
+    streams = [worker_stream_index(restart, w) for w in range(W)]
+    keys = np.concatenate([philox_keys([s], streams) for s in seeds])
+    t = as_ngram_table(table)
+    res = engine.mas_climb(texts, np.repeat(np.arange(n, dtype=np.int32), W), keys, t.scores,
+                           cfg.climbings, order=t.order, group_size=W, early_exit=True)
+    out = []
+    for i, text in enumerate(texts):
+        sc = res.scores[i * W:(i + 1) * W]
+        best = int(res.group_best[i])
+        out.append(SolveResult(best_text=res.keys[i * W + best].astype(np.int64)[text],
+                               best_score=int(sc[best]), per_worker_scores=[int(v) for v in sc],
+                               history=[]))
+    return out

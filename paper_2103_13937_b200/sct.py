@@ -154,3 +154,39 @@ def solve_sct(cipher: MappedText, logs: LogBigramTable, cfg: SctSolverConfig, jo
         raise ValueError("ciphertext shorter than the key")
     return _batched_restarts(lambda rs: _restart_batch(text, logs, cfg, rs), cfg.restarts,
                              cfg.workers, stop)
+
+
+def solve_sct_batch(ciphers, logs, cfg: SctSolverConfig, restart: int = 0, seeds=None,
+                    key_lengths=None) -> list[SolveResult]:
+    """One restart of solve_sct (sct.py:179-210) for many equal-length ciphertexts in one GPU
+    launch; key_lengths (default cfg.key_length) may differ per ciphertext.  Ciphertext i
+    uses the streams (restart << 32) | w of seed `seeds[i]` (default cfg.global_seed)."""
+    texts = [np.asarray(c, dtype=np.int64) for c in ciphers]
+    n, W = len(texts), cfg.workers
+    if n == 0:
+        return []
+    seeds = [cfg.global_seed] * n if seeds is None else list(seeds)
+    klens = [cfg.key_length] * n if key_lengths is None else [int(k) for k in key_lengths]
+    if len(seeds) != n or len(klens) != n:
+        raise ValueError("one seed and key length per ciphertext required")
+    for t, k in zip(texts, klens):
+        if k < 2:
+            raise ValueError("key_length must be at least 2")
+        if t.size < k:
+            raise ValueError("ciphertext shorter than the key")
+    streams = [worker_stream_index(restart, w) for w in range(W)]
+    keys = np.concatenate([philox_keys([s], streams) for s in seeds])
+    lt = as_log_ngram_table(logs)
+    res = engine.sct_climb(texts, np.repeat(np.arange(n, dtype=np.int32), W), keys, lt.logs,
+                           np.repeat(np.array(klens, dtype=np.int32), W), cfg.climbings,
+                           p1=cfg.p1, p2=cfg.p2, op1_hop=cfg.op1_hop, op2_hop=cfg.op2_hop,
+                           group_size=W, order=lt.order)
+    out = []
+    for i, text in enumerate(texts):
+        sc = res.scores[i * W:(i + 1) * W]
+        best = int(res.group_best[i])
+        key = res.keys[i * W + best, :klens[i]].astype(np.int64)
+        out.append(SolveResult(best_text=sct_decrypt(text, key), best_score=float(sc[best]),
+                               per_worker_scores=[float(v) for v in sc], history=[],
+                               best_key=key))
+    return out

@@ -784,3 +784,25 @@ def test_fuzz_sct_vs_oracle():
                                          p1=p1, p2=p2, op1_hop=2, op2_hop=4)
             assert float(res.scores[i]) == score, (trial, i)
             assert np.array_equal(res.keys[i, :k].astype(np.int64), key)
+
+
+def test_batch_solvers_equal_per_ciphertext_solves(golden):
+    rng = np.random.default_rng(21)
+    table = cc.BigramTable(golden.english_scores())
+    ciphers = [rng.integers(0, 26, int(L)) for L in (50, 120, 300)]
+    cfg = cc.MasSolverConfig(workers=16, climbings=3000, global_seed=5)
+    got = cc.solve_stochastic_batch(ciphers, table, cfg, restart=2, seeds=[5, 6, 7])
+    for c, s, g in zip(ciphers, (5, 6, 7), got):
+        want = cc.solve_stochastic(c, table, cc.MasSolverConfig(workers=16, climbings=3000,
+                                                                 global_seed=s), restart=2)
+        assert g.per_worker_scores == want.per_worker_scores
+        assert np.array_equal(g.best_text, want.best_text)
+    logs = cc.LogBigramTable(golden.english_logs(), -24.0)
+    sct_c = [rng.integers(0, 26, 240) for _ in range(3)]
+    scfg = cc.SctSolverConfig(key_length=6, workers=8, climbings=600, global_seed=9)
+    got = cc.solve_sct_batch(sct_c, logs, scfg, key_lengths=[5, 6, 9])
+    for c, k, g in zip(sct_c, (5, 6, 9), got):
+        want, _ = cc.solve_sct(c, logs, cc.SctSolverConfig(key_length=k, workers=8, climbings=600,
+                                                           global_seed=9))
+        assert g.per_worker_scores == want.per_worker_scores
+        assert np.array_equal(g.best_key, want.best_key)
