@@ -15,6 +15,11 @@
 // FIRST touched position is i (so a window holding several touched positions is counted
 // once).  Cost per evaluation ~ (occurrences of a and b) x G x 2 lookups instead of O(n).
 //
+// Delta cache.  A rejected proposal leaves the state unchanged, so every computed delta is
+// kept (per letter pair, tagged with an epoch that each accept advances): after the last
+// accept of a climb -- typically within its first ~20 % of tries -- almost every proposal
+// is a cache hit.
+//
 // Warp layout.  Four proposals are evaluated per iteration, one per 8-lane group (lanes
 // 8g..8g+7 walk the touched positions of proposal g).  Proposals never read the state
 // (rng.py:81-89), so all four are scored against the state before the first; the common
@@ -38,8 +43,10 @@ __host__ __device__ constexpr int pow26(int g) { return g == 0 ? 1 : 26 * pow26(
 __host__ __device__ inline uint32_t ng_text_stride(int max_len) {
   return ((uint32_t)max_len + 12u + 15u) & ~15u;  // plaintext at +4, >= 8 bytes of slack after
 }
+constexpr uint32_t kCacheBytes = 676u * 4u + 676u * 2u + 8u;  // delta cache + epoch tags
 __host__ __device__ inline uint32_t ng_warp_bytes(int max_len) {
-  return ng_text_stride(max_len) + ((2u * (uint32_t)max_len + 15u) & ~15u) + 32u * 2u + 32u * 4u;
+  return ng_text_stride(max_len) + ((2u * (uint32_t)max_len + 15u) & ~15u) + 32u * 2u + 32u * 4u +
+         kCacheBytes;
 }
 
 // per-byte equality mask (0x80 in each byte of x equal to the byte in rep), exact for bytes < 0x80
@@ -135,6 +142,11 @@ __global__ void __launch_bounds__(kNgWarps * 32) mas_ngram_kernel(const MasNgram
   uint16_t* start = reinterpret_cast<uint16_t*>(wb + ng_text_stride(max_len) +
                                                 ((2u * (uint32_t)max_len + 15u) & ~15u));
   uint32_t* cursor = reinterpret_cast<uint32_t*>(start + 32);
+  // exact deltas of the current state already computed, keyed by the letter pair (a < b):
+  // valid while dtag == epoch, and every accept starts a new epoch (a rejected proposal leaves
+  // the state unchanged, so late in a climb almost every proposal is a cache hit)
+  int* dcache = reinterpret_cast<int*>(cursor + 32);
+  uint16_t* dtag = reinterpret_cast<uint16_t*>(dcache + 676);
 
   NgState<G, SMEM_TAB> st;
   st.tab = p.table;
@@ -190,6 +202,9 @@ __global__ void __launch_bounds__(kNgWarps * 32) mas_ngram_kernel(const MasNgram
       score = (int64_t)(int)__reduce_add_sync(kFull, (uint32_t)part);
     }
     int pinv = lane < kAlpha ? lane : 0;  // pi^-1(lane): the cipher letter holding plaintext lane
+    for (int i = lane; i < 676 / 2; i += 32) reinterpret_cast<uint32_t*>(dtag)[i] = 0u;
+    uint32_t epoch = 1;
+    __syncwarp();
 
     ByteWindow win;
     win.key = p.keys + 2 * w;
@@ -203,11 +218,21 @@ __global__ void __launch_bounds__(kNgWarps * 32) mas_ngram_kernel(const MasNgram
       const int sa = start[xa], na = (int)start[xa + 1] - sa;
       const int sb = start[xb], nb = (int)start[xb + 1] - sb;
       const uint32_t arep = a * 0x01010101u, brep = b * 0x01010101u;
+      const int key = (int)(min(a, b) * kAlpha + max(a, b));
+      const bool hit = a == b || dtag[key] == epoch;  // a == b: no interchange, delta 0
+      const int m = hit ? 0 : na + nb;
       int d = 0;
-      for (int j = sl; j < na + nb; j += 8) d += st.position_delta(st.touched(j, sa, na, sb), arep, brep);
+      for (int j = sl; j < m; j += 8) d += st.position_delta(st.touched(j, sa, na, sb), arep, brep);
       d += __shfl_xor_sync(kFull, d, 1);
       d += __shfl_xor_sync(kFull, d, 2);
       d += __shfl_xor_sync(kFull, d, 4);
+      if (hit) {
+        d = a == b ? 0 : dcache[key];
+      } else if (sl == 0) {
+        dcache[key] = d;
+        dtag[key] = (uint16_t)epoch;
+      }
+      __syncwarp();
       return d;
     };
     auto eval_one = [&](uint32_t a, uint32_t b) -> int {
@@ -215,9 +240,17 @@ __global__ void __launch_bounds__(kNgWarps * 32) mas_ngram_kernel(const MasNgram
       const int sa = start[xa], na = (int)start[xa + 1] - sa;
       const int sb = start[xb], nb = (int)start[xb + 1] - sb;
       const uint32_t arep = a * 0x01010101u, brep = b * 0x01010101u;
+      const int key = (int)(min(a, b) * kAlpha + max(a, b));
+      if (dtag[key] == epoch) return dcache[key];
       int d = 0;
       for (int j = lane; j < na + nb; j += 32) d += st.position_delta(st.touched(j, sa, na, sb), arep, brep);
-      return (int)__reduce_add_sync(kFull, (uint32_t)d);
+      d = (int)__reduce_add_sync(kFull, (uint32_t)d);
+      if (lane == 0) {
+        dcache[key] = d;
+        dtag[key] = (uint16_t)epoch;
+      }
+      __syncwarp();
+      return d;
     };
     // commit a<->b (mas.py:237-243)
     auto accept = [&](int a, int b, int d) {
@@ -232,6 +265,10 @@ __global__ void __launch_bounds__(kNgWarps * 32) mas_ngram_kernel(const MasNgram
       }
       if (lane == a) pinv = xb;
       if (lane == b) pinv = xa;
+      if (++epoch == 0x10000u) {  // tags wrap: clear them
+        for (int i = lane; i < 676 / 2; i += 32) reinterpret_cast<uint32_t*>(dtag)[i] = 0u;
+        epoch = 1;
+      }
       __syncwarp();
     };
     auto improvable = [&]() {
