@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kDetThreads) det_step_kernel(const uint8_t* te
 
 // mas.py:140-169 solve_deterministic, one job per CTA.
 template <typename Acc>
-__global__ void __launch_bounds__(kDetThreads) det_solve_kernel(const MasDetLaunch p) {
+__global__ void __launch_bounds__(kDetThreads, 5) det_solve_kernel(const MasDetLaunch p) {
   __shared__ DetShared<Acc> sh;
   const int64_t job = blockIdx.x;
   const int32_t cid = p.cipher_of[job];
