@@ -124,7 +124,7 @@ struct NgState {
 };
 
 template <int G, bool SMEM_TAB, int kNgWarps>
-__global__ void __launch_bounds__(kNgWarps * 32) mas_ngram_kernel(const MasNgramLaunch p) {
+__global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngram_kernel(const MasNgramLaunch p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int kTab = pow26(G);
@@ -383,13 +383,15 @@ cudaError_t launch_ng_w(cudaStream_t s, const MasNgramLaunch& p, int sm_count) {
   return cudaGetLastError();
 }
 
-// 16 warps per block when the shared-memory layout fits (more latency hiding for the
-// table lookups), else 8.
+// The largest block the shared-memory layout allows: 32 warps when a staged table is shared
+// by a whole SM, else 16, else 8 (more warps hide the table-lookup latency).
 template <int G, bool SMEM_TAB>
 cudaError_t launch_ng(cudaStream_t s, const MasNgramLaunch& p, int sm_count) {
   const size_t tab = SMEM_TAB ? (((size_t)pow26(G) * 2 + 15) & ~(size_t)15) : 0;
-  if (tab + 16 * (size_t)ng_warp_bytes((int)p.max_len) <= 200 * 1024)
-    return launch_ng_w<G, SMEM_TAB, 16>(s, p, sm_count);
+  const size_t wb = ng_warp_bytes((int)p.max_len);
+  if (SMEM_TAB && tab + 32 * wb <= 220 * 1024)  // one 32-warp block per SM shares the table
+    return launch_ng_w<G, SMEM_TAB, 32>(s, p, sm_count);
+  if (tab + 16 * wb <= 200 * 1024) return launch_ng_w<G, SMEM_TAB, 16>(s, p, sm_count);
   return launch_ng_w<G, SMEM_TAB, 8>(s, p, sm_count);
 }
 
