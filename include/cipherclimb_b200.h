@@ -172,6 +172,8 @@ typedef struct {
   int64_t *group_best;
   int64_t max_len;            /* required by the _dev entry point only */
   uint32_t flags;
+  int64_t *computed;          /* [n_workers] deltas computed by a position walk (the other tries
+                                 read the delta cache of the unchanged state), or NULL */
 } ccg_mas_ngram_args;
 
 int ccg_mas_ngram_climb(ccg_ctx *ctx, const ccg_mas_ngram_args *args);

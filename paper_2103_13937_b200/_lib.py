@@ -58,7 +58,7 @@ class MasNgramArgs(C.Structure):
         ("skips", _P), ("n_workers", _i64), ("climbings", _i64), ("order", _i32), ("table", _P),
         ("scores", _P), ("maps", _P), ("draws_used", _P), ("last_accept", _P),
         ("tries_done", _P), ("group_size", _i32), ("group_best", _P), ("max_len", _i64),
-        ("flags", _u32),
+        ("flags", _u32), ("computed", _P),
     ]
 
 

@@ -701,6 +701,7 @@ static int ngram_launch(ccg_ctx* ctx, const ccg_mas_ngram_args* a, int64_t max_l
   p.draws_used = a->draws_used;
   p.last_accept = a->last_accept;
   p.tries_done = a->tries_done;
+  p.computed = a->computed;
   p.flags = a->flags;
   ctx->launches++;
   cudaError_t e = launch_mas_ngram_climb(ctx->stream, p, ctx->sm_count);
@@ -778,6 +779,10 @@ int ccg_mas_ngram_climb(ccg_ctx* ctx, const ccg_mas_ngram_args* a) {
     if ((rc = ctx->buf(10, (size_t)nw * 8, &p))) return rc;
     d.tries_done = (int64_t*)p;
   }
+  if (a->computed) {
+    if ((rc = ctx->buf(12, (size_t)nw * 8, &p))) return rc;
+    d.computed = (int64_t*)p;
+  }
   const int64_t ng = a->group_size > 0 ? nw / a->group_size : 0;
   if (a->group_best && ng) {
     if ((rc = ctx->buf(11, (size_t)ng * 8, &p))) return rc;
@@ -792,6 +797,7 @@ int ccg_mas_ngram_climb(ccg_ctx* ctx, const ccg_mas_ngram_args* a) {
   if (a->last_accept && (rc = download(ctx, a->last_accept, d.last_accept, (size_t)nw * 8)))
     return rc;
   if (a->tries_done && (rc = download(ctx, a->tries_done, d.tries_done, (size_t)nw * 8))) return rc;
+  if (a->computed && (rc = download(ctx, a->computed, d.computed, (size_t)nw * 8))) return rc;
   if (ng && a->group_best && (rc = download(ctx, a->group_best, d.group_best, (size_t)ng * 8)))
     return rc;
   return finish(ctx, cudaSuccess, "mas_ngram_climb");

@@ -56,6 +56,7 @@ struct MasNgramLaunch {
   int64_t* last_accept;
   int64_t* tries_done;
   uint32_t flags;
+  int64_t* computed;
 };
 
 // Deterministic best-neighbour MAS (ccg_mas_det.cu): one job = one (ciphertext, restart).

@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
     int pinv = lane < kAlpha ? lane : 0;  // pi^-1(lane): the cipher letter holding plaintext lane
     for (int i = lane; i < 676 / 2; i += 32) reinterpret_cast<uint32_t*>(dtag)[i] = 0u;
     uint32_t epoch = 1;
+    int64_t walks = 0;  // deltas computed by a position walk (the rest came from the cache)
     __syncwarp();
 
     ByteWindow win;
@@ -221,6 +222,7 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
       const int key = (int)(min(a, b) * kAlpha + max(a, b));
       const bool hit = a == b || dtag[key] == epoch;  // a == b: no interchange, delta 0
       const int m = hit ? 0 : na + nb;
+      walks += __popc(__ballot_sync(kFull, !hit && sl == 0));
       int d = 0;
       for (int j = sl; j < m; j += 8) d += st.position_delta(st.touched(j, sa, na, sb), arep, brep);
       d += __shfl_xor_sync(kFull, d, 1);
@@ -242,6 +244,7 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
       const uint32_t arep = a * 0x01010101u, brep = b * 0x01010101u;
       const int key = (int)(min(a, b) * kAlpha + max(a, b));
       if (dtag[key] == epoch) return dcache[key];
+      ++walks;
       int d = 0;
       for (int j = lane; j < na + nb; j += 32) d += st.position_delta(st.touched(j, sa, na, sb), arep, brep);
       d = (int)__reduce_add_sync(kFull, (uint32_t)d);
@@ -360,6 +363,7 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
       if (p.draws_used) p.draws_used[w] = win.position();
       if (p.last_accept) p.last_accept[w] = last;
       if (p.tries_done) p.tries_done[w] = t;
+      if (p.computed) p.computed[w] = walks;
     }
     __syncwarp();
   }

@@ -71,6 +71,7 @@ class ClimbResult:
     tries_done: np.ndarray | None
     launches: int
     accepts: np.ndarray | None = None   # accepted interchanges per worker (bigram MAS kernels)
+    computed: np.ndarray | None = None  # n-gram kernel: deltas computed by position walks
 
 
 def _run_sharded(n_workers, group_size, devs, fn):
@@ -91,7 +92,7 @@ def _concat(parts, name):
 
 def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, group_size=0,
               draws_used=False, last_accept=False, tries_done=False, early_exit=False,
-              order=2, ngram_kernel=False, kernel="auto", accepts=False,
+              order=2, ngram_kernel=False, kernel="auto", accepts=False, computed=False,
               out: ClimbResult | None = None, devices_=None) -> ClimbResult:
     """Run stochastic_worker (mas.py:218-244) for every worker on the GPU(s).
 
@@ -146,6 +147,7 @@ def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, 
                 tries_done=np.empty(m, dtype=np.int64) if tries_done else None,
                 launches=0,
                 accepts=np.empty(m, dtype=np.int64) if (accepts and not use_ng) else None,
+                computed=np.empty(m, dtype=np.int64) if (computed and use_ng) else None,
             )
         if m == 0:
             return out
@@ -165,6 +167,7 @@ def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, 
         a.flags = (_lib.FLAG_EARLY_EXIT if early_exit else 0) | _lib.KERNEL_FLAGS[kernel]
         if use_ng:
             a.order = order
+            a.computed = _lib.ptr(out.computed)
         ctx = _lib.context(dev)
         with ctx.lock:
             before = ctx.launches()
@@ -182,6 +185,7 @@ def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, 
         group_best=_concat(parts, "group_best"), draws_used=_concat(parts, "draws_used"),
         last_accept=_concat(parts, "last_accept"), tries_done=_concat(parts, "tries_done"),
         launches=sum(p.launches for p in parts), accepts=_concat(parts, "accepts"),
+        computed=_concat(parts, "computed"),
     )
 
 

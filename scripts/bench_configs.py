@@ -192,7 +192,8 @@ def c4(args):
         ciphers.append(O.permutation(400000 + i, KEYGEN, 26)[p])
     cof = np.repeat(np.arange(n_c, dtype=np.int32), R)
     keys = philox_keys([4000], list(range(cof.size)))
-    res, dt = timed(lambda: engine.mas_climb(ciphers, cof, keys, q4.scores, K, order=4, group_size=R))
+    res, dt = timed(lambda: engine.mas_climb(ciphers, cof, keys, q4.scores, K, order=4, group_size=R,
+                                             computed=True))
     evals = cof.size * K
     ok = sum(np.array_equal(res.keys[j * R + int(res.group_best[j])].astype(np.int64)[ciphers[j]],
                             plains[j]) for j in range(n_c))
@@ -203,6 +204,7 @@ def c4(args):
     emit({"config": "C4", "what": "MAS 60-100 letters, quadgram uint16 table via L2, one worker per "
                                   "restart", "ciphers": n_c, "restarts_per_cipher": R,
           "climbings": K, "evals": evals, "seconds": dt, "evals_per_s": evals / dt,
+          "computed_by_walk": float(res.computed.sum() / evals),
           "recovered": int(ok), "of": n_c, "cpu_evals_per_s": rate_cpu, "cpu_cores": THREADS,
           "cpu_kind": "oracle port, full rescore per try"})
 
@@ -219,10 +221,14 @@ def c5(args):
     for order in (2, 3, 4):
         for n in sizes:
             keys = philox_keys([5], list(range(n)))
-            _, dt = timed(lambda: engine.mas_climb([cipher], np.zeros(n, np.int32), keys, tabs[order],
-                                                   K, order=order))
-            emit({"config": "C5", "order": order, "workers": n, "climbings": K, "text_len": 300,
-                  "evals_per_s": n * K / dt, "seconds": dt})
+            res, dt = timed(lambda: engine.mas_climb([cipher], np.zeros(n, np.int32), keys,
+                                                     tabs[order], K, order=order,
+                                                     computed=order > 2))
+            line = {"config": "C5", "order": order, "workers": n, "climbings": K, "text_len": 300,
+                    "evals_per_s": n * K / dt, "seconds": dt}
+            if order > 2:
+                line["computed_by_walk"] = float(res.computed.sum() / (n * K))
+            emit(line)
 
 
 def main():

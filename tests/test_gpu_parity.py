@@ -490,7 +490,9 @@ def test_ngram_climb_english_quadgram_and_early_exit(golden):
     streams = list(range(cof.size))
     keys = philox_keys([4242], streams)
     full = engine.mas_climb(ciphers, cof, keys, q4.scores, 6000, order=4, group_size=8,
-                            tries_done=True)
+                            tries_done=True, computed=True)
+    # most tries are served by the delta cache once the climb has settled
+    assert (full.computed > 0).all() and full.computed.sum() < 0.5 * full.tries_done.sum()
     want_s, _ = O.ngram_workers(ciphers, cof, seeds, streams, 4, q4.scores, 6000)
     assert full.scores.tolist() == want_s.tolist()
     early = engine.mas_climb(ciphers, cof, keys, q4.scores, 6000, order=4, group_size=8,
