@@ -1,4 +1,7 @@
-// ccg_mas.cu -- monoalphabetic-substitution (MAS) kernels for sm_100a.
+// ccg_mas.cu -- monoalphabetic-substitution (MAS) kernels for sm_100a: the pi-form climb
+// (packed 16-bit and wide int64 variants -- the engine's exact fallback for tables past the
+// D-form / T-form gates: max(S) > 32767 or very long texts), the fitness-oracle kernels
+// (score_text, swap_delta batches), Philox draws and the per-group first-max.
 //
 // Reference path: mas.py:218-244 stochastic_worker (per try: draw a distinct letter pair,
 // exact score delta of interchanging the two letters in the current text via the

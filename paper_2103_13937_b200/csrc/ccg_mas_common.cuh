@@ -1,6 +1,7 @@
 // ccg_mas_common.cuh -- device helpers shared by the MAS climb kernels (ccg_mas.cu,
-// ccg_mas_tform.cu): the per-worker letter window over the numpy Philox stream
-// (rng.py:81-89 next_distinct_pair(26)) and raw shared-memory accessors.
+// ccg_mas_tform.cu, ccg_mas_dform.cu, ccg_mas_ngram.cu): the per-worker letter windows over
+// the numpy Philox stream (rng.py:81-89 next_distinct_pair(26)) and raw shared-memory
+// accessors.
 #pragma once
 #include "ccg_internal.h"
 #include "ccg_rng.cuh"

@@ -1,5 +1,7 @@
-// ccg_mas_dform.cu -- the MAS stochastic climb with a maintained table of exact swap deltas
-// ("D-form"): the sm_100a fast path of mas.py:218-244 stochastic_worker.
+// ccg_mas_dform.cu -- the MAS stochastic climb from maintained aggregates that give every
+// exact swap delta in O(1) ("D-form"): the sm_100a fast path of mas.py:218-244
+// stochastic_worker.  Default: deltas computed on demand from T, N (five reads); variant
+// CCG_FLAG_KERNEL_DTABLE keeps the full 325-entry delta table instead.
 //
 // Why.  A rejected proposal does not change the state, and ~99% of proposals are rejected
 // (the reference accepts ~70 of 10,000 tries, mas.py:237).  The reference recomputes

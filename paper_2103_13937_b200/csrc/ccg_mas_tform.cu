@@ -1,5 +1,6 @@
-// ccg_mas_tform.cu -- the MAS climb in "T-form": the sm_100a fast path of
-// mas.py:218-244 stochastic_worker (driven by mas.py:253-278 solve_stochastic).
+// ccg_mas_tform.cu -- the MAS climb in "T-form": mas.py:218-244 stochastic_worker (driven
+// by mas.py:253-278 solve_stochastic) for tables beyond the D-form gate (ccg_mas_dform.cu
+// is the fast path; this kernel was the round-1 headline before it).
 //
 // State.  Like the reference, the warp keeps the bigram-count matrix T of the CURRENT
 // plaintext (mas.py:230, rows/columns swapped on accept at mas.py:239-240), not the
