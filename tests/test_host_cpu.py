@@ -217,3 +217,54 @@ def test_ngram_file_formats_round_trip(golden):
         cc.parse_ngram_file("abc -1\n", 3)
     with pytest.warns(UserWarning):
         cc.parse_ngram_file("abc 1\nabc 2\n", 3)
+
+
+def test_packed_batches_and_ragged():
+    flat, off = _lib.ragged([np.array([1, 2]), [3], np.zeros(0, np.int64)])
+    assert flat.tolist() == [1, 2, 3] and off.tolist() == [0, 2, 3, 3]
+    p = _lib.Packed.of([[0, 25], [7]])
+    assert len(p) == 2 and p[0].tolist() == [0, 25] and p[1].tolist() == [7]
+    assert _lib.ragged(p)[0] is p.flat
+    for bad in ([[26]], [[-1]]):
+        with pytest.raises(ValueError):
+            _lib.ragged(bad)
+    with pytest.raises(ValueError):
+        _lib.Packed(np.array([1, 2], np.uint8), np.array([0, 3]))   # offsets past the end
+    with pytest.raises(ValueError):
+        _lib.Packed(np.array([1, 2], np.uint8), np.array([1, 2]))   # not starting at 0
+
+
+def test_ngram_tables_validate():
+    with pytest.raises(ValueError):
+        cc.NgramTable(5, np.zeros(26**2, np.int64))
+    with pytest.raises(ValueError):
+        cc.NgramTable(3, np.zeros(26**2, np.int64))
+    with pytest.raises(ValueError):
+        cc.NgramTable(3, -np.ones(26**3, np.int64))
+    with pytest.raises(ValueError):
+        cc.LogNgramTable(3, np.ones(26**3), -24.0)          # positive log-probabilities
+    t = cc.build_ngram_table_from_corpus("the theme then", 3)
+    lg = cc.build_log_ngram_table(t, floor=-30.0)
+    q = cc.quantize_log_table(lg)
+    assert q.order == 3 and q.scores.max() <= 65535 and q.scores.min() >= 0
+    # the affine map keeps the order of the log-probabilities (ties allowed by rounding)
+    order = np.argsort(lg.logs, kind="stable")
+    assert (np.diff(q.scores[order]) >= 0).all()
+    with pytest.raises(ValueError):
+        cc.build_log_ngram_table(t, floor=-1.0)                # floor above the rarest trigram
+    assert cc.as_ngram_table(cc.BigramTable(np.arange(676))).order == 2
+
+
+def test_batch_solver_validation_happens_before_the_gpu():
+    logs = cc.LogBigramTable(np.full(676, -10.0), -24.0)
+    cfg = cc.SctSolverConfig(key_length=5)
+    with pytest.raises(ValueError):
+        cc.solve_sct_batch([np.zeros(4, np.int64)], logs, cfg)               # shorter than the key
+    with pytest.raises(ValueError):
+        cc.solve_sct_batch([np.zeros(40, np.int64)] * 2, logs, cfg, seeds=[1])
+    table = cc.BigramTable(np.ones(676, np.int64))
+    with pytest.raises(ValueError):
+        cc.solve_stochastic_batch([np.zeros(5, np.int64)], table, cc.MasSolverConfig())  # 1 letter
+    assert cc.solve_stochastic_batch([], table, cc.MasSolverConfig()) == []
+    with pytest.raises(ValueError):
+        cc.encrypt_batch([[1, 2]], "xyz", key_seeds=[1])
