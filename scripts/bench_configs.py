@@ -231,14 +231,70 @@ def c5(args):
             emit(line)
 
 
+def ttr(args):
+    """Time to recover the key on the reference's acceptance recipes (tests/test_acceptance.py
+    :146-198; BASELINE.json metric "time-to-recover key"): MAS #07 (471 letters, 10 keys,
+    64 workers x 10k, <= 20 restarts) and SCT #08 (596 letters, k = 10 / 15, 64 x 15k,
+    <= 5 / 10 restarts), stop on the exact plaintext, through the public API.  CPU column:
+    the C oracle port on all host cores running the same restarts until the same stop."""
+    from oracle import oracle as O
+
+    plain = G.plain_mas(471)
+    table = cc.BigramTable(G.english_scores())
+    gpu_t, cpu_t, ok, ok_cpu, restarts = [], [], 0, 0, []
+    for e in range(10 if not args.quick else 3):
+        cipher = O.permutation(700 + e, KEYGEN, 26)[plain]
+        cfg = cc.MasSolverConfig(workers=64, climbings=10_000, restarts=20, global_seed=7000 + e)
+        t0 = time.perf_counter()
+        best, summ = cc.solve_with_restarts(cipher, table, cfg,
+                                            stop=lambda r: bool(np.array_equal(r.best_text, plain)))
+        gpu_t.append(time.perf_counter() - t0)
+        ok += bool(np.array_equal(best.best_text, plain))
+        restarts.append(len(summ))
+        t0 = time.perf_counter()
+        for r in range(20):
+            s, m = O.mas_workers([cipher], np.zeros(64, np.int32), [7000 + e] * 64,
+                                 [(r << 32) | w for w in range(64)], table.scores, 10_000,
+                                 threads=THREADS)
+            if np.array_equal(m[int(np.argmax(s))][cipher], plain):
+                ok_cpu += 1
+                break
+        cpu_t.append(time.perf_counter() - t0)
+    emit({"config": "TTR", "what": "acceptance #07 MAS: 10 keys, 471 letters, 64 x 10k, <= 20 "
+                                   "restarts, stop on the plaintext",
+          "recovered": ok, "recovered_cpu": ok_cpu, "of": len(gpu_t),
+          "restarts_used": restarts, "gpu_seconds_total": sum(gpu_t),
+          "gpu_seconds_per_key": gpu_t, "cpu_seconds_total": sum(cpu_t), "cpu_cores": THREADS,
+          "reference_python_seconds_total": 146.0,
+          "reference_note": "the Python reference took 146.0 s for this gate (jobs=2) in the "
+                            "build container (SURVEY.md section 6)"})
+    plain = G.plain_sct(596)
+    logs = cc.LogBigramTable(G.english_logs(), -24.0)
+    for k, R in ((10, 5), (15, 10)):
+        gpu_t, ok = [], 0
+        for e in range(10 if not args.quick else 3):
+            cipher = cc.sct_encrypt(plain, O.permutation(800 + e, KEYGEN, k))
+            cfg = cc.SctSolverConfig(key_length=k, workers=64, climbings=15_000, restarts=R,
+                                     global_seed=8000 + e)
+            t0 = time.perf_counter()
+            best, _ = cc.solve_sct(cipher, logs, cfg,
+                                   stop=lambda r: bool(np.array_equal(r.best_text, plain)))
+            gpu_t.append(time.perf_counter() - t0)
+            ok += bool(np.array_equal(best.best_text, plain))
+        emit({"config": "TTR", "what": f"acceptance #08 SCT: k={k}, 596 letters, 64 x 15k, "
+                                       f"<= {R} restarts, stop on the plaintext",
+              "recovered": ok, "of": len(gpu_t), "gpu_seconds_total": sum(gpu_t),
+              "gpu_seconds_per_key": gpu_t})
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
-    ap.add_argument("--only", default="C1,C1d,C3,C4,C5")
+    ap.add_argument("--only", default="C1,C1d,C3,C4,C5,TTR")
     args = ap.parse_args()
     engine.set_devices([0])
     for name in args.only.split(","):
-        {"C1": c1, "C1d": c1d, "C3": c3, "C4": c4, "C5": c5}[name.strip()](args)
+        {"C1": c1, "C1d": c1d, "C3": c3, "C4": c4, "C5": c5, "TTR": ttr}[name.strip()](args)
 
 
 if __name__ == "__main__":
