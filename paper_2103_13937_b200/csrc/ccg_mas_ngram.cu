@@ -20,13 +20,16 @@
 // accept of a climb -- typically within its first ~20 % of tries -- almost every proposal
 // is a cache hit.
 //
-// Warp layout.  Four proposals are evaluated per iteration, one per 8-lane group (lanes
-// 8g..8g+7 walk the touched positions of proposal g).  Proposals never read the state
-// (rng.py:81-89), so all four are scored against the state before the first; the common
-// all-rejected case is exactly the sequential outcome, otherwise the batch is replayed in
-// order with re-evaluation after the first accept (as in ccg_mas_tform.cu).  The window
-// bytes around a position come from three 32-bit shared loads and two funnel shifts; the
-// a/b tests and the swapped copy are SWAR byte operations on those words.
+// Warp rounds.  A round pairs up to 32 proposals, one per lane, exactly as the D-form
+// kernel does (rng.py:81-89), and reads their cached deltas: the cache-hit prefix before the
+// first miss decides it (first positive delta accepted, else all rejected).  On a miss the
+// first four misses of the round are walked at once, one per 8-lane group, into the cache,
+// and the round is re-run -- proposals never read the state (rng.py:81-89), so computing
+// deltas ahead of the sequential order is exact; after an accept they are simply stale.
+// The window bytes around a position come from three 32-bit shared loads and two funnel
+// shifts; the a/b tests and the swapped copy are SWAR byte operations on those words.  The
+// table score of every window of the current plaintext is kept in shared memory (refreshed
+// around the touched positions on accept), so a walk looks up only the new windows.
 //
 // Tables: G <= 3 are staged in shared memory (1.3 KB / 34 KB of uint16); the quadgram
 // table (914 KB uint16) is read through L1/L2 with __ldg.
@@ -44,9 +47,13 @@ __host__ __device__ inline uint32_t ng_text_stride(int max_len) {
   return ((uint32_t)max_len + 12u + 15u) & ~15u;  // plaintext at +4, >= 8 bytes of slack after
 }
 constexpr uint32_t kCacheBytes = 676u * 4u + 676u * 2u + 8u;  // delta cache + epoch tags
+__host__ __device__ inline uint32_t ng_u16_bytes(int max_len) {
+  return (2u * (uint32_t)max_len + 15u) & ~15u;
+}
+// plaintext | occurrence lists | start | cursor | delta cache + tags | window scores
 __host__ __device__ inline uint32_t ng_warp_bytes(int max_len) {
-  return ng_text_stride(max_len) + ((2u * (uint32_t)max_len + 15u) & ~15u) + 32u * 2u + 32u * 4u +
-         kCacheBytes;
+  return ng_text_stride(max_len) + ng_u16_bytes(max_len) + 32u * 2u + 32u * 4u + kCacheBytes +
+         ng_u16_bytes(max_len);
 }
 
 // per-byte equality mask (0x80 in each byte of x equal to the byte in rep), exact for bytes < 0x80
@@ -64,6 +71,7 @@ struct NgState {
   uint32_t text_base;    // shared address of the plaintext buffer (plain[i] at +4+i)
   const uint16_t* occ;   // occurrence lists (shared)
   const uint16_t* start; // start[x] .. start[x+1] (shared)
+  uint32_t ws_base;      // shared address of the window scores
   int n;
 
   __device__ __forceinline__ int lookup(int idx) const {
@@ -102,16 +110,14 @@ struct NgState {
       for (int j = first; j < 3; ++j) before |= touched_lo & (1u << (8 * j));
       const bool valid = s >= 0 && s + G <= n && before == 0;
       if (valid) {
-        int io = 0, in = 0;
+        int in = 0;
 #pragma unroll
         for (int j = 0; j < G; ++j) {
           const int b = first + j;
-          const uint32_t ob = b < 4 ? (lo >> (8 * b)) & 0xffu : (hi >> (8 * (b - 4))) & 0xffu;
           const uint32_t nb = b < 4 ? (nlo >> (8 * b)) & 0xffu : (nhi >> (8 * (b - 4))) & 0xffu;
-          io = io * kAlpha + (int)ob;
           in = in * kAlpha + (int)nb;
         }
-        delta += lookup(in) - lookup(io);
+        delta += lookup(in) - lds_u16(ws_base + 2u * (uint32_t)s);
       }
     }
     return delta;
@@ -139,14 +145,15 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
   unsigned char* wb = smem_raw + tab_bytes + (size_t)warp * ng_warp_bytes(max_len);
   uint8_t* text = wb;  // plain[i] at text[4 + i]
   uint16_t* occ = reinterpret_cast<uint16_t*>(wb + ng_text_stride(max_len));
-  uint16_t* start = reinterpret_cast<uint16_t*>(wb + ng_text_stride(max_len) +
-                                                ((2u * (uint32_t)max_len + 15u) & ~15u));
+  uint16_t* start = reinterpret_cast<uint16_t*>(wb + ng_text_stride(max_len) + ng_u16_bytes(max_len));
   uint32_t* cursor = reinterpret_cast<uint32_t*>(start + 32);
   // exact deltas of the current state already computed, keyed by the letter pair (a < b):
   // valid while dtag == epoch, and every accept starts a new epoch (a rejected proposal leaves
   // the state unchanged, so late in a climb almost every proposal is a cache hit)
   int* dcache = reinterpret_cast<int*>(cursor + 32);
   uint16_t* dtag = reinterpret_cast<uint16_t*>(dcache + 676);
+  // table score of every window of the current plaintext (ws[s] for the window starting at s)
+  uint16_t* ws = reinterpret_cast<uint16_t*>(reinterpret_cast<unsigned char*>(dcache) + kCacheBytes);
 
   NgState<G, SMEM_TAB> st;
   st.tab = p.table;
@@ -154,10 +161,10 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
   st.text_base = smem_addr(text);
   st.occ = occ;
   st.start = start;
+  st.ws_base = smem_addr(ws);
 
   const int64_t stride = (int64_t)gridDim.x * kNgWarps;
   const uint32_t climbings = (uint32_t)p.climbings;
-  const int g8 = lane >> 3, sl = lane & 7;
 
   for (int64_t w = (int64_t)blockIdx.x * kNgWarps + warp; w < p.n_workers; w += stride) {
     const int32_t cid = p.cipher_of[w];
@@ -196,7 +203,9 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
         int idx = 0;
 #pragma unroll
         for (int j = 0; j < G; ++j) idx = idx * kAlpha + text[4 + s + j];
-        part += st.lookup(idx);
+        const int v = st.lookup(idx);
+        ws[s] = (uint16_t)v;
+        part += v;
       }
       // partial sums < 32 x ceil(n/32) x 65535 < 2^31 for n <= 32768
       score = (int64_t)(int)__reduce_add_sync(kFull, (uint32_t)part);
@@ -213,29 +222,53 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
     win.o = 0;
     win.refill(lane);
 
-    // group-of-W evaluation of the interchange (a, b): every lane of the group gets the sum
-    auto eval_group = [&](uint32_t a, uint32_t b) -> int {
-      const int xa = __shfl_sync(kFull, pinv, (int)a), xb = __shfl_sync(kFull, pinv, (int)b);
+    // Exact deltas of up to four interchanges (lane g < 4 holds pair g in ga, gb; valid: it
+    // is a miss to compute) into the cache.  Their touched positions are concatenated and
+    // walked by all 32 lanes, so uneven letter frequencies do not idle lanes.
+    auto eval_misses = [&](uint32_t ga, uint32_t gb, bool valid) {
+      const int xa = __shfl_sync(kFull, pinv, (int)ga), xb = __shfl_sync(kFull, pinv, (int)gb);
       const int sa = start[xa], na = (int)start[xa + 1] - sa;
       const int sb = start[xb], nb = (int)start[xb + 1] - sb;
-      const uint32_t arep = a * 0x01010101u, brep = b * 0x01010101u;
-      const int key = (int)(min(a, b) * kAlpha + max(a, b));
-      const bool hit = a == b || dtag[key] == epoch;  // a == b: no interchange, delta 0
-      const int m = hit ? 0 : na + nb;
-      walks += __popc(__ballot_sync(kFull, !hit && sl == 0));
-      int d = 0;
-      for (int j = sl; j < m; j += 8) d += st.position_delta(st.touched(j, sa, na, sb), arep, brep);
-      d += __shfl_xor_sync(kFull, d, 1);
-      d += __shfl_xor_sync(kFull, d, 2);
-      d += __shfl_xor_sync(kFull, d, 4);
-      if (hit) {
-        d = a == b ? 0 : dcache[key];
-      } else if (sl == 0) {
-        dcache[key] = d;
+      const int cnt = valid ? na + nb : 0;
+      int incl = cnt;
+      {
+        const int u1 = __shfl_up_sync(kFull, incl, 1);
+        if (lane >= 1) incl += u1;
+        const int u2 = __shfl_up_sync(kFull, incl, 2);
+        if (lane >= 2) incl += u2;
+      }
+      const int e0 = __shfl_sync(kFull, incl, 0), e1 = __shfl_sync(kFull, incl, 1);
+      const int e2 = __shfl_sync(kFull, incl, 2), total = __shfl_sync(kFull, incl, 3);
+      const uint32_t pk1 = (uint32_t)sa | ((uint32_t)na << 16);
+      const uint32_t pk2 = (uint32_t)sb | (ga << 16) | (gb << 24);
+      walks += __popc(__ballot_sync(kFull, valid));
+      int d0 = 0, d1 = 0, d2 = 0, d3 = 0;
+      for (int jb = 0; jb < total; jb += 32) {
+        const int j = jb + lane;
+        const int g = (j >= e0) + (j >= e1) + (j >= e2);
+        const int pre = g == 0 ? 0 : g == 1 ? e0 : g == 2 ? e1 : e2;
+        const uint32_t q1 = __shfl_sync(kFull, pk1, g), q2 = __shfl_sync(kFull, pk2, g);
+        if (j < total) {
+          const uint32_t a = (q2 >> 16) & 0xffu, b = q2 >> 24;
+          const int v = st.position_delta(st.touched(j - pre, (int)(q1 & 0xffffu), (int)(q1 >> 16),
+                                                      (int)(q2 & 0xffffu)),
+                                          a * 0x01010101u, b * 0x01010101u);
+          d0 += g == 0 ? v : 0;
+          d1 += g == 1 ? v : 0;
+          d2 += g == 2 ? v : 0;
+          d3 += g == 3 ? v : 0;
+        }
+      }
+      d0 = (int)__reduce_add_sync(kFull, (uint32_t)d0);
+      d1 = (int)__reduce_add_sync(kFull, (uint32_t)d1);
+      d2 = (int)__reduce_add_sync(kFull, (uint32_t)d2);
+      d3 = (int)__reduce_add_sync(kFull, (uint32_t)d3);
+      if (valid) {
+        const int key = (int)(min(ga, gb) * kAlpha + max(ga, gb));
+        dcache[key] = lane == 0 ? d0 : lane == 1 ? d1 : lane == 2 ? d2 : d3;
         dtag[key] = (uint16_t)epoch;
       }
       __syncwarp();
-      return d;
     };
     auto eval_one = [&](uint32_t a, uint32_t b) -> int {
       const int xa = __shfl_sync(kFull, pinv, (int)a), xb = __shfl_sync(kFull, pinv, (int)b);
@@ -266,6 +299,20 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
         const int i = st.touched(j, sa, na, sb);
         text[4 + i] = (uint8_t)(j < na ? b : a);
       }
+      __syncwarp();
+      for (int j = lane; j < na + nb; j += 32) {  // windows holding a touched position
+        const int i = st.touched(j, sa, na, sb);
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+          const int s0 = i - (G - 1) + k;
+          if (s0 >= 0 && s0 + G <= st.n) {
+            int idx = 0;
+#pragma unroll
+            for (int q = 0; q < G; ++q) idx = idx * kAlpha + text[4 + s0 + q];
+            ws[s0] = (uint16_t)st.lookup(idx);
+          }
+        }
+      }
       if (lane == a) pinv = xb;
       if (lane == b) pinv = xa;
       if (++epoch == 0x10000u) {  // tags wrap: clear them
@@ -283,55 +330,94 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
 
     int last = -1;
     uint32_t t = 0, since = 0, next_check = 256;
-    bool dirty = false;
-    auto step = [&](uint32_t a, uint32_t b, int dd) -> bool {
-      if (a == b) return false;
-      const int d = dirty ? eval_one(a, b) : dd;
-      win.o += 2;
-      if (d > 0) {
-        accept((int)a, (int)b, d);
+    auto check_exit = [&]() {  // true: the climb is at a local optimum (early-exit mode)
+      if (!(p.flags & CCG_FLAG_EARLY_EXIT) || since < next_check) return false;
+      if (!improvable()) return true;
+      next_check *= 4;
+      return false;
+    };
+    while (t < climbings) {
+      if (win.o > 120) win.refill(lane);
+      // Round: up to 32 proposals, one per lane, paired exactly as in ccg_mas_dform.cu
+      // (aligned pairs, one redraw, shifted pairs; rng.py:81-89).  The cached deltas of the
+      // prefix before the first cache miss decide it: the first positive one is accepted,
+      // otherwise the prefix is rejected.  On a miss, the first four misses of the round are
+      // computed (one per 8-lane group) into the cache and the round is re-run from the
+      // first miss -- proposals never read the state, so computing ahead is exact.
+      const uint32_t o = win.o;
+      const uint32_t pos = o + 2u * (uint32_t)lane;
+      const int src = (int)((pos >> 2) & 31u);
+      const uint32_t x0 = __shfl_sync(kFull, win.lo, src), x1 = __shfl_sync(kFull, win.hi, src);
+      const uint32_t wd = __funnelshift_r(x0, x1, (pos & 3u) * 8u);
+      const uint32_t c0 = wd & 0xffu, c1 = (wd >> 8) & 0xffu, c2 = (wd >> 16) & 0xffu;
+      const uint32_t nA = (128u - o) >> 1, nB = (127u - o) >> 1;
+      const uint32_t eqA = __ballot_sync(kFull, c0 == c1);
+      const uint32_t r0 = eqA ? (uint32_t)(__ffs(eqA) - 1) : 32u;
+      uint32_t R;
+      bool seq = false;  // the round stopped at a pair that needs the sequential redraw path
+      if (r0 >= nA) {
+        R = min(nA, 32u);
+      } else {
+        const uint32_t c2r = __shfl_sync(kFull, c2, (int)r0), c0r = __shfl_sync(kFull, c0, (int)r0);
+        if (r0 >= nB || c2r == c0r) {
+          R = r0;
+          seq = true;
+        } else {
+          const uint32_t eqB = __ballot_sync(kFull, c1 == c2) & ~((2u << r0) - 1u);
+          R = eqB ? (uint32_t)(__ffs(eqB) - 1) : 32u;
+          R = min(R, nB);
+        }
+      }
+      if (R > climbings - t) {
+        R = climbings - t;
+        seq = false;
+      }
+      const uint32_t j = (uint32_t)lane;
+      const uint32_t pa = j <= r0 ? c0 : c1, pb = j < r0 ? c1 : c2;
+      const int key = (int)(min(pa, pb) * kAlpha + max(pa, pb));
+      const bool in = j < R;
+      const bool hit = in && dtag[key] == epoch;
+      const int d = hit ? dcache[key] : 0;
+      const uint32_t miss = __ballot_sync(kFull, in && !hit);
+      const uint32_t f = miss ? (uint32_t)(__ffs(miss) - 1) : R;
+      const uint32_t acc = __ballot_sync(kFull, j < f && d > 0);
+      if (acc) {
+        const uint32_t k = (uint32_t)(__ffs(acc) - 1);
+        const int ak = __shfl_sync(kFull, (int)pa, (int)k), bk = __shfl_sync(kFull, (int)pb, (int)k);
+        const int dk = __shfl_sync(kFull, d, (int)k);
+        t += k;
+        win.o += 2u * (k + 1u) + (k + 1u > r0 ? 1u : 0u);
+        accept(ak, bk, dk);
         last = (int)t;
-        dirty = true;
         since = 0;
         next_check = 256;
-      } else {
-        ++since;
-      }
-      ++t;
-      return true;
-    };
-    while (t + 3 < climbings) {
-      if (win.o > 120) win.refill(lane);
-      uint32_t La, Lb;
-      win.peek8(La, Lb);
-      // group g takes pair g: bytes (2g, 2g+1) of La:Lb
-      const uint32_t Lg = g8 < 2 ? La : Lb;
-      const uint32_t ga = (Lg >> (16 * (g8 & 1))) & 0xffu, gb = (Lg >> (16 * (g8 & 1) + 8)) & 0xffu;
-      const int dg = eval_group(ga, gb);
-      const int d1 = __shfl_sync(kFull, dg, 0), d2 = __shfl_sync(kFull, dg, 8);
-      const int d3 = __shfl_sync(kFull, dg, 16), d4 = __shfl_sync(kFull, dg, 24);
-      const uint32_t a1 = La & 0xffu, b1 = (La >> 8) & 0xffu, a2 = (La >> 16) & 0xffu, b2 = La >> 24;
-      const uint32_t a3 = Lb & 0xffu, b3 = (Lb >> 8) & 0xffu, a4 = (Lb >> 16) & 0xffu, b4 = Lb >> 24;
-      const bool ok = a1 != b1 && a2 != b2 && a3 != b3 && a4 != b4;
-      if (ok && max(max(d1, d2), max(d3, d4)) <= 0) {
-        win.o += 8;
-        t += 4;
-        if (p.flags & CCG_FLAG_EARLY_EXIT) {
-          since += 4;
-          if (since >= next_check) {
-            if (!improvable()) break;
-            next_check *= 4;
-          }
-        }
+        ++t;
         continue;
       }
-      dirty = false;
-      if (!(step(a1, b1, d1) && step(a2, b2, d2) && step(a3, b3, d3) && step(a4, b4, d4))) {
-        int a, b;
-        win.pair(lane, a, b);  // a redraw is due (rng.py:81-89)
-        const int d = eval_one((uint32_t)a, (uint32_t)b);
-        if (d > 0) {
-          accept(a, b, d);
+      t += f;
+      since += f;
+      win.o += 2u * f + (f > r0 ? 1u : 0u);
+      if (f < R) {
+        // lane g < 4 takes the g-th miss of the round
+        uint32_t m = miss, mg = 32u;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const uint32_t q = m ? (uint32_t)(__ffs(m) - 1) : 32u;
+          if (g == lane) mg = q;
+          m &= m - 1u;
+        }
+        const int ga = __shfl_sync(kFull, (int)pa, (int)(mg & 31u));
+        const int gb = __shfl_sync(kFull, (int)pb, (int)(mg & 31u));
+        eval_misses((uint32_t)ga, (uint32_t)gb, mg < 32u);
+        continue;
+      }
+      if (check_exit()) break;
+      if (seq && t < climbings) {  // one try through the sequential redraw path
+        int a2, b2;
+        win.pair(lane, a2, b2);
+        const int d2 = eval_one((uint32_t)a2, (uint32_t)b2);
+        if (d2 > 0) {
+          accept(a2, b2, d2);
           last = (int)t;
           since = 0;
           next_check = 256;
@@ -339,24 +425,9 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
           ++since;
         }
         ++t;
-      }
-      if ((p.flags & CCG_FLAG_EARLY_EXIT) && since >= next_check) {
-        if (!improvable()) break;
-        next_check *= 4;
+        if (check_exit()) break;
       }
     }
-    const bool done = (p.flags & CCG_FLAG_EARLY_EXIT) && t + 3 < climbings;
-    while (!done && t < climbings) {
-      int a, b;
-      win.pair(lane, a, b);
-      const int d = eval_one((uint32_t)a, (uint32_t)b);
-      if (d > 0) {
-        accept(a, b, d);
-        last = (int)t;
-      }
-      ++t;
-    }
-
     if (lane < kAlpha && p.maps) p.maps[w * kAlpha + pinv] = (uint8_t)lane;
     if (lane == 0) {
       p.scores[w] = score;
@@ -388,7 +459,7 @@ cudaError_t launch_ng_w(cudaStream_t s, const MasNgramLaunch& p, int sm_count) {
 }
 
 // The largest block the shared-memory layout allows: 32 warps when a staged table is shared
-// by a whole SM, else 16, else 8 (more warps hide the table-lookup latency).
+// by a whole SM, else 16, 8 or 4 (more warps hide the table-lookup latency).
 template <int G, bool SMEM_TAB>
 cudaError_t launch_ng(cudaStream_t s, const MasNgramLaunch& p, int sm_count) {
   const size_t tab = SMEM_TAB ? (((size_t)pow26(G) * 2 + 15) & ~(size_t)15) : 0;
@@ -396,7 +467,8 @@ cudaError_t launch_ng(cudaStream_t s, const MasNgramLaunch& p, int sm_count) {
   if (SMEM_TAB && tab + 32 * wb <= 220 * 1024)  // one 32-warp block per SM shares the table
     return launch_ng_w<G, SMEM_TAB, 32>(s, p, sm_count);
   if (tab + 16 * wb <= 200 * 1024) return launch_ng_w<G, SMEM_TAB, 16>(s, p, sm_count);
-  return launch_ng_w<G, SMEM_TAB, 8>(s, p, sm_count);
+  if (tab + 8 * wb <= 200 * 1024) return launch_ng_w<G, SMEM_TAB, 8>(s, p, sm_count);
+  return launch_ng_w<G, SMEM_TAB, 4>(s, p, sm_count);
 }
 
 // ngrams.py:134-140 generalised to order G: one warp per text, int64 sum.
