@@ -89,36 +89,35 @@ struct NgState {
     const uint32_t w0 = lds_u32(wa), w1 = lds_u32(wa + 4), w2 = lds_u32(wa + 8);
     const uint32_t sh = (off & 3u) * 8u;
     const uint32_t lo = __funnelshift_r(w0, w1, sh), hi = __funnelshift_r(w1, w2, sh);
-    // byte j of (lo,hi) is plain[i - 3 + j]; the centre is byte 3
-    const uint32_t ma_lo = eq_bytes(lo, arep), mb_lo = eq_bytes(lo, brep);
-    const uint32_t ma_hi = eq_bytes(hi, arep), mb_hi = eq_bytes(hi, brep);
-    const uint32_t ea_lo = expand_mask(ma_lo), eb_lo = expand_mask(mb_lo);
-    const uint32_t ea_hi = expand_mask(ma_hi), eb_hi = expand_mask(mb_hi);
-    const uint32_t nlo = (lo & ~(ea_lo | eb_lo)) | (brep & ea_lo) | (arep & eb_lo);
-    const uint32_t nhi = (hi & ~(ea_hi | eb_hi)) | (brep & ea_hi) | (arep & eb_hi);
-    // touched bytes before the centre: bits of (ma|mb) in bytes 0..2 of lo
-    const uint32_t touched_lo = (ma_lo | mb_lo) >> 7;  // bit 8j set for touched byte j
+    // byte j of (lo,hi) is plain[i - 3 + j]; the centre is byte 3.  Bytes equal to a or b
+    // are exchanged by XOR with a^b.
+    const uint32_t m_lo = eq_bytes(lo, arep) | eq_bytes(lo, brep);
+    const uint32_t m_hi = eq_bytes(hi, arep) | eq_bytes(hi, brep);
+    const uint32_t abx = arep ^ brep;
+    const uint32_t nlo = lo ^ (expand_mask(m_lo) & abx), nhi = hi ^ (expand_mask(m_hi) & abx);
+    const uint32_t touched_lo = m_lo >> 7;  // bit 8j set for touched byte j
     int delta = 0;
-    // window k covers bytes 3-(G-1)+k .. 3+k (k = 0..G-1), start s = i-(G-1)+k
+    // window k covers bytes 3-(G-1)+k .. 3+k (k = 0..G-1), start s = i-(G-1)+k; it is
+    // counted here when no byte before the centre in it is touched (positions s .. i-1)
 #pragma unroll
     for (int k = 0; k < G; ++k) {
       const int s = i - (G - 1) + k;
       const int first = 3 - (G - 1) + k;  // first byte of the window
-      // no touched byte in [first, 3) (positions s .. i-1)
       uint32_t before = 0;
 #pragma unroll
       for (int j = first; j < 3; ++j) before |= touched_lo & (1u << (8 * j));
       const bool valid = s >= 0 && s + G <= n && before == 0;
-      if (valid) {
-        int in = 0;
+      int in = 0;
 #pragma unroll
-        for (int j = 0; j < G; ++j) {
-          const int b = first + j;
-          const uint32_t nb = b < 4 ? (nlo >> (8 * b)) & 0xffu : (nhi >> (8 * (b - 4))) & 0xffu;
-          in = in * kAlpha + (int)nb;
-        }
-        delta += lookup(in) - lds_u16(ws_base + 2u * (uint32_t)s);
+      for (int j = 0; j < G; ++j) {
+        const int b = first + j;
+        const uint32_t nb = b < 4 ? __byte_perm(nlo, 0u, 0x4440u + (uint32_t)b)
+                                  : __byte_perm(nhi, 0u, 0x4440u + (uint32_t)(b - 4));
+        in = in * kAlpha + (int)nb;
       }
+      // invalid windows read entry 0 and a neighbouring score; both are discarded
+      const int v = lookup(valid ? in : 0) - lds_u16(ws_base + 2u * (uint32_t)s);
+      delta += valid ? v : 0;
     }
     return delta;
   }
@@ -157,7 +156,9 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
 
   NgState<G, SMEM_TAB> st;
   st.tab = p.table;
-  st.tab_s = smem_addr(smem_raw);
+  // held in a register (an opaque copy: the compiler would otherwise rebuild the shared
+  // window address with uniform-datapath instructions at every lookup)
+  asm volatile("mov.u32 %0, %1;" : "=r"(st.tab_s) : "r"(smem_addr(smem_raw)));
   st.text_base = smem_addr(text);
   st.occ = occ;
   st.start = start;
@@ -223,8 +224,9 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
     win.refill(lane);
 
     // Exact deltas of up to four interchanges (lane g < 4 holds pair g in ga, gb; valid: it
-    // is a miss to compute) into the cache.  Their touched positions are concatenated and
-    // walked by all 32 lanes, so uneven letter frequencies do not idle lanes.
+    // is a miss to compute) into the cache.  The warp's lanes are split between the four
+    // walks in proportion to their touched-position counts (at least one lane each), so
+    // uneven letter frequencies do not idle lanes.
     auto eval_misses = [&](uint32_t ga, uint32_t gb, bool valid) {
       const int xa = __shfl_sync(kFull, pinv, (int)ga), xb = __shfl_sync(kFull, pinv, (int)gb);
       const int sa = start[xa], na = (int)start[xa + 1] - sa;
@@ -237,32 +239,28 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
         const int u2 = __shfl_up_sync(kFull, incl, 2);
         if (lane >= 2) incl += u2;
       }
-      const int e0 = __shfl_sync(kFull, incl, 0), e1 = __shfl_sync(kFull, incl, 1);
-      const int e2 = __shfl_sync(kFull, incl, 2), total = __shfl_sync(kFull, incl, 3);
-      const uint32_t pk1 = (uint32_t)sa | ((uint32_t)na << 16);
-      const uint32_t pk2 = (uint32_t)sb | (ga << 16) | (gb << 24);
+      const int total = max(__shfl_sync(kFull, incl, 3), 1);
+      // first lane of walk g: floor(29 * positions before g / total) + g (< 32 for g = 3
+      // whenever walk 3 has positions)
+      const int first = (29 * (incl - cnt)) / total + lane;
+      const int f1 = __shfl_sync(kFull, first, 1), f2 = __shfl_sync(kFull, first, 2);
+      const int f3 = __shfl_sync(kFull, first, 3);
+      const int g = (lane >= f1) + (lane >= f2) + (lane >= f3);
+      const int lo_lane = g == 0 ? 0 : g == 1 ? f1 : g == 2 ? f2 : f3;
+      const int hi_lane = g == 0 ? f1 : g == 1 ? f2 : g == 2 ? f3 : 32;
+      const int msa = __shfl_sync(kFull, sa, g), mna = __shfl_sync(kFull, na, g);
+      const int msb = __shfl_sync(kFull, sb, g), mcnt = __shfl_sync(kFull, cnt, g);
+      const uint32_t ma = (uint32_t)__shfl_sync(kFull, (int)ga, g);
+      const uint32_t mb = (uint32_t)__shfl_sync(kFull, (int)gb, g);
+      const uint32_t arep = ma * 0x01010101u, brep = mb * 0x01010101u;
       walks += __popc(__ballot_sync(kFull, valid));
-      int d0 = 0, d1 = 0, d2 = 0, d3 = 0;
-      for (int jb = 0; jb < total; jb += 32) {
-        const int j = jb + lane;
-        const int g = (j >= e0) + (j >= e1) + (j >= e2);
-        const int pre = g == 0 ? 0 : g == 1 ? e0 : g == 2 ? e1 : e2;
-        const uint32_t q1 = __shfl_sync(kFull, pk1, g), q2 = __shfl_sync(kFull, pk2, g);
-        if (j < total) {
-          const uint32_t a = (q2 >> 16) & 0xffu, b = q2 >> 24;
-          const int v = st.position_delta(st.touched(j - pre, (int)(q1 & 0xffffu), (int)(q1 >> 16),
-                                                      (int)(q2 & 0xffffu)),
-                                          a * 0x01010101u, b * 0x01010101u);
-          d0 += g == 0 ? v : 0;
-          d1 += g == 1 ? v : 0;
-          d2 += g == 2 ? v : 0;
-          d3 += g == 3 ? v : 0;
-        }
-      }
-      d0 = (int)__reduce_add_sync(kFull, (uint32_t)d0);
-      d1 = (int)__reduce_add_sync(kFull, (uint32_t)d1);
-      d2 = (int)__reduce_add_sync(kFull, (uint32_t)d2);
-      d3 = (int)__reduce_add_sync(kFull, (uint32_t)d3);
+      int d = 0;
+      for (int j = lane - lo_lane; j < mcnt; j += hi_lane - lo_lane)
+        d += st.position_delta(st.touched(j, msa, mna, msb), arep, brep);
+      const int d0 = (int)__reduce_add_sync(kFull, (uint32_t)(g == 0 ? d : 0));
+      const int d1 = (int)__reduce_add_sync(kFull, (uint32_t)(g == 1 ? d : 0));
+      const int d2 = (int)__reduce_add_sync(kFull, (uint32_t)(g == 2 ? d : 0));
+      const int d3 = (int)__reduce_add_sync(kFull, (uint32_t)(g == 3 ? d : 0));
       if (valid) {
         const int key = (int)(min(ga, gb) * kAlpha + max(ga, gb));
         dcache[key] = lane == 0 ? d0 : lane == 1 ? d1 : lane == 2 ? d2 : d3;
