@@ -240,14 +240,17 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
         if (lane >= 2) incl += u2;
       }
       const int total = max(__shfl_sync(kFull, incl, 3), 1);
-      // first lane of walk g: floor(29 * positions before g / total) + g (< 32 for g = 3
-      // whenever walk 3 has positions)
-      const int first = (29 * (incl - cnt)) / total + lane;
+      // first lane of walk g: ~floor(29 * positions before g / total) + g, monotone with
+      // steps >= 1 and < 32 for g = 3 (any such split is exact; it only balances the work)
+      float rt;
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rt) : "f"((float)total));
+      const int first = min((int)(29.0f * (float)(incl - cnt) * rt), 28) + lane;
       const int f1 = __shfl_sync(kFull, first, 1), f2 = __shfl_sync(kFull, first, 2);
       const int f3 = __shfl_sync(kFull, first, 3);
+      const int nxt = __shfl_down_sync(kFull, first, 1);
       const int g = (lane >= f1) + (lane >= f2) + (lane >= f3);
-      const int lo_lane = g == 0 ? 0 : g == 1 ? f1 : g == 2 ? f2 : f3;
-      const int hi_lane = g == 0 ? f1 : g == 1 ? f2 : g == 2 ? f3 : 32;
+      const int lo_lane = __shfl_sync(kFull, first, g);
+      const int hi_lane = __shfl_sync(kFull, lane == 3 ? 32 : nxt, g);
       const int msa = __shfl_sync(kFull, sa, g), mna = __shfl_sync(kFull, na, g);
       const int msb = __shfl_sync(kFull, sb, g), mcnt = __shfl_sync(kFull, cnt, g);
       const uint32_t ma = (uint32_t)__shfl_sync(kFull, (int)ga, g);
