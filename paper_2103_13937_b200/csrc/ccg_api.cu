@@ -66,6 +66,15 @@ struct ccg_ctx {
     *out = b.first;
     return CCG_OK;
   }
+  // a zeroed worker ticket counter for the next climb launch (WorkerTickets)
+  int tickets(unsigned long long** out) {
+    void* t = nullptr;
+    int rc = buf(15, sizeof(unsigned long long), &t);
+    if (rc) return rc;
+    CCG_CUDA(cudaMemsetAsync(t, 0, sizeof(unsigned long long), stream));
+    *out = (unsigned long long*)t;
+    return CCG_OK;
+  }
 };
 
 namespace {
@@ -533,6 +542,7 @@ static int mas_launch(ccg_ctx* ctx, const ccg_mas_climb_args* a, int64_t max_len
   p.tries_done = a->tries_done;
   p.flags = a->flags;
   p.accepts = a->accepts;
+  if (int rc = ctx->tickets(&p.tickets)) return rc;
   ctx->launches++;
   cudaError_t e;
   const uint32_t kern = a->flags & CCG_FLAG_KERNEL_MASK;
@@ -703,6 +713,7 @@ static int ngram_launch(ccg_ctx* ctx, const ccg_mas_ngram_args* a, int64_t max_l
   p.tries_done = a->tries_done;
   p.computed = a->computed;
   p.flags = a->flags;
+  if (int rc = ctx->tickets(&p.tickets)) return rc;
   ctx->launches++;
   cudaError_t e = launch_mas_ngram_climb(ctx->stream, p, ctx->sm_count);
   if (e != cudaSuccess) return cuda_fail(e, "mas_ngram kernel");
@@ -1032,6 +1043,7 @@ static int sct_launch(ccg_ctx* ctx, const ccg_sct_climb_args* a, int64_t n) {
   p.last_accept = a->last_accept;
   p.tries_done = a->tries_done;
   p.flags = a->flags;
+  if (int rc = ctx->tickets(&p.tickets)) return rc;
   ctx->launches++;
   cudaError_t e = launch_sct_climb(ctx->stream, p, plan, ctx->sm_count);
   if (e != cudaSuccess) return cuda_fail(e, "sct_climb kernel");

@@ -35,6 +35,7 @@ struct MasLaunch {
   uint32_t flags;
   int64_t* accepts;
   const void* init;  // D-form: per-ciphertext initial states (dform_init_kernel), or NULL
+  unsigned long long* tickets;  // worker ticket counter, zero at launch (or NULL: static stride)
 };
 
 // MAS climb with an order-G n-gram table (ccg_mas_ngram.cu).
@@ -57,6 +58,7 @@ struct MasNgramLaunch {
   int64_t* tries_done;
   uint32_t flags;
   int64_t* computed;
+  unsigned long long* tickets;  // worker ticket counter, zero at launch (or NULL)
 };
 
 // Deterministic best-neighbour MAS (ccg_mas_det.cu): one job = one (ciphertext, restart).
@@ -110,7 +112,28 @@ struct SctLaunch {
   int64_t* last_accept;
   int64_t* tries_done;
   uint32_t flags;
+  unsigned long long* tickets;  // worker ticket counter, zero at launch (or NULL)
 };
+
+#ifdef __CUDACC__
+// Worker scheduling for the persistent climb kernels: a warp's first worker is static
+// (warp index), later ones are tickets from a global counter zeroed before the launch, so a
+// warp that finishes early takes the next worker and the launch's tail is about one worker
+// long.  Outputs are per worker, so the assignment does not change any result.  Without a
+// counter the warps stride statically.
+struct WorkerTickets {
+  unsigned long long* ctr;
+  int64_t n_warps;  // warps in the grid: the static first workers are 0 .. n_warps-1
+  __device__ __forceinline__ int64_t next(int64_t w, int lane) const {
+    if (!ctr) return w + n_warps;
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(ctr, 1ULL);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    return n_warps + (int64_t)t;
+  }
+};
+
+#endif
 
 void build_sum_plan(int64_t n_terms, SumPlan* plan);
 

@@ -132,7 +132,8 @@ __global__ void __launch_bounds__(kMasWarps * 32, 4)
   const int64_t stride = (int64_t)gridDim.x * kMasWarps;
   const uint32_t climbings = (uint32_t)p.climbings;
 
-  for (int64_t w = (int64_t)blockIdx.x * kMasWarps + warp; w < p.n_workers; w += stride) {
+  const WorkerTickets tk{p.tickets, stride};
+  for (int64_t w = (int64_t)blockIdx.x * kMasWarps + warp; w < p.n_workers; w = tk.next(w, lane)) {
     const int32_t cid = p.cipher_of[w];
     const int64_t off = p.offsets[cid], n = p.offsets[cid + 1] - off;
     build_counts(C, p.ciphers + off, n, lane);

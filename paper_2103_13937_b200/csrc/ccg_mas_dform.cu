@@ -206,7 +206,8 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
   const int y = lane < kAlpha ? lane : 0;  // the column this lane owns in N updates
   const uint32_t ks_s = smem_addr(B.KS);
 
-  for (int64_t w = (int64_t)blockIdx.x * kDWarps + warp; w < p.n_workers; w += stride) {
+  const WorkerTickets tk{p.tickets, stride};
+  for (int64_t w = (int64_t)blockIdx.x * kDWarps + warp; w < p.n_workers; w = tk.next(w, lane)) {
     const int32_t cid = p.cipher_of[w];
     const int64_t off = p.offsets[cid], n = p.offsets[cid + 1] - off;
     const uint8_t* text = p.ciphers + off;

@@ -167,7 +167,8 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
   const int64_t stride = (int64_t)gridDim.x * kNgWarps;
   const uint32_t climbings = (uint32_t)p.climbings;
 
-  for (int64_t w = (int64_t)blockIdx.x * kNgWarps + warp; w < p.n_workers; w += stride) {
+  const WorkerTickets tk{p.tickets, stride};
+  for (int64_t w = (int64_t)blockIdx.x * kNgWarps + warp; w < p.n_workers; w = tk.next(w, lane)) {
     const int32_t cid = p.cipher_of[w];
     const int64_t off = p.offsets[cid];
     const int n = (int)(p.offsets[cid + 1] - off);

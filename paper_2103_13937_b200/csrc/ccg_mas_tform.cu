@@ -81,7 +81,8 @@ __global__ void __launch_bounds__(kTWarps * 32) mas_climb_tform_kernel(const Mas
     }
   };
 
-  for (int64_t w = (int64_t)blockIdx.x * kTWarps + warp; w < p.n_workers; w += stride) {
+  const WorkerTickets tk{p.tickets, stride};
+  for (int64_t w = (int64_t)blockIdx.x * kTWarps + warp; w < p.n_workers; w = tk.next(w, lane)) {
     const int32_t cid = p.cipher_of[w];
     const int64_t off = p.offsets[cid], n = p.offsets[cid + 1] - off;
     const uint8_t* text = p.ciphers + off;

@@ -353,7 +353,8 @@ __global__ void __launch_bounds__(kSctWarps * 32, 4)
   const int kmax = p.k;  // keys_out stride
   const int64_t stride = (int64_t)gridDim.x * kSctWarps;
 
-  for (int64_t w = (int64_t)blockIdx.x * kSctWarps + warp; w < p.n_workers; w += stride) {
+  const WorkerTickets tk{p.tickets, stride};
+  for (int64_t w = (int64_t)blockIdx.x * kSctWarps + warp; w < p.n_workers; w = tk.next(w, lane)) {
     const int32_t cid = p.cipher_of[w];
     const int k = p.key_lengths ? p.key_lengths[w] : kmax;
     if (p.key_lengths) ev.set_k(k, lane);
