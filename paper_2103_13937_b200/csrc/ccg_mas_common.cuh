@@ -107,6 +107,64 @@ struct ByteWindow {
   __device__ __forceinline__ uint64_t position() const { return base + o; }
 };
 
+// 256 draws of one stream as letters int(u*26), one byte each, in two halves: lane L holds
+// draws base+4L .. base+4L+3 in `A` and base+128+4L .. +3 in `B`.  A round that starts at
+// offset o < 128 reads at most 66 draws from o on, so it always finds its 32 pairs in the
+// window (a 128-draw window truncates about a third of the rounds); when o passes 128 the
+// halves shift by one Philox block per lane.
+struct ByteWindow2 {
+  const uint64_t* key;
+  uint64_t base;    // stream index of draw 0 of half A (multiple of 4)
+  uint32_t A, B;
+  uint32_t o;       // window offset of the next draw (0 .. 255)
+  uint32_t rk = 0;  // shared address of precomputed round keys (philox_round_keys), or 0
+
+  __device__ __forceinline__ uint32_t letters(uint64_t block) const {
+    uint64_t v0, v1, v2, v3;
+    if (rk)
+      philox4x64_10_rk(rk, block + 1, v0, v1, v2, v3);
+    else
+      philox4x64_10(__ldg(key), __ldg(key + 1), block + 1, v0, v1, v2, v3);
+    return int_below_tiny(v0, 26) | (int_below_tiny(v1, 26) << 8) |
+           (int_below_tiny(v2, 26) << 16) | (int_below_tiny(v3, 26) << 24);
+  }
+  __device__ __forceinline__ void start(uint64_t pos, int lane) {
+    base = pos & ~3ULL;
+    o = (uint32_t)(pos & 3);
+    A = letters((base >> 2) + (uint64_t)lane);
+    B = letters((base >> 2) + 32 + (uint64_t)lane);
+  }
+  __device__ __forceinline__ void advance(int lane) {
+    base += 128;
+    o -= 128;
+    A = B;
+    B = letters((base >> 2) + 32 + (uint64_t)lane);
+  }
+  // Lane j's three letters at draws o+2j .. o+2j+2 (o < 128; byte 0 = draw o+2j).  The words
+  // a round needs span 18 < 32 lanes, so each source lane offers the one half it is asked for.
+  __device__ __forceinline__ uint32_t round_letters(int lane) const {
+    const uint32_t src = (uint32_t)lane >= (o >> 2) ? A : B;
+    const uint32_t pos = o + 2u * (uint32_t)lane;
+    const int w = (int)(pos >> 2);
+    const uint32_t x0 = __shfl_sync(kFull, src, w & 31), x1 = __shfl_sync(kFull, src, (w + 1) & 31);
+    return __funnelshift_r(x0, x1, (pos & 3u) * 8u);
+  }
+  __device__ __forceinline__ int next(int lane) {
+    if (o > 255u) advance(lane);
+    const uint32_t x = __shfl_sync(kFull, o < 128u ? A : B, (int)((o >> 2) & 31u));
+    const int v = (int)((x >> ((o & 3u) * 8u)) & 0xffu);
+    ++o;
+    return v;
+  }
+  // rng.py:81-89 next_distinct_pair(26)
+  __device__ __forceinline__ void pair(int lane, int& a, int& b) {
+    a = next(lane);
+    b = next(lane);
+    while (b == a) b = next(lane);
+  }
+  __device__ __forceinline__ uint64_t position() const { return base + o; }
+};
+
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }

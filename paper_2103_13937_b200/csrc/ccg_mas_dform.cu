@@ -232,14 +232,12 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
     }
 
     int pv = lane < kAlpha ? lane : 0;  // pi(lane): cipher letter -> plaintext letter
-    ByteWindow win;
+    ByteWindow2 win;
     win.key = p.keys + 2 * w;
     philox_round_keys(W.rk, __ldg(win.key), __ldg(win.key + 1), lane);
     __syncwarp();
     win.rk = smem_addr(W.rk);
-    win.base = p.skips ? p.skips[w] : 0;
-    win.o = 0;
-    win.refill(lane);
+    win.start(p.skips ? p.skips[w] : 0, lane);
 
     // commit the interchange a<->b (mas.py:237-243)
     auto accept = [&](int a, int b, int d) {
@@ -305,36 +303,29 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
     uint32_t t = 0;
     bool done = EARLY && optimum();
     while (!done && t < climbings) {
-      if (win.o > 120u) win.refill(lane);
+      if (win.o >= 128u) win.advance(lane);  // o <= 128 at every round start
       const uint32_t o = win.o;
       // Lane j reads letters c0, c1, c2 = L[o+2j], L[o+2j+1], L[o+2j+2].  Pairs j < r0 are
       // aligned (c0, c1); r0 is the first pair needing a redraw (c0 == c1); its partner is
       // c2 of lane r0 unless that equals c0 too; the pairs after it are shifted by one draw
       // (c1, c2) up to the next redraw.  rng.py:81-89 exactly.
-      const uint32_t pos = o + 2u * (uint32_t)lane;
-      const int src = (int)((pos >> 2) & 31u);
-      const uint32_t x0 = __shfl_sync(kFull, win.lo, src), x1 = __shfl_sync(kFull, win.hi, src);
-      const uint32_t wd = __funnelshift_r(x0, x1, (pos & 3u) * 8u);
+      const uint32_t wd = win.round_letters(lane);
       const int c0 = (int)(wd & 0xffu), c1 = (int)((wd >> 8) & 0xffu), c2 = (int)((wd >> 16) & 0xffu);
-      const uint32_t nA = (128u - o) >> 1;  // pairs whose two letters are in the window
-      const uint32_t nB = (127u - o) >> 1;  // shifted pairs / redraw partners in the window
+      // (o <= 128, so all 32 pairs and their redraw partners lie in the 256-draw window)
       const uint32_t eqA = __ballot_sync(kFull, c0 == c1);
       const uint32_t r0 = eqA ? (uint32_t)(__ffs(eqA) - 1) : 32u;
-      uint32_t R;          // pairs in this round
+      uint32_t R = 32u;    // pairs in this round
       bool seq = false;    // the round stopped at a pair that needs the sequential path
-      if (r0 >= nA) {
-        R = min(nA, 32u);
-      } else {
+      if (r0 < 32u) {
         const int c2r = __shfl_sync(kFull, c2, (int)r0), c0r = __shfl_sync(kFull, c0, (int)r0);
-        if (r0 >= nB || c2r == c0r) {
+        if (c2r == c0r) {
           R = r0;
           seq = true;
         } else {
-          const uint32_t eqB = __ballot_sync(kFull, c1 == c2) & ~((2u << r0) - 1u);
-          R = eqB ? (uint32_t)(__ffs(eqB) - 1) : 32u;
-          R = min(R, nB);
           // a second redraw ends the round; the next round starts at that pair, which it
           // handles as its first-segment redraw (no sequential try needed)
+          const uint32_t eqB = __ballot_sync(kFull, c1 == c2) & ~((2u << r0) - 1u);
+          if (eqB) R = (uint32_t)(__ffs(eqB) - 1);
         }
       }
       if (R > climbings - t) {

@@ -218,11 +218,9 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
     int64_t walks = 0;  // deltas computed by a position walk (the rest came from the cache)
     __syncwarp();
 
-    ByteWindow win;
+    ByteWindow2 win;
     win.key = p.keys + 2 * w;
-    win.base = p.skips ? p.skips[w] : 0;
-    win.o = 0;
-    win.refill(lane);
+    win.start(p.skips ? p.skips[w] : 0, lane);
 
     // Exact deltas of up to four interchanges (lane g < 4 holds pair g in ga, gb; valid: it
     // is a miss to compute) into the cache.  The warp's lanes are split between the four
@@ -339,7 +337,7 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
       return false;
     };
     while (t < climbings) {
-      if (win.o > 120) win.refill(lane);
+      if (win.o >= 128u) win.advance(lane);  // o <= 128 at every round start
       // Round: up to 32 proposals, one per lane, paired exactly as in ccg_mas_dform.cu
       // (aligned pairs, one redraw, shifted pairs; rng.py:81-89).  The cached deltas of the
       // prefix before the first cache miss decide it: the first positive one is accepted,
@@ -347,27 +345,23 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
       // computed (one per 8-lane group) into the cache and the round is re-run from the
       // first miss -- proposals never read the state, so computing ahead is exact.
       const uint32_t o = win.o;
-      const uint32_t pos = o + 2u * (uint32_t)lane;
-      const int src = (int)((pos >> 2) & 31u);
-      const uint32_t x0 = __shfl_sync(kFull, win.lo, src), x1 = __shfl_sync(kFull, win.hi, src);
-      const uint32_t wd = __funnelshift_r(x0, x1, (pos & 3u) * 8u);
+      const uint32_t wd = win.round_letters(lane);
       const uint32_t c0 = wd & 0xffu, c1 = (wd >> 8) & 0xffu, c2 = (wd >> 16) & 0xffu;
-      const uint32_t nA = (128u - o) >> 1, nB = (127u - o) >> 1;
+      // (o <= 128, so all 32 pairs and their redraw partners lie in the 256-draw window)
       const uint32_t eqA = __ballot_sync(kFull, c0 == c1);
       const uint32_t r0 = eqA ? (uint32_t)(__ffs(eqA) - 1) : 32u;
-      uint32_t R;
-      bool seq = false;  // the round stopped at a pair that needs the sequential redraw path
-      if (r0 >= nA) {
-        R = min(nA, 32u);
-      } else {
+      uint32_t R = 32u;    // pairs in this round
+      bool seq = false;    // the round stopped at a pair that needs the sequential path
+      if (r0 < 32u) {
         const uint32_t c2r = __shfl_sync(kFull, c2, (int)r0), c0r = __shfl_sync(kFull, c0, (int)r0);
-        if (r0 >= nB || c2r == c0r) {
+        if (c2r == c0r) {
           R = r0;
           seq = true;
         } else {
+          // a second redraw ends the round; the next round starts at that pair, which it
+          // handles as its first-segment redraw (no sequential try needed)
           const uint32_t eqB = __ballot_sync(kFull, c1 == c2) & ~((2u << r0) - 1u);
-          R = eqB ? (uint32_t)(__ffs(eqB) - 1) : 32u;
-          R = min(R, nB);
+          if (eqB) R = (uint32_t)(__ffs(eqB) - 1);
         }
       }
       if (R > climbings - t) {
