@@ -39,13 +39,19 @@ constexpr int kSctWarps = 8;
 // (one Philox4x64-10 block per lane per refill, rng.py:68-75), so a scalar draw is one
 // broadcast 64-bit shared load.  Every SCT bound is < 2^11 (100, hops, k <= 64, ...), so
 // int(u*bound) uses the single-product exact conversion (ccg_rng.cuh int_below_small).
+__device__ __noinline__ int slow_below(uint64_t m, uint32_t bound) {
+  return (int)int_below_small(m << 11, bound);
+}
+
 struct Draws {
   const uint64_t* key;  // &keys[2*w] (global; re-read at refill)
   uint32_t win;         // shared address of the 128-slot window; slot j holds draw base+j >> 11
   uint64_t base;        // stream index of window slot 0 (multiple of 4)
   uint32_t o;           // window slot of the next draw
 
-  __device__ __forceinline__ void refill(int lane) {
+  // out of line: one copy of the Philox block instead of one per draw site (the climb loop
+  // was instruction-fetch bound with it inlined everywhere)
+  __device__ __noinline__ void refill(int lane) {
     base += o & ~3u;
     o &= 3u;
     uint64_t v0, v1, v2, v3;
@@ -77,7 +83,7 @@ struct Draws {
     ++o;
     const uint64_t P = m * (uint64_t)bound;
     if (((P >> 10) & ((1ULL << 43) - 1)) != ((1ULL << 43) - 1)) return (int)(P >> 53);
-    return (int)int_below_small(m << 11, bound);
+    return slow_below(m, bound);
   }
   // rng.py:81-89
   __device__ __forceinline__ void pair(uint32_t bound, int lane, int& a, int& b) {
@@ -372,19 +378,25 @@ __global__ void __launch_bounds__(kSctWarps * 32, 4)
       const int j = d.below((uint32_t)(i + 1), lane);
       key.swap_pos(i, j, lane);
     }
-    double score = ev.score(key, ws.txt, ws.colstart, ws.plain, logs, lane);
-    int64_t last = -1, t = 0;
+    // t = -1 scores the start key (sct.py:157); one call site keeps a single inlined copy of
+    // the evaluator in the loop (the kernel is instruction-fetch sensitive)
+    double score = 0.0;
+    int64_t last = -1, t = -1;
     for (; t < p.climbings; ++t) {
-      const int u = d.below(100u, lane);
       Key cand = key;
-      if (u < p.p1)
-        op_element_swaps(cand, d, k, p.op1_hop, lane);
-      else if (u < p.p2)
-        op_block_swaps(cand, d, k, p.op2_hop, lane);
-      else
-        op_block_shift(cand, d, k, lane);
+      if (t >= 0) {
+        const int u = d.below(100u, lane);
+        if (u < p.p1)
+          op_element_swaps(cand, d, k, p.op1_hop, lane);
+        else if (u < p.p2)
+          op_block_swaps(cand, d, k, p.op2_hop, lane);
+        else
+          op_block_shift(cand, d, k, lane);
+      }
       const double cs = ev.score(cand, ws.txt, ws.colstart, ws.plain, logs, lane);
-      if (cs > score) {
+      if (t < 0) {
+        score = cs;
+      } else if (cs > score) {
         key = cand;
         score = cs;
         last = t;

@@ -138,7 +138,7 @@ def c3(args):
     l3 = cc.build_log_ngram_table(cc.build_ngram_table_from_corpus(corpus_text(), 3))
     corpus = G.corpus()
     n_c = 1000
-    W, K = (8, 1000) if args.quick else (32, 1000)
+    W, K = (8, 1000) if args.quick else (32, 15_000)  # climbings 15,000
     ks = list(range(5, 21))
     ciphers, plains, kofc = [], [], []
     for i in range(n_c):
