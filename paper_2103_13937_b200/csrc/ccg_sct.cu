@@ -71,18 +71,16 @@ struct Draws {
     o = (uint32_t)(pos & 3);
   }
   __device__ __forceinline__ uint64_t position() const { return base + o; }
-  // rng.py:77-79: int(u * bound) for the next draw, 1 <= bound < 2^11.  With m = x >> 11 and
-  // P = m * bound (< 2^64, exact), the double product rounds P * 2^-53 to 53 bits; truncation
-  // can differ from P >> 53 only when the fraction P mod 2^53 lies within 2^10 of 2^53 (the
-  // rounding step is at most 2^(bitlen(P) - 54) <= 2^10), so the exact test of
-  // int_below_small runs only then.
+  // rng.py:77-79: int(u * bound) for the next draw, 1 <= bound < 2^11, m = x >> 11.  The top
+  // 32 bits of the draw give it with one 32x32 product unless the product's low word is
+  // within `bound` of wrapping (probability < 2^-21), when the exact 64-bit conversion runs.
   __device__ __forceinline__ int below(uint32_t bound, int lane) {
     if (o > 127u) refill(lane);
     uint64_t m;
     asm volatile("ld.shared.u64 %0, [%1];" : "=l"(m) : "r"(win + 8u * o));
     ++o;
-    const uint64_t P = m * (uint64_t)bound;
-    if (((P >> 10) & ((1ULL << 43) - 1)) != ((1ULL << 43) - 1)) return (int)(P >> 53);
+    const uint64_t A = (uint64_t)(uint32_t)(m >> 21) * bound;
+    if ((uint32_t)A < 0u - bound) return (int)(A >> 32);
     return slow_below(m, bound);
   }
   // rng.py:81-89
@@ -129,6 +127,7 @@ struct SlotPlan {
   int leaf;       // leaf id handled by this lane's 8-lane group in this slot (-1: none)
   int count;      // strided terms per accumulator (len/8, 0 for a sequential leaf)
   int tail;       // terms added in order after the tree
+  int mtail;      // the largest tail in the warp (warp-uniform loop bound)
   int p0;         // plaintext position of this lane's first strided term
   int pt;         // position of the first tail term
 };
@@ -172,6 +171,7 @@ struct Evaluator {
         q.tail = 0;
         q.p0 = q.pt = 0;
       }
+      q.mtail = (int)__reduce_max_sync(kFull, (unsigned)q.tail);
     }
   }
 
@@ -237,8 +237,14 @@ struct Evaluator {
       acc += __shfl_xor_sync(kFull, acc, 1);
       acc += __shfl_xor_sync(kFull, acc, 2);
       acc += __shfl_xor_sync(kFull, acc, 4);
-      t = q.pt;
-      for (int u = 0; u < q.tail; ++u, ++t) acc += term(plain, logs, t);
+      // the tail terms follow in order (numpy pairwise_sum): lane j of the group evaluates
+      // tail term j, the additions run through shuffles
+      double tv = 0.0;
+      if ((lane & 7) < q.tail) tv = term(plain, logs, q.pt + (lane & 7));
+      for (int u = 0; u < q.mtail; ++u) {
+        const double v = __shfl_sync(kFull, tv, (lane & ~7) | u);
+        if (u < q.tail) acc += v;
+      }
       res[s] = acc;
     }
     // replay the recursion's merges (post-order): leaf[dst] = leaf[dst] + leaf[src]
