@@ -136,7 +136,7 @@ template <int SLOTS, int ORDER>
 struct Evaluator {
   SlotPlan sp[SLOTS];
   int k, n, base, rem;
-  int c0, r0, q32, r32;  // grid position of plaintext position `lane`; 32 = q32*k + r32
+  int c0, r0, qs, rs;  // grid position of plaintext position 4*lane; 128 = qs*k + rs
   const SumPlan* plan;
 
   // the key length may change per worker (ragged SCT batches)
@@ -144,10 +144,10 @@ struct Evaluator {
     k = k_;
     base = n / k;
     rem = n - base * k;
-    q32 = 32 / k;
-    r32 = 32 - q32 * k;
-    r0 = lane / k;
-    c0 = lane - r0 * k;
+    qs = 128 / k;
+    rs = 128 - qs * k;
+    r0 = 4 * lane / k;
+    c0 = 4 * lane - r0 * k;
   }
 
   __device__ void init(const SumPlan& P, int k_, int n_, int lane) {
@@ -208,13 +208,25 @@ struct Evaluator {
       if (lane + 32 < k) colstart[key.v1] = (uint16_t)(tot0 + inc1 - len1);
     }
     __syncwarp();
-    // decrypt (ciphers.py:107-113): plain[t] = cipher[colstart[t % k] + t / k]
+    // decrypt (ciphers.py:107-113): plain[t] = cipher[colstart[t % k] + t / k], four
+    // consecutive positions per lane and one 32-bit store (positions past n land in the
+    // buffer's padding and are never read)
     {
       int c = c0, r = r0;
-      for (int t = lane; t < n; t += 32) {
-        plain[t] = txt[colstart[c] + r];
-        c += r32;
-        r += q32;
+      for (int t = 4 * lane; t < n; t += 128) {
+        uint32_t wd = 0;
+        int cc = c, rr = r;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          wd |= (uint32_t)txt[colstart[cc] + rr] << (8 * q);
+          if (++cc == k) {
+            cc = 0;
+            ++rr;
+          }
+        }
+        *reinterpret_cast<uint32_t*>(plain + t) = wd;
+        c += rs;
+        r += qs;
         if (c >= k) {
           c -= k;
           ++r;
