@@ -940,10 +940,45 @@ int ccg_mas_det_solve(ccg_ctx* ctx, const ccg_mas_det_args* a) {
   if ((rc = det_launch(ctx, &d, max_len, tmax))) return rc;
   if ((rc = download(ctx, a->scores, d.scores, (size_t)nj * 8))) return rc;
   if (a->maps && (rc = download(ctx, a->maps, d.maps, (size_t)nj * kAlpha))) return rc;
-  if (a->hist_iter && (rc = download(ctx, a->hist_iter, d.hist_iter, (size_t)nj * it * 4))) return rc;
-  if (a->hist_score && (rc = download(ctx, a->hist_score, d.hist_score, (size_t)nj * it * 8))) return rc;
-  if (a->hist_len && (rc = download(ctx, a->hist_len, d.hist_len, (size_t)nj * 4))) return rc;
   if (a->draws_used && (rc = download(ctx, a->draws_used, d.draws_used, (size_t)nj * 8))) return rc;
+  if (a->hist_iter && a->hist_score && a->hist_len) {
+    // histories are short (a climb stops at its local optimum): pack them on the device and
+    // read back only the entries, then place each job's prefix in its row
+    if ((rc = download(ctx, a->hist_len, d.hist_len, (size_t)nj * 4))) return rc;
+    CCG_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::vector<int64_t> offs((size_t)nj + 1, 0);
+    for (int64_t j = 0; j < nj; ++j) {
+      const int32_t l = a->hist_len[j];
+      if (l < 0 || l > it) return fail(CCG_ERR_CUDA, "history length out of range");
+      offs[j + 1] = offs[j] + l;
+    }
+    const int64_t total = offs[nj];
+    if (total > 0) {
+      if ((rc = upload(ctx, 11, offs.data(), offs.size() * 8, &p))) return rc;
+      const int64_t* doffs = (const int64_t*)p;
+      void *pi, *ps;
+      if ((rc = ctx->buf(12, (size_t)total * 4, &pi))) return rc;
+      if ((rc = ctx->buf(13, (size_t)total * 8, &ps))) return rc;
+      ctx->launches++;
+      cudaError_t e = launch_compact_history(ctx->stream, d.hist_iter, d.hist_score, it, doffs, nj,
+                                             (int32_t*)pi, (int64_t*)ps);
+      if (e != cudaSuccess) return cuda_fail(e, "compact_history kernel");
+      std::vector<int32_t> hi((size_t)total);
+      std::vector<int64_t> hs((size_t)total);
+      if ((rc = download(ctx, hi.data(), pi, (size_t)total * 4))) return rc;
+      if ((rc = download(ctx, hs.data(), ps, (size_t)total * 8))) return rc;
+      CCG_CUDA(cudaStreamSynchronize(ctx->stream));
+      for (int64_t j = 0; j < nj; ++j) {
+        const int64_t l = offs[j + 1] - offs[j];
+        std::memcpy(a->hist_iter + j * it, hi.data() + offs[j], (size_t)l * 4);
+        std::memcpy(a->hist_score + j * it, hs.data() + offs[j], (size_t)l * 8);
+      }
+    }
+  } else {
+    if (a->hist_iter && (rc = download(ctx, a->hist_iter, d.hist_iter, (size_t)nj * it * 4))) return rc;
+    if (a->hist_score && (rc = download(ctx, a->hist_score, d.hist_score, (size_t)nj * it * 8))) return rc;
+    if (a->hist_len && (rc = download(ctx, a->hist_len, d.hist_len, (size_t)nj * 4))) return rc;
+  }
   return finish(ctx, cudaSuccess, "mas_det_solve");
 }
 

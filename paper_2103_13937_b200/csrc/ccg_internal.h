@@ -168,6 +168,11 @@ cudaError_t launch_mas_det_step(cudaStream_t s, const uint8_t* texts, const int6
                                 int64_t n, const int32_t* pivots, const int64_t* table, bool wide,
                                 int64_t* out);
 cudaError_t launch_mas_det_solve(cudaStream_t s, const MasDetLaunch& p, bool wide);
+// pack each job's hist_len[j] history entries (rows of `iterations`) densely at offsets[j]
+cudaError_t launch_compact_history(cudaStream_t s, const int32_t* hist_iter,
+                                   const int64_t* hist_score, int64_t iterations,
+                                   const int64_t* offsets, int64_t n_jobs, int32_t* out_iter,
+                                   int64_t* out_score);
 cudaError_t launch_group_best_i64(cudaStream_t s, const int64_t* scores, int64_t n_groups,
                                   int32_t group_size, int64_t* out);
 cudaError_t launch_group_best_f64(cudaStream_t s, const double* scores, int64_t n_groups,

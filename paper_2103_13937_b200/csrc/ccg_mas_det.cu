@@ -321,4 +321,31 @@ cudaError_t launch_mas_det_solve(cudaStream_t s, const MasDetLaunch& p, bool wid
   return cudaGetLastError();
 }
 
+// One warp per job copies its history prefix into the packed arrays, so the host reads
+// sum(hist_len) entries instead of n_jobs x iterations.
+__global__ void compact_history_kernel(const int32_t* __restrict__ hist_iter,
+                                       const int64_t* __restrict__ hist_score, int64_t iterations,
+                                       const int64_t* __restrict__ offsets, int64_t n_jobs,
+                                       int32_t* __restrict__ out_iter, int64_t* __restrict__ out_score) {
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= n_jobs) return;
+  const int64_t o = offsets[j], len = offsets[j + 1] - o;
+  for (int64_t i = lane; i < len; i += 32) {
+    out_iter[o + i] = hist_iter[j * iterations + i];
+    out_score[o + i] = hist_score[j * iterations + i];
+  }
+}
+
+cudaError_t launch_compact_history(cudaStream_t s, const int32_t* hist_iter,
+                                   const int64_t* hist_score, int64_t iterations,
+                                   const int64_t* offsets, int64_t n_jobs, int32_t* out_iter,
+                                   int64_t* out_score) {
+  if (n_jobs <= 0) return cudaSuccess;
+  const int64_t blocks = (n_jobs + 7) / 8;
+  compact_history_kernel<<<(unsigned)blocks, 256, 0, s>>>(hist_iter, hist_score, iterations, offsets,
+                                                          n_jobs, out_iter, out_score);
+  return cudaGetLastError();
+}
+
 }  // namespace ccg

@@ -14,6 +14,8 @@ Device selection: set_devices([...]) or the CCG_DEVICES environment variable
 """
 from __future__ import annotations
 
+import bisect
+import collections.abc
 import os
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
@@ -340,11 +342,41 @@ def mas_det_step_batch(texts, pivots, table_scores) -> np.ndarray:
     return out
 
 
+class JobHistories(collections.abc.Sequence):
+    """Per-job [(iteration, score), ...] lists of a mas_det_solve batch, built on access:
+    turning every history of a 20,000-job batch into Python tuples up front would cost more
+    than the solve itself."""
+
+    def __init__(self, parts=()):
+        self._parts = [p for p in parts if p[2].size]  # (iterations, scores, lengths)
+        self._ends = np.cumsum([p[2].size for p in self._parts]).tolist()
+
+    def __len__(self):
+        return self._ends[-1] if self._ends else 0
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        n = len(self)
+        if i < 0:
+            i += n
+        if not 0 <= i < n:
+            raise IndexError("job index out of range")
+        k = bisect.bisect_right(self._ends, i)
+        it, sc, ln = self._parts[k]
+        j = i - (self._ends[k - 1] if k else 0)
+        m = int(ln[j])
+        return list(zip(it[j, :m].tolist(), sc[j, :m].tolist()))
+
+    def __eq__(self, other):
+        return len(self) == len(other) and all(a == b for a, b in zip(self, other))
+
+
 @dataclass
 class DetResult:
     scores: np.ndarray          # int64 per job
     maps: np.ndarray            # uint8[n, 26] cipher letter -> plaintext letter
-    history: list               # per job: [(iteration, score), ...]
+    history: JobHistories       # per job: [(iteration, score), ...] (built on access)
     draws_used: np.ndarray
     launches: int
 
@@ -364,7 +396,7 @@ def mas_det_solve(ciphers, cipher_of, keys, table_scores, iterations, *, devices
     def run(dev, lo, hi):
         m = hi - lo
         out = DetResult(scores=np.empty(m, dtype=np.int64), maps=np.empty((m, 26), dtype=np.uint8),
-                        history=[], draws_used=np.empty(m, dtype=np.uint64), launches=0)
+                        history=JobHistories(), draws_used=np.empty(m, dtype=np.uint64), launches=0)
         if m == 0:
             return out
         hi_it = np.empty((m, max(1, it)), dtype=np.int32)
@@ -383,14 +415,13 @@ def mas_det_solve(ciphers, cipher_of, keys, table_scores, iterations, *, devices
             before = ctx.launches()
             _lib.check(_lib.load().ccg_mas_det_solve(ctx.handle, a), "mas_det_solve")
             out.launches = ctx.launches() - before
-        out.history = [list(zip(hi_it[j, :hl[j]].tolist(), hi_sc[j, :hl[j]].tolist()))
-                       for j in range(m)]
+        out.history = JobHistories([(hi_it, hi_sc, hl)])
         return out
 
     parts = _run_sharded(n, 0, devs, run)
     return DetResult(scores=np.concatenate([p.scores for p in parts]),
                      maps=np.concatenate([p.maps for p in parts]),
-                     history=[h for p in parts for h in p.history],
+                     history=JobHistories([q for p in parts for q in p.history._parts]),
                      draws_used=np.concatenate([p.draws_used for p in parts]),
                      launches=sum(p.launches for p in parts))
 
