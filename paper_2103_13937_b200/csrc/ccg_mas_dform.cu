@@ -204,7 +204,10 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
   const int64_t stride = (int64_t)gridDim.x * kDWarps;
   const uint32_t climbings = (uint32_t)p.climbings;
   const int y = lane < kAlpha ? lane : 0;  // the column this lane owns in N updates
-  const uint32_t ks_s = smem_addr(B.KS);
+  // held in a register (an opaque copy: otherwise the shared window address is rebuilt with
+  // S2R/uniform instructions in every round)
+  uint32_t ks_s;
+  asm volatile("mov.u32 %0, %1;" : "=r"(ks_s) : "r"(smem_addr(B.KS)));
 
   const WorkerTickets tk{p.tickets, stride};
   for (int64_t w = (int64_t)blockIdx.x * kDWarps + warp; w < p.n_workers; w = tk.next(w, lane)) {
