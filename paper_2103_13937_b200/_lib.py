@@ -20,6 +20,7 @@ ALPHA = 26
 
 CCG_OK, CCG_ERR_INVALID, CCG_ERR_CUDA, CCG_ERR_NO_DEVICE, CCG_ERR_UNSUPPORTED = 0, -1, -2, -3, -4
 FLAG_EARLY_EXIT = 1
+FLAG_SCT_NO_SPEC = 0x100  # SCT: never use the speculative CTA-per-worker kernel
 KERNEL_FLAGS = {"auto": 0, "dform": 0x10, "tform": 0x20, "packed": 0x30, "dtable": 0x40}
 
 

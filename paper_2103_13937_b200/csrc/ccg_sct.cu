@@ -432,6 +432,122 @@ __global__ void __launch_bounds__(kSctWarps * 32, 4)
   }
 }
 
+// Latency mode (few workers: a time-to-recover solve runs 64): one CTA of P warps per
+// worker, evaluating P consecutive proposals at once.  Proposals never read the key to
+// choose their draws, and a rejected proposal leaves the key unchanged, so warp j builds
+// proposal t+j from the current key after replaying the draws of proposals t..t+j-1; the
+// first proposal whose score beats the current one is accepted (exactly the sequential
+// outcome), everything after it is discarded and the stream resumes right after it.
+struct SpecExchange {
+  double score[8];
+  uint64_t end[8];   // draw position after each warp's proposal
+  uint8_t key[kSctMaxKey];
+};
+
+template <int SLOTS, int ORDER, int P>
+__global__ void __launch_bounds__(P * 32)
+    sct_climb_spec_kernel(const SctLaunch p, const __grid_constant__ SumPlan plan) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const WarpSmem ws(smem, warp, p.n);
+  const double* logs = stage_logs<ORDER>(reinterpret_cast<double*>(smem), p.logs);
+  SpecExchange& ex = *reinterpret_cast<SpecExchange*>(smem + kLogsBytes + P * sct_warp_bytes(p.n));
+
+  Evaluator<SLOTS, ORDER> ev;
+  ev.init(plan, p.k, p.n, lane);
+  const int kmax = p.k;
+  const int64_t climbings = p.climbings;
+
+  for (int64_t w = blockIdx.x; w < p.n_workers; w += gridDim.x) {
+    const int32_t cid = p.cipher_of[w];
+    const int k = p.key_lengths ? p.key_lengths[w] : kmax;
+    if (p.key_lengths) ev.set_k(k, lane);
+    stage_text(ws.txt, p.ciphers + p.offsets[cid], p.n, lane);
+    Draws d;
+    d.key = p.keys + 2 * w;
+    d.win = ws.win;
+    d.start(p.skips ? p.skips[w] : 0, lane);
+    Key key;
+    key.v0 = lane;
+    key.v1 = lane + 32;
+    for (int i = k - 1; i > 0; --i) {  // rng.py:91-97
+      const int j = d.below((uint32_t)(i + 1), lane);
+      key.swap_pos(i, j, lane);
+    }
+    double score = 0.0;
+    int64_t last = -1, t = 0;
+    bool first = true;  // the first pass scores the start key (one evaluator call site)
+    while (first || t < climbings) {
+      Key cand = key;
+      const bool mine = !first && t + warp < climbings;
+      if (mine) {
+        for (int j = 0; j <= warp; ++j) {
+          Key c = key;
+          const int u = d.below(100u, lane);
+          if (u < p.p1)
+            op_element_swaps(c, d, k, p.op1_hop, lane);
+          else if (u < p.p2)
+            op_block_swaps(c, d, k, p.op2_hop, lane);
+          else
+            op_block_shift(c, d, k, lane);
+          if (j == warp) cand = c;
+        }
+      }
+      double cs = 0.0;
+      if (first || mine) cs = ev.score(cand, ws.txt, ws.colstart, ws.plain, logs, lane);
+      if (first) {
+        score = cs;
+        first = false;
+        continue;
+      }
+      if (lane == 0) {
+        ex.score[warp] = cs;
+        ex.end[warp] = d.position();
+      }
+      __syncthreads();
+      const int avail = climbings - t < P ? (int)(climbings - t) : P;
+      int acc = -1;
+      for (int j = 0; j < avail; ++j)
+        if (ex.score[j] > score) {
+          acc = j;
+          break;
+        }
+      const int used = acc >= 0 ? acc : avail - 1;  // the last proposal consumed
+      const uint64_t pos = ex.end[used];
+      if (acc >= 0 && warp == acc) {
+        if (lane < k) ex.key[lane] = (uint8_t)cand.v0;
+        if (lane + 32 < k) ex.key[lane + 32] = (uint8_t)cand.v1;
+      }
+      const double next_score = acc >= 0 ? ex.score[acc] : score;
+      __syncthreads();
+      if (acc >= 0) {
+        key.v0 = lane < k ? ex.key[lane] : lane;
+        key.v1 = lane + 32 < k ? ex.key[lane + 32] : lane + 32;
+        score = next_score;
+        last = t + acc;
+      }
+      t += used + 1;
+      // resume every warp's stream right after the last proposal consumed
+      if (pos >= d.base && pos - d.base < 128)
+        d.o = (uint32_t)(pos - d.base);
+      else
+        d.start(pos, lane);
+      __syncthreads();  // ex is rewritten by the next round
+    }
+    if (warp == 0) {
+      if (lane < k) p.keys_out[w * kmax + lane] = (uint8_t)key.v0;
+      if (lane + 32 < k) p.keys_out[w * kmax + lane + 32] = (uint8_t)key.v1;
+      if (lane == 0) {
+        p.scores[w] = score;
+        if (p.draws_used) p.draws_used[w] = d.position();
+        if (p.last_accept) p.last_accept[w] = last;
+        if (p.tries_done) p.tries_done[w] = t;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Score given (cipher, key) pairs with the same evaluator (sct.py:158-160).
 template <int SLOTS, int ORDER>
 __global__ void __launch_bounds__(kSctWarps * 32)
@@ -576,6 +692,18 @@ cudaError_t climb_slots(cudaStream_t s, const SctLaunch& p, const SumPlan& plan,
   return cudaGetLastError();
 }
 
+constexpr int kSpecWarps = 4;
+
+template <int SLOTS, int ORDER>
+cudaError_t climb_spec_slots(cudaStream_t s, const SctLaunch& p, const SumPlan& plan) {
+  auto kern = sct_climb_spec_kernel<SLOTS, ORDER, kSpecWarps>;
+  const size_t bytes = kLogsBytes + kSpecWarps * sct_warp_bytes(p.n) + sizeof(SpecExchange);
+  cudaError_t e = prep_smem(kern, bytes);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)p.n_workers, kSpecWarps * 32, bytes, s>>>(p, plan);
+  return cudaGetLastError();
+}
+
 template <int SLOTS, int ORDER>
 cudaError_t score_slots(cudaStream_t s, const uint8_t* ciphers, const int64_t* offsets,
                         const int32_t* cipher_of, const uint8_t* keys, int32_t k, int64_t n_keys,
@@ -630,6 +758,15 @@ cudaError_t launch_sct_score_long(cudaStream_t s, const uint8_t* ciphers, const 
 template <int ORDER>
 static cudaError_t climb_order(cudaStream_t s, const SctLaunch& p, const SumPlan& plan,
                                int sm_count) {
+  // latency mode: at most one worker per SM -- give each worker a CTA of speculating warps
+  if (p.n_workers <= sm_count && !(p.flags & CCG_FLAG_SCT_NO_SPEC)) {
+    switch (slots_for(plan)) {
+      case 1: return climb_spec_slots<1, ORDER>(s, p, plan);
+      case 2: return climb_spec_slots<2, ORDER>(s, p, plan);
+      case 4: return climb_spec_slots<4, ORDER>(s, p, plan);
+      default: return climb_spec_slots<8, ORDER>(s, p, plan);
+    }
+  }
   switch (slots_for(plan)) {
     case 1: return climb_slots<1, ORDER>(s, p, plan, sm_count);
     case 2: return climb_slots<2, ORDER>(s, p, plan, sm_count);

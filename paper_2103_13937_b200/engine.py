@@ -193,12 +193,14 @@ def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, 
 
 def sct_climb(ciphers, cipher_of, keys, logs, key_length, climbings, *, p1=33, p2=66, op1_hop=3,
               op2_hop=3, skips=None, group_size=0, draws_used=False, last_accept=False,
-              tries_done=False, order=2, devices_=None) -> ClimbResult:
+              tries_done=False, order=2, speculate=True, devices_=None) -> ClimbResult:
     """Run sct_worker (sct.py:148-170) for every worker on the GPU(s).  All ciphertexts
     referenced by one call must share a length (the numpy pairwise-sum plan is per length).
     logs: float64[26**order] (order 2 = the reference's bigram table).  key_length may be an
     int or one length per worker (a ragged batch in one launch); keys come back as
-    uint8[n, max key length], row i valid in its first key_length[i] entries."""
+    uint8[n, max key length], row i valid in its first key_length[i] entries.  With at most
+    one worker per SM the engine evaluates consecutive proposals of a worker on several warps
+    at once (identical results, lower latency); speculate=False forces one warp per worker."""
     flat, off = _lib.ragged(ciphers)
     cof = np.ascontiguousarray(cipher_of, dtype=np.int32).reshape(-1)
     keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, 2)
@@ -245,6 +247,7 @@ def sct_climb(ciphers, cipher_of, keys, logs, key_length, climbings, *, p1=33, p
         a.tries_done = _lib.ptr(out.tries_done)
         a.group_size, a.group_best = int(group_size), _lib.ptr(out.group_best)
         a.order = int(order)
+        a.flags = 0 if speculate else _lib.FLAG_SCT_NO_SPEC
         kl = None if klens is None else np.ascontiguousarray(klens[lo:hi])
         a.key_lengths = _lib.ptr(kl)
         ctx = _lib.context(dev)

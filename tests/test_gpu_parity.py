@@ -248,6 +248,31 @@ def test_mas_results_independent_of_device_split():
     assert np.array_equal(one.group_best, two.group_best)
 
 
+@pytest.mark.parametrize("order", [2, 3])
+def test_sct_speculative_kernel_matches_warp_kernel(order):
+    """Few workers run on the speculative CTA-per-worker kernel (ccg_sct.cu
+    sct_climb_spec_kernel): every output equals the one-warp-per-worker kernel's, for ragged
+    key lengths and budgets that are not multiples of the speculation depth."""
+    rng = np.random.default_rng(90 + order)
+    n_len = 333
+    cs = [rng.integers(0, 26, n_len) for _ in range(3)]
+    logs = -rng.random(26**order) * 20 - 1
+    m = 40
+    cof = rng.integers(0, 3, m).astype(np.int32)
+    klens = rng.integers(2, 41, m).astype(np.int32)
+    keys = philox_keys([23], list(range(m)))
+    for climb in (0, 1, 2, 3, 5, 417):
+        kw = dict(order=order, draws_used=True, last_accept=True, tries_done=True)
+        a = engine.sct_climb(cs, cof, keys, logs, klens, climb, **kw)
+        b = engine.sct_climb(cs, cof, keys, logs, klens, climb, speculate=False, **kw)
+        assert a.scores.tolist() == b.scores.tolist(), climb
+        for i in range(m):
+            assert np.array_equal(a.keys[i, :klens[i]], b.keys[i, :klens[i]]), (climb, i)
+        assert np.array_equal(a.draws_used, b.draws_used), climb
+        assert np.array_equal(a.last_accept, b.last_accept), climb
+        assert np.array_equal(a.tries_done, b.tries_done), climb
+
+
 def test_restarts_stop_and_prefix(golden):
     table = cc.BigramTable(np.random.default_rng(29).integers(0, 500, 676))
     cipher = np.random.default_rng(30).integers(0, 26, 120)
