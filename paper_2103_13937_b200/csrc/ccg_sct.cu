@@ -445,7 +445,7 @@ struct SpecExchange {
 };
 
 template <int SLOTS, int ORDER, int P>
-__global__ void __launch_bounds__(P * 32)
+__global__ void __launch_bounds__(P * 32, 32 / P)
     sct_climb_spec_kernel(const SctLaunch p, const __grid_constant__ SumPlan plan) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -692,17 +692,34 @@ cudaError_t climb_slots(cudaStream_t s, const SctLaunch& p, const SumPlan& plan,
   return cudaGetLastError();
 }
 
-// 8 warps: one restart of the #08 shape takes 24 ms (28 ms with 4, 61 ms with one warp)
-constexpr int kSpecWarps = 8;
-
-template <int SLOTS, int ORDER>
-cudaError_t climb_spec_slots(cudaStream_t s, const SctLaunch& p, const SumPlan& plan) {
-  auto kern = sct_climb_spec_kernel<SLOTS, ORDER, kSpecWarps>;
-  const size_t bytes = kLogsBytes + kSpecWarps * sct_warp_bytes(p.n) + sizeof(SpecExchange);
+template <int SLOTS, int ORDER, int P>
+cudaError_t spec_launch(cudaStream_t s, const SctLaunch& p, const SumPlan& plan, int sm_count,
+                        bool* launched) {
+  *launched = false;
+  auto kern = sct_climb_spec_kernel<SLOTS, ORDER, P>;
+  const size_t bytes = kLogsBytes + P * sct_warp_bytes(p.n) + sizeof(SpecExchange);
   cudaError_t e = prep_smem(kern, bytes);
   if (e != cudaSuccess) return e;
-  kern<<<(unsigned)p.n_workers, kSpecWarps * 32, bytes, s>>>(p, plan);
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P * 32, bytes);
+  if (e != cudaSuccess) return e;
+  if ((int64_t)per_sm * sm_count < p.n_workers) return cudaSuccess;  // more than one wave
+  kern<<<(unsigned)p.n_workers, P * 32, bytes, s>>>(p, plan);
+  *launched = true;
   return cudaGetLastError();
+}
+
+// Latency mode: the deepest speculation (8, 4 or 2 warps per worker) whose CTAs all fit on
+// the GPU at once -- one restart of the #08 shape (64 workers) takes 24 ms with 8 warps,
+// 28 ms with 4, 61 ms with one warp per worker.  false: use the one-warp kernel.
+template <int SLOTS, int ORDER>
+cudaError_t climb_spec_slots(cudaStream_t s, const SctLaunch& p, const SumPlan& plan, int sm_count,
+                             bool* launched) {
+  cudaError_t e = spec_launch<SLOTS, ORDER, 8>(s, p, plan, sm_count, launched);
+  if (e != cudaSuccess || *launched) return e;
+  e = spec_launch<SLOTS, ORDER, 4>(s, p, plan, sm_count, launched);
+  if (e != cudaSuccess || *launched) return e;
+  return spec_launch<SLOTS, ORDER, 2>(s, p, plan, sm_count, launched);
 }
 
 template <int SLOTS, int ORDER>
@@ -759,14 +776,17 @@ cudaError_t launch_sct_score_long(cudaStream_t s, const uint8_t* ciphers, const 
 template <int ORDER>
 static cudaError_t climb_order(cudaStream_t s, const SctLaunch& p, const SumPlan& plan,
                                int sm_count) {
-  // latency mode: at most one worker per SM -- give each worker a CTA of speculating warps
-  if (p.n_workers <= sm_count && !(p.flags & CCG_FLAG_SCT_NO_SPEC)) {
+  // latency mode: few enough workers that each can get a CTA of speculating warps
+  if (p.n_workers <= 4 * (int64_t)sm_count && !(p.flags & CCG_FLAG_SCT_NO_SPEC)) {
+    bool launched = false;
+    cudaError_t e;
     switch (slots_for(plan)) {
-      case 1: return climb_spec_slots<1, ORDER>(s, p, plan);
-      case 2: return climb_spec_slots<2, ORDER>(s, p, plan);
-      case 4: return climb_spec_slots<4, ORDER>(s, p, plan);
-      default: return climb_spec_slots<8, ORDER>(s, p, plan);
+      case 1: e = climb_spec_slots<1, ORDER>(s, p, plan, sm_count, &launched); break;
+      case 2: e = climb_spec_slots<2, ORDER>(s, p, plan, sm_count, &launched); break;
+      case 4: e = climb_spec_slots<4, ORDER>(s, p, plan, sm_count, &launched); break;
+      default: e = climb_spec_slots<8, ORDER>(s, p, plan, sm_count, &launched); break;
     }
+    if (e != cudaSuccess || launched) return e;
   }
   switch (slots_for(plan)) {
     case 1: return climb_slots<1, ORDER>(s, p, plan, sm_count);

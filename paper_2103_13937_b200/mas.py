@@ -121,14 +121,18 @@ def solve_stochastic(cipher: MappedText, table: BigramTable, cfg: MasSolverConfi
 def _batched_restarts(make_batch, restarts: int, workers: int, stop):
     """Lazily evaluate restarts in device-sized chunks, fold them in order (search.py:61-86).
     Results equal the sequential reference: restarts are independent of each other and of
-    `stop`, which is still applied restart by restart."""
+    `stop`, which is still applied restart by restart.  With a `stop` callback the chunks
+    grow 1, 2, 4, ... restarts (a solve usually stops after its first restart, and a small
+    launch finishes sooner); without one, every chunk is a full wave."""
     target = 8192 * max(1, len(engine.devices()))  # workers per chunk: ~one full wave
     chunk = max(1, min(restarts, target // max(1, workers)))
 
     def gen():
         r = 0
+        size = 1 if stop is not None else chunk
         while r < restarts:
-            rs = list(range(r, min(restarts, r + chunk)))
+            rs = list(range(r, min(restarts, r + size)))
+            size = min(chunk, 2 * size)
             t0 = time.perf_counter()
             results = make_batch(rs)
             dt = (time.perf_counter() - t0) / len(rs)
