@@ -364,6 +364,31 @@ __device__ __forceinline__ void op_block_shift(Key& c, Draws& d, int k, int lane
   c = c.gather(src(lane), src(lane + 32), k > 32);
 }
 
+// The draws of one proposal without building it (sct.py:69-135: the operator choice and
+// every operator's draws depend only on the stream and k, never on the key).
+__device__ __forceinline__ void skip_proposal(Draws& d, int k, int p1, int p2, int hop1, int hop2,
+                                           int lane) {
+  const int u = d.below(100u, lane);
+  int a, b;
+  if (u < p1) {
+    const int hops = 1 + d.below((uint32_t)hop1, lane);
+    for (int h = 0; h < hops; ++h) d.pair((uint32_t)k, lane, a, b);
+  } else if (u < p2) {
+    const int hops = 1 + d.below((uint32_t)hop2, lane);
+    for (int h = 0; h < hops; ++h) {
+      const int len = 1 + d.below((uint32_t)(k / 2), lane);
+      d.pair((uint32_t)(k - len + 1), lane, a, b);
+      while (abs(a - b) < len) d.pair((uint32_t)(k - len + 1), lane, a, b);
+    }
+  } else {
+    const int len = 1 + d.below((uint32_t)(k - 1), lane);
+    const int starts = k - len + 1;
+    a = d.below((uint32_t)starts, lane);
+    b = d.below((uint32_t)starts, lane);
+    while (b == a) b = d.below((uint32_t)starts, lane);
+  }
+}
+
 template <int SLOTS, int ORDER>
 __global__ void __launch_bounds__(kSctWarps * 32, 4)
     sct_climb_kernel(const SctLaunch p, const __grid_constant__ SumPlan plan) {
@@ -481,17 +506,14 @@ __global__ void __launch_bounds__(P * 32, 32 / P)
       Key cand = key;
       const bool mine = !first && t + warp < climbings;
       if (mine) {
-        for (int j = 0; j <= warp; ++j) {
-          Key c = key;
-          const int u = d.below(100u, lane);
-          if (u < p.p1)
-            op_element_swaps(c, d, k, p.op1_hop, lane);
-          else if (u < p.p2)
-            op_block_swaps(c, d, k, p.op2_hop, lane);
-          else
-            op_block_shift(c, d, k, lane);
-          if (j == warp) cand = c;
-        }
+        for (int j = 0; j < warp; ++j) skip_proposal(d, k, p.p1, p.p2, p.op1_hop, p.op2_hop, lane);
+        const int u = d.below(100u, lane);
+        if (u < p.p1)
+          op_element_swaps(cand, d, k, p.op1_hop, lane);
+        else if (u < p.p2)
+          op_block_swaps(cand, d, k, p.op2_hop, lane);
+        else
+          op_block_shift(cand, d, k, lane);
       }
       double cs = 0.0;
       if (first || mine) cs = ev.score(cand, ws.txt, ws.colstart, ws.plain, logs, lane);
