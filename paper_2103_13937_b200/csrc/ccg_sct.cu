@@ -464,13 +464,13 @@ __global__ void __launch_bounds__(kSctWarps * 32, 4)
 // first proposal whose score beats the current one is accepted (exactly the sequential
 // outcome), everything after it is discarded and the stream resumes right after it.
 struct SpecExchange {
-  double score[8];
-  uint64_t end[8];   // draw position after each warp's proposal
+  double score[16];
+  uint64_t end[16];  // draw position after each warp's proposal
   uint8_t key[kSctMaxKey];
 };
 
 template <int SLOTS, int ORDER, int P>
-__global__ void __launch_bounds__(P * 32, 32 / P)
+__global__ void __launch_bounds__(P * 32, P >= 32 ? 1 : 32 / P)
     sct_climb_spec_kernel(const SctLaunch p, const __grid_constant__ SumPlan plan) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -731,13 +731,16 @@ cudaError_t spec_launch(cudaStream_t s, const SctLaunch& p, const SumPlan& plan,
   return cudaGetLastError();
 }
 
-// Latency mode: the deepest speculation (8, 4 or 2 warps per worker) whose CTAs all fit on
-// the GPU at once -- one restart of the #08 shape (64 workers) takes 24 ms with 8 warps,
+// Latency mode: the deepest speculation (16, 8, 4 or 2 warps per worker) whose CTAs all fit
+// on the GPU at once -- one restart of the #08 shape (64 workers) takes 21 ms with 16 warps,
+// 23 ms with 8,
 // 28 ms with 4, 61 ms with one warp per worker.  false: use the one-warp kernel.
 template <int SLOTS, int ORDER>
 cudaError_t climb_spec_slots(cudaStream_t s, const SctLaunch& p, const SumPlan& plan, int sm_count,
                              bool* launched) {
-  cudaError_t e = spec_launch<SLOTS, ORDER, 8>(s, p, plan, sm_count, launched);
+  cudaError_t e = spec_launch<SLOTS, ORDER, 16>(s, p, plan, sm_count, launched);
+  if (e != cudaSuccess || *launched) return e;
+  e = spec_launch<SLOTS, ORDER, 8>(s, p, plan, sm_count, launched);
   if (e != cudaSuccess || *launched) return e;
   e = spec_launch<SLOTS, ORDER, 4>(s, p, plan, sm_count, launched);
   if (e != cudaSuccess || *launched) return e;
