@@ -733,8 +733,8 @@ cudaError_t spec_launch(cudaStream_t s, const SctLaunch& p, const SumPlan& plan,
 
 // Latency mode: the deepest speculation (16, 8, 4 or 2 warps per worker) whose CTAs all fit
 // on the GPU at once -- one restart of the #08 shape (64 workers) takes 21 ms with 16 warps,
-// 23 ms with 8,
-// 28 ms with 4, 61 ms with one warp per worker.  false: use the one-warp kernel.
+// 23 ms with 8, 28 ms with 4, 61 ms with one warp per worker.  *launched = false: none fits,
+// use the one-warp kernel.
 template <int SLOTS, int ORDER>
 cudaError_t climb_spec_slots(cudaStream_t s, const SctLaunch& p, const SumPlan& plan, int sm_count,
                              bool* launched) {
