@@ -35,6 +35,36 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kSctWarps = 8;
 
+// raw shared-memory accessors on 32-bit shared addresses (ld/st.shared): the evaluator keeps
+// its buffers' addresses in registers instead of letting the compiler rebuild the shared
+// window base (S2R + uniform arithmetic) at every access
+__device__ __forceinline__ uint32_t pin_smem(const void* p) {
+  uint32_t a;
+  asm volatile("mov.u32 %0, %1;" : "=r"(a) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+  return a;
+}
+__device__ __forceinline__ uint32_t lds8(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double ldsf64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
 // The worker's draw window: 128 consecutive raw draws of its stream in shared memory
 // (one Philox4x64-10 block per lane per refill, rng.py:68-75), so a scalar draw is one
 // broadcast 64-bit shared load.  Every SCT bound is < 2^11 (100, hops, k <= 64, ...), so
@@ -176,17 +206,21 @@ struct Evaluator {
   }
 
   // log-probability of the window of ORDER plaintext letters starting at position t
-  __device__ __forceinline__ double term(const uint8_t* plain, const double* logs, int t) const {
-    int idx = plain[t];
+  __device__ __forceinline__ double term(uint32_t plain, uint32_t slogs, const double* logs,
+                                        int t) const {
+    int idx = (int)lds8(plain + (uint32_t)t);
 #pragma unroll
-    for (int j = 1; j < ORDER; ++j) idx = idx * kAlpha + plain[t + j];
-    if (ORDER == 2) return logs[idx];
+    for (int j = 1; j < ORDER; ++j) idx = idx * kAlpha + (int)lds8(plain + (uint32_t)(t + j));
+    if (ORDER == 2) return ldsf64(slogs + 8u * (uint32_t)idx);
     return __ldg(logs + idx);  // trigram/quadgram tables are read through L1/L2
   }
 
   // Score of decrypting txt with the lane-distributed key.
-  __device__ double score(const Key& key, const uint8_t* txt, uint16_t* colstart,
-                          uint8_t* plain, const double* logs, int lane) const {
+  __device__ double score(const Key& key, const uint8_t* txt_p, uint16_t* colstart_p,
+                          uint8_t* plain_p, const double* logs, int lane) const {
+    const uint32_t txt = pin_smem(txt_p), colstart = pin_smem(colstart_p);
+    const uint32_t plain = pin_smem(plain_p);
+    const uint32_t slogs = ORDER == 2 ? pin_smem(logs) : 0u;
     // colstart[key[j]] = sum of segment lengths of key positions < j (ciphers.py:79-86)
     const bool wide = k > 32;
     const int len0 = lane < k ? base + (key.v0 < rem ? 1 : 0) : 0;
@@ -202,10 +236,10 @@ struct Evaluator {
       }
     }
     __syncwarp();
-    if (lane < k) colstart[key.v0] = (uint16_t)(inc0 - len0);
+    if (lane < k) sts16(colstart + 2u * (uint32_t)key.v0, (uint32_t)(inc0 - len0));
     if (wide) {
       const int tot0 = __shfl_sync(kFull, inc0, 31);
-      if (lane + 32 < k) colstart[key.v1] = (uint16_t)(tot0 + inc1 - len1);
+      if (lane + 32 < k) sts16(colstart + 2u * (uint32_t)key.v1, (uint32_t)(tot0 + inc1 - len1));
     }
     __syncwarp();
     // decrypt (ciphers.py:107-113): plain[t] = cipher[colstart[t % k] + t / k], four
@@ -218,13 +252,13 @@ struct Evaluator {
         int cc = c, rr = r;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          wd |= (uint32_t)txt[colstart[cc] + rr] << (8 * q);
+          wd |= lds8(txt + lds16(colstart + 2u * (uint32_t)cc) + (uint32_t)rr) << (8 * q);
           if (++cc == k) {
             cc = 0;
             ++rr;
           }
         }
-        *reinterpret_cast<uint32_t*>(plain + t) = wd;
+        sts32(plain + (uint32_t)t, wd);
         c += rs;
         r += qs;
         if (c >= k) {
@@ -242,7 +276,7 @@ struct Evaluator {
       double acc = 0.0;
       int t = q.p0;
       for (int i = 0; i < q.count; ++i, t += 8) {
-        const double v = term(plain, logs, t);
+        const double v = term(plain, slogs, logs, t);
         acc = i == 0 ? v : acc + v;
       }
       // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) as an xor butterfly over the 8-lane group
@@ -252,7 +286,7 @@ struct Evaluator {
       // the tail terms follow in order (numpy pairwise_sum): lane j of the group evaluates
       // tail term j, the additions run through shuffles
       double tv = 0.0;
-      if ((lane & 7) < q.tail) tv = term(plain, logs, q.pt + (lane & 7));
+      if ((lane & 7) < q.tail) tv = term(plain, slogs, logs, q.pt + (lane & 7));
       for (int u = 0; u < q.mtail; ++u) {
         const double v = __shfl_sync(kFull, tv, (lane & ~7) | u);
         if (u < q.tail) acc += v;
