@@ -47,7 +47,7 @@ constexpr int kDS = 32;  // D row stride (int32): D[a][b] sits in bank b
 // each looked-up delta from T, N and ks on demand (no rebuild, 3.3 KB less per warp).
 template <bool TABLE>
 struct alignas(16) DWarp {
-  uint64_t rk[20];  // Philox round keys of the current worker's stream
+  uint64_t rk[22];  // Philox round keys of the current worker's stream (+ M0*k0)
   int16_t T[kAlpha * kTS];
   int N[kAlpha * kNS];
   int D[TABLE ? kAlpha * kDS : 4];

@@ -83,27 +83,41 @@ __device__ __forceinline__ uint32_t int_below_tiny(uint64_t x, uint32_t bound) {
 }
 
 // Philox4x64-10 with the ten round keys (k0 + r*W0, k1 + r*W1) precomputed in shared memory
-// at `rk` (20 x u64, see philox_round_keys): one broadcast LDS.128 per round instead of two
-// 64-bit key additions.
+// at `rk` (22 x u64, see philox_round_keys): one broadcast LDS.128 per round instead of two
+// 64-bit key additions.  The counter is (c0, 0, 0, 0), so round 1 multiplies only x0 and
+// leaves x0 = k0 for round 2, whose M0*k0 product is the same for every block of the stream:
+// rk[20..21] hold it (one 64x64 multiply of twenty saved per block).
 __device__ __forceinline__ void philox_round_keys(uint64_t* rk, uint64_t k0, uint64_t k1,
                                                   int lane) {
   if (lane < 10) {
     rk[2 * lane] = k0 + (uint64_t)lane * kPhiloxW0;
     rk[2 * lane + 1] = k1 + (uint64_t)lane * kPhiloxW1;
   }
+  if (lane == 10) rk[20] = kPhiloxM0 * k0;
+  if (lane == 11) rk[21] = __umul64hi(kPhiloxM0, k0);
 }
 __device__ __forceinline__ void philox4x64_10_rk(uint32_t rk, uint64_t c0, uint64_t& o0,
                                                  uint64_t& o1, uint64_t& o2, uint64_t& o3) {
-  uint64_t x0 = c0, x1 = 0, x2 = 0, x3 = 0;
+  uint64_t k0, k1, pl, ph;
+  // round 1: x = (c0, 0, 0, 0)
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(k0), "=l"(k1) : "r"(rk));
+  const uint64_t lo0 = kPhiloxM0 * c0, hi0 = __umul64hi(kPhiloxM0, c0);
+  uint64_t x2 = hi0 ^ k1, x3 = lo0;
+  // round 2: x = (k0, 0, x2, x3) with M0*k0 precomputed
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(k0), "=l"(k1) : "r"(rk + 16u));
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(pl), "=l"(ph) : "r"(rk + 160u));
+  const uint64_t lo1 = kPhiloxM1 * x2, hi1 = __umul64hi(kPhiloxM1, x2);
+  uint64_t x0 = hi1 ^ k0, x1 = lo1;
+  x2 = ph ^ x3 ^ k1;
+  x3 = pl;
 #pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    uint64_t k0, k1;
+  for (int r = 2; r < 10; ++r) {
     asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(k0), "=l"(k1) : "r"(rk + 16u * r));
-    const uint64_t lo0 = kPhiloxM0 * x0, hi0 = __umul64hi(kPhiloxM0, x0);
-    const uint64_t lo1 = kPhiloxM1 * x2, hi1 = __umul64hi(kPhiloxM1, x2);
-    const uint64_t n0 = hi1 ^ x1 ^ k0;
-    const uint64_t n2 = hi0 ^ x3 ^ k1;
-    x0 = n0; x1 = lo1; x2 = n2; x3 = lo0;
+    const uint64_t a0 = kPhiloxM0 * x0, b0 = __umul64hi(kPhiloxM0, x0);
+    const uint64_t a1 = kPhiloxM1 * x2, b1 = __umul64hi(kPhiloxM1, x2);
+    const uint64_t n0 = b1 ^ x1 ^ k0;
+    const uint64_t n2 = b0 ^ x3 ^ k1;
+    x0 = n0; x1 = a1; x2 = n2; x3 = a0;
   }
   o0 = x0; o1 = x1; o2 = x2; o3 = x3;
 }
