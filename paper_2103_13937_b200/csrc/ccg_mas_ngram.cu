@@ -50,10 +50,11 @@ constexpr uint32_t kCacheBytes = 676u * 4u + 676u * 2u + 8u;  // delta cache + e
 __host__ __device__ inline uint32_t ng_u16_bytes(int max_len) {
   return (2u * (uint32_t)max_len + 15u) & ~15u;
 }
-// plaintext | occurrence lists | start | cursor | delta cache + tags | window scores
+constexpr uint32_t kRoundKeyBytes = 22u * 8u;  // Philox round keys (philox_round_keys)
+// plaintext | occurrence lists | start | cursor | delta cache + tags | window scores | round keys
 __host__ __device__ inline uint32_t ng_warp_bytes(int max_len) {
   return ng_text_stride(max_len) + ng_u16_bytes(max_len) + 32u * 2u + 32u * 4u + kCacheBytes +
-         ng_u16_bytes(max_len);
+         ng_u16_bytes(max_len) + kRoundKeyBytes;
 }
 
 // per-byte equality mask (0x80 in each byte of x equal to the byte in rep), exact for bytes < 0x80
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
   uint16_t* dtag = reinterpret_cast<uint16_t*>(dcache + 676);
   // table score of every window of the current plaintext (ws[s] for the window starting at s)
   uint16_t* ws = reinterpret_cast<uint16_t*>(reinterpret_cast<unsigned char*>(dcache) + kCacheBytes);
+  uint64_t* rk = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(ws) + ng_u16_bytes(max_len));
 
   NgState<G, SMEM_TAB> st;
   st.tab = p.table;
@@ -220,6 +222,9 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
 
     ByteWindow2 win;
     win.key = p.keys + 2 * w;
+    philox_round_keys(rk, __ldg(win.key), __ldg(win.key + 1), lane);
+    __syncwarp();
+    win.rk = smem_addr(rk);
     win.start(p.skips ? p.skips[w] : 0, lane);
 
     // Exact deltas of up to four interchanges (lane g < 4 holds pair g in ga, gb; valid: it
@@ -460,7 +465,7 @@ template <int G, bool SMEM_TAB>
 cudaError_t launch_ng(cudaStream_t s, const MasNgramLaunch& p, int sm_count) {
   const size_t tab = SMEM_TAB ? (((size_t)pow26(G) * 2 + 15) & ~(size_t)15) : 0;
   const size_t wb = ng_warp_bytes((int)p.max_len);
-  if (SMEM_TAB && tab + 32 * wb <= 220 * 1024)  // one 32-warp block per SM shares the table
+  if (SMEM_TAB && tab + 32 * wb <= 227 * 1024)  // one 32-warp block per SM shares the table (opt-in max)
     return launch_ng_w<G, SMEM_TAB, 32>(s, p, sm_count);
   if (tab + 16 * wb <= 200 * 1024) return launch_ng_w<G, SMEM_TAB, 16>(s, p, sm_count);
   if (tab + 8 * wb <= 200 * 1024) return launch_ng_w<G, SMEM_TAB, 8>(s, p, sm_count);
