@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
       const int d1 = (int)__reduce_add_sync(kFull, (uint32_t)(g == 1 ? d : 0));
       const int d2 = (int)__reduce_add_sync(kFull, (uint32_t)(g == 2 ? d : 0));
       const int d3 = (int)__reduce_add_sync(kFull, (uint32_t)(g == 3 ? d : 0));
+      __syncwarp();  // the round's cache reads precede these writes
       if (valid) {
         const int key = (int)(min(ga, gb) * kAlpha + max(ga, gb));
         dcache[key] = lane == 0 ? d0 : lane == 1 ? d1 : lane == 2 ? d2 : d3;
@@ -286,6 +287,7 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
       int d = 0;
       for (int j = lane; j < na + nb; j += 32) d += st.position_delta(st.touched(j, sa, na, sb), arep, brep);
       d = (int)__reduce_add_sync(kFull, (uint32_t)d);
+      __syncwarp();  // every lane's tag read precedes the write
       if (lane == 0) {
         dcache[key] = d;
         dtag[key] = (uint16_t)epoch;

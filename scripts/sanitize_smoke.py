@@ -1,0 +1,45 @@
+#!/usr/bin/env python
+"""Small runs of every climb kernel for compute-sanitizer (memcheck / racecheck / synccheck):
+D-form / T-form / packed MAS, n-gram orders 2-4, deterministic MAS, SCT warp and speculative
+kernels.  Checks results against the oracle as well."""
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+from oracle import oracle as O  # noqa: E402
+from paper_2103_13937_b200 import engine  # noqa: E402
+from paper_2103_13937_b200.rng import philox_keys  # noqa: E402
+
+rng = np.random.default_rng(5)
+cs = [rng.integers(0, 26, int(L)) for L in (40, 97, 300)]
+cof = np.array([0, 1, 2, 2, 1, 0, 2, 1], np.int32)
+seeds, streams = [3] * 8, list(range(8))
+keys = philox_keys(seeds, streams)
+table = rng.integers(0, 700, 676)
+for kern in ("dform", "dtable", "tform", "packed"):
+    r = engine.mas_climb(cs, cof, keys, table, 300, kernel=kern)
+    s, _ = O.mas_workers(cs, cof, seeds, streams, table, 300)
+    assert r.scores.tolist() == s.tolist(), kern
+for order in (2, 3, 4):
+    t = rng.integers(0, 60000, 26**order)
+    r = engine.mas_climb(cs, cof, keys, t, 300, order=order, ngram_kernel=True)
+    s, _ = O.ngram_workers(cs, cof, seeds, streams, order, t, 300)
+    assert r.scores.tolist() == s.tolist(), order
+dk = philox_keys([9], [(r << 32) | (2**32 - 1) for r in range(3)])
+d = engine.mas_det_solve(cs, np.arange(3, dtype=np.int32), dk, table, 20)
+for j, c in enumerate(cs):
+    _, sc, _ = O.solve_deterministic(c, table, 20, 9, j)
+    assert int(d.scores[j]) == sc
+logs = -rng.random(676) * 20 - 1
+sc_c = [rng.integers(0, 26, 200) for _ in range(2)]
+sc_cof = np.array([0, 1, 1, 0], np.int32)
+sk = philox_keys([4] * 4, list(range(4)))
+for spec in (True, False):
+    r = engine.sct_climb(sc_c, sc_cof, sk, logs, 9, 60, speculate=spec)
+    for i in range(4):
+        _, s, _ = O.sct_worker(sc_c[sc_cof[i]], logs, 9, 60, 4, i)
+        assert float(r.scores[i]) == s, (spec, i)
+print("sanitize smoke ok")
