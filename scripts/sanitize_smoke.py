@@ -42,4 +42,23 @@ for spec in (True, False):
     for i in range(4):
         _, s, _ = O.sct_worker(sc_c[sc_cof[i]], logs, 9, 60, 4, i)
         assert float(r.scores[i]) == s, (spec, i)
+# scoring / delta / test-set kernels
+from paper_2103_13937_b200 import ciphers as C  # noqa: E402
+from paper_2103_13937_b200 import rng as R  # noqa: E402
+texts = [rng.integers(0, 26, int(L)) for L in (0, 1, 2, 9, 130, 600)]
+for order in (2, 3, 4):
+    t = rng.integers(0, 1000, 26**order)
+    got = engine.ngram_score_batch(texts, order, t)
+    assert got.tolist() == [int(O.ngram_score_text(x, order, t)) for x in texts], order
+    lg = -rng.random(26**order) * 10 - 1
+    got = engine.ngram_log_score_batch(texts, order, lg)
+    assert got.tolist() == [O.ngram_log_score_text(x, order, lg) for x in texts], order
+pairs = np.array([[0, 1], [3, 7], [25, 24]], np.int32)
+engine.mas_delta_batch(texts[3:], pairs, table)
+keys10 = np.array([rng.permutation(9) for _ in range(4)], np.uint8)
+engine.sct_score_batch(sc_c, sc_cof, keys10, logs)
+C.encrypt_batch([rng.integers(0, 26, 50) for _ in range(5)], "mas", key_seeds=list(range(5)))
+C.encrypt_batch([rng.integers(0, 26, 50) for _ in range(5)], "sct", key_seeds=list(range(5)),
+                key_lengths=[5, 6, 7, 8, 9])
+R.draws(5, 7, 300)
 print("sanitize smoke ok")
