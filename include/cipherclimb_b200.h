@@ -208,6 +208,10 @@ typedef struct {
   uint64_t *draws_used;       /* [n_jobs] pivot draws consumed, or NULL */
   int64_t max_len;            /* required by the _dev entry point only */
   int64_t table_max;          /* required by the _dev entry point only */
+  int64_t *hist_offsets;      /* [n_jobs + 1] or NULL (host entry point only): when set, the
+                                 histories come back packed -- job j's accepts at
+                                 hist_iter/hist_score[hist_offsets[j] .. hist_offsets[j+1]) --
+                                 so only their entries are written */
 } ccg_mas_det_args;
 
 int ccg_mas_det_solve(ccg_ctx *ctx, const ccg_mas_det_args *args);

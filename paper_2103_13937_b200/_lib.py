@@ -68,7 +68,7 @@ class MasDetArgs(C.Structure):
         ("ciphers", _P), ("offsets", _P), ("n_ciphers", _i64), ("cipher_of", _P), ("keys", _P),
         ("n_jobs", _i64), ("iterations", _i64), ("table", _P), ("scores", _P), ("maps", _P),
         ("hist_iter", _P), ("hist_score", _P), ("hist_len", _P), ("draws_used", _P),
-        ("max_len", _i64), ("table_max", _i64),
+        ("max_len", _i64), ("table_max", _i64), ("hist_offsets", _P),
     ]
 
 

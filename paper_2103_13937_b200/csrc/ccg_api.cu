@@ -963,17 +963,27 @@ int ccg_mas_det_solve(ccg_ctx* ctx, const ccg_mas_det_args* a) {
       cudaError_t e = launch_compact_history(ctx->stream, d.hist_iter, d.hist_score, it, doffs, nj,
                                              (int32_t*)pi, (int64_t*)ps);
       if (e != cudaSuccess) return cuda_fail(e, "compact_history kernel");
-      std::vector<int32_t> hi((size_t)total);
-      std::vector<int64_t> hs((size_t)total);
-      if ((rc = download(ctx, hi.data(), pi, (size_t)total * 4))) return rc;
-      if ((rc = download(ctx, hs.data(), ps, (size_t)total * 8))) return rc;
-      CCG_CUDA(cudaStreamSynchronize(ctx->stream));
-      for (int64_t j = 0; j < nj; ++j) {
-        const int64_t l = offs[j + 1] - offs[j];
-        std::memcpy(a->hist_iter + j * it, hi.data() + offs[j], (size_t)l * 4);
-        std::memcpy(a->hist_score + j * it, hs.data() + offs[j], (size_t)l * 8);
+      std::vector<int32_t> hi;
+      std::vector<int64_t> hs;
+      int32_t* dst_i = a->hist_iter;  // packed output: straight into the caller's arrays
+      int64_t* dst_s = a->hist_score;
+      if (!a->hist_offsets) {
+        hi.resize((size_t)total);
+        hs.resize((size_t)total);
+        dst_i = hi.data();
+        dst_s = hs.data();
       }
+      if ((rc = download(ctx, dst_i, pi, (size_t)total * 4))) return rc;
+      if ((rc = download(ctx, dst_s, ps, (size_t)total * 8))) return rc;
+      CCG_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (!a->hist_offsets)
+        for (int64_t j = 0; j < nj; ++j) {
+          const int64_t l = offs[j + 1] - offs[j];
+          std::memcpy(a->hist_iter + j * it, hi.data() + offs[j], (size_t)l * 4);
+          std::memcpy(a->hist_score + j * it, hs.data() + offs[j], (size_t)l * 8);
+        }
     }
+    if (a->hist_offsets) std::memcpy(a->hist_offsets, offs.data(), offs.size() * 8);
   } else {
     if (a->hist_iter && (rc = download(ctx, a->hist_iter, d.hist_iter, (size_t)nj * it * 4))) return rc;
     if (a->hist_score && (rc = download(ctx, a->hist_score, d.hist_score, (size_t)nj * it * 8))) return rc;

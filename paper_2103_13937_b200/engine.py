@@ -351,8 +351,9 @@ class JobHistories(collections.abc.Sequence):
     than the solve itself."""
 
     def __init__(self, parts=()):
-        self._parts = [p for p in parts if p[2].size]  # (iterations, scores, lengths)
-        self._ends = np.cumsum([p[2].size for p in self._parts]).tolist()
+        # (iterations, scores, offsets): job j's entries at [offsets[j], offsets[j+1])
+        self._parts = [p for p in parts if p[2].size > 1]
+        self._ends = np.cumsum([p[2].size - 1 for p in self._parts]).tolist()
 
     def __len__(self):
         return self._ends[-1] if self._ends else 0
@@ -366,10 +367,10 @@ class JobHistories(collections.abc.Sequence):
         if not 0 <= i < n:
             raise IndexError("job index out of range")
         k = bisect.bisect_right(self._ends, i)
-        it, sc, ln = self._parts[k]
+        it, sc, off = self._parts[k]
         j = i - (self._ends[k - 1] if k else 0)
-        m = int(ln[j])
-        return list(zip(it[j, :m].tolist(), sc[j, :m].tolist()))
+        lo, hi = int(off[j]), int(off[j + 1])
+        return list(zip(it[lo:hi].tolist(), sc[lo:hi].tolist()))
 
     def __eq__(self, other):
         return len(self) == len(other) and all(a == b for a, b in zip(self, other))
@@ -402,9 +403,11 @@ def mas_det_solve(ciphers, cipher_of, keys, table_scores, iterations, *, devices
                         history=JobHistories(), draws_used=np.empty(m, dtype=np.uint64), launches=0)
         if m == 0:
             return out
-        hi_it = np.empty((m, max(1, it)), dtype=np.int32)
-        hi_sc = np.empty((m, max(1, it)), dtype=np.int64)
+        # packed histories: capacity m * iterations, but only the accepts' pages are touched
+        hi_it = np.empty(m * max(1, it), dtype=np.int32)
+        hi_sc = np.empty(m * max(1, it), dtype=np.int64)
         hl = np.empty(m, dtype=np.int32)
+        hoff = np.zeros(m + 1, dtype=np.int64)
         c_of = np.ascontiguousarray(cof[lo:hi])
         k = np.ascontiguousarray(keys[lo:hi])
         a = _lib.MasDetArgs()
@@ -413,12 +416,13 @@ def mas_det_solve(ciphers, cipher_of, keys, table_scores, iterations, *, devices
         a.table, a.scores, a.maps = _lib.ptr(table), _lib.ptr(out.scores), _lib.ptr(out.maps)
         a.hist_iter, a.hist_score, a.hist_len = _lib.ptr(hi_it), _lib.ptr(hi_sc), _lib.ptr(hl)
         a.draws_used = _lib.ptr(out.draws_used)
+        a.hist_offsets = _lib.ptr(hoff)
         ctx = _lib.context(dev)
         with ctx.lock:
             before = ctx.launches()
             _lib.check(_lib.load().ccg_mas_det_solve(ctx.handle, a), "mas_det_solve")
             out.launches = ctx.launches() - before
-        out.history = JobHistories([(hi_it, hi_sc, hl)])
+        out.history = JobHistories([(hi_it, hi_sc, hoff)])
         return out
 
     parts = _run_sharded(n, 0, devs, run)

@@ -273,10 +273,10 @@ def test_batch_solver_validation_happens_before_the_gpu():
 def test_job_histories_are_lazy_lists():
     """engine.JobHistories (mas_det_solve's per-job histories, built on access) behaves as the
     list of [(iteration, score), ...] lists it replaces, across device parts."""
-    it = np.arange(12, dtype=np.int32).reshape(3, 4)
+    it = np.array([0, 8, 9, 10], dtype=np.int32)
     sc = it.astype(np.int64) * 10
-    ln = np.array([1, 0, 3], dtype=np.int32)
-    h = engine.JobHistories([(it, sc, ln), (it[:0], sc[:0], ln[:0]), (it, sc, ln)])
+    off = np.array([0, 1, 1, 4], dtype=np.int64)
+    h = engine.JobHistories([(it, sc, off), (it[:0], sc[:0], off[:1]), (it, sc, off)])
     want = [[(0, 0)], [], [(8, 80), (9, 90), (10, 100)]] * 2
     assert len(h) == 6 and list(h) == want and h == want
     assert h[-1] == want[-1] and h[1:3] == want[1:3]
