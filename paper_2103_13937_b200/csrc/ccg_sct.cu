@@ -143,7 +143,14 @@ struct Key {
     o.v1 = s1 < 32 ? a1 : b1;
     return o;
   }
+  template <bool MAYBE_WIDE = true>
   __device__ __forceinline__ void swap_pos(int i, int j, int lane) {
+    if (!MAYBE_WIDE) {  // k <= 32: positions live in v0 only
+      const int vi = __shfl_sync(kFull, v0, i), vj = __shfl_sync(kFull, v0, j);
+      if (lane == i) v0 = vj;
+      if (lane == j) v0 = vi;
+      return;
+    }
     const int vi = at(i), vj = at(j);
     if (lane == i) v0 = vj;
     if (lane == j) v0 = vi;
@@ -216,13 +223,15 @@ struct Evaluator {
   }
 
   // Score of decrypting txt with the lane-distributed key.
+  // MAYBE_WIDE = false: the caller guarantees k <= 32 (no second key register)
+  template <bool MAYBE_WIDE = true>
   __device__ double score(const Key& key, const uint8_t* txt_p, uint16_t* colstart_p,
                           uint8_t* plain_p, const double* logs, int lane) const {
     const uint32_t txt = pin_smem(txt_p), colstart = pin_smem(colstart_p);
     const uint32_t plain = pin_smem(plain_p);
     const uint32_t slogs = ORDER == 2 ? pin_smem(logs) : 0u;
     // colstart[key[j]] = sum of segment lengths of key positions < j (ciphers.py:79-86)
-    const bool wide = k > 32;
+    const bool wide = MAYBE_WIDE && k > 32;
     const int len0 = lane < k ? base + (key.v0 < rem ? 1 : 0) : 0;
     const int len1 = lane + 32 < k ? base + (key.v1 < rem ? 1 : 0) : 0;
     int inc0 = len0, inc1 = len1;
@@ -351,16 +360,18 @@ struct WarpSmem {
 };
 
 // sct.py:82-89 apply_element_swaps
+template <bool MAYBE_WIDE = true>
 __device__ __forceinline__ void op_element_swaps(Key& c, Draws& d, int k, int max_hops, int lane) {
   const int hops = 1 + d.below((uint32_t)max_hops, lane);
   for (int h = 0; h < hops; ++h) {
     int i, j;
     d.pair((uint32_t)k, lane, i, j);
-    c.swap_pos(i, j, lane);
+    c.template swap_pos<MAYBE_WIDE>(i, j, lane);
   }
 }
 
 // sct.py:92-112 apply_block_swaps
+template <bool MAYBE_WIDE = true>
 __device__ __forceinline__ void op_block_swaps(Key& c, Draws& d, int k, int max_hops, int lane) {
   const int hops = 1 + d.below((uint32_t)max_hops, lane);
   for (int h = 0; h < hops; ++h) {
@@ -374,11 +385,12 @@ __device__ __forceinline__ void op_block_swaps(Key& c, Draws& d, int k, int max_
       if (l >= q && l < q + len) return l - q + p;
       return l;
     };
-    c = c.gather(src(lane), src(lane + 32), k > 32);
+    c = c.gather(src(lane), src(lane + 32), MAYBE_WIDE && k > 32);
   }
 }
 
 // sct.py:115-135 apply_block_shift
+template <bool MAYBE_WIDE = true>
 __device__ __forceinline__ void op_block_shift(Key& c, Draws& d, int k, int lane) {
   const int len = 1 + d.below((uint32_t)(k - 1), lane);
   const int starts = k - len + 1;
@@ -395,7 +407,7 @@ __device__ __forceinline__ void op_block_shift(Key& c, Draws& d, int k, int lane
     }
     return l;
   };
-  c = c.gather(src(lane), src(lane + 32), k > 32);
+  c = c.gather(src(lane), src(lane + 32), MAYBE_WIDE && k > 32);
 }
 
 // The draws of one proposal without building it (sct.py:69-135: the operator choice and
@@ -423,7 +435,7 @@ __device__ __forceinline__ void skip_proposal(Draws& d, int k, int p1, int p2, i
   }
 }
 
-template <int SLOTS, int ORDER>
+template <int SLOTS, int ORDER, bool MAYBE_WIDE>
 __global__ void __launch_bounds__(kSctWarps * 32, 4)
     sct_climb_kernel(const SctLaunch p, const __grid_constant__ SumPlan plan) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -453,7 +465,7 @@ __global__ void __launch_bounds__(kSctWarps * 32, 4)
     key.v1 = lane + 32;
     for (int i = k - 1; i > 0; --i) {
       const int j = d.below((uint32_t)(i + 1), lane);
-      key.swap_pos(i, j, lane);
+      key.template swap_pos<MAYBE_WIDE>(i, j, lane);
     }
     // t = -1 scores the start key (sct.py:157); one call site keeps a single inlined copy of
     // the evaluator in the loop (the kernel is instruction-fetch sensitive)
@@ -464,13 +476,13 @@ __global__ void __launch_bounds__(kSctWarps * 32, 4)
       if (t >= 0) {
         const int u = d.below(100u, lane);
         if (u < p.p1)
-          op_element_swaps(cand, d, k, p.op1_hop, lane);
+          op_element_swaps<MAYBE_WIDE>(cand, d, k, p.op1_hop, lane);
         else if (u < p.p2)
-          op_block_swaps(cand, d, k, p.op2_hop, lane);
+          op_block_swaps<MAYBE_WIDE>(cand, d, k, p.op2_hop, lane);
         else
-          op_block_shift(cand, d, k, lane);
+          op_block_shift<MAYBE_WIDE>(cand, d, k, lane);
       }
-      const double cs = ev.score(cand, ws.txt, ws.colstart, ws.plain, logs, lane);
+      const double cs = ev.template score<MAYBE_WIDE>(cand, ws.txt, ws.colstart, ws.plain, logs, lane);
       if (t < 0) {
         score = cs;
       } else if (cs > score) {
@@ -733,7 +745,9 @@ int slots_for(const SumPlan& plan) {
 
 template <int SLOTS, int ORDER>
 cudaError_t climb_slots(cudaStream_t s, const SctLaunch& p, const SumPlan& plan, int sm_count) {
-  auto kern = sct_climb_kernel<SLOTS, ORDER>;
+  // keys of at most 32 positions (every worker: p.k is the batch maximum) skip the second
+  // key register in every operator and in the segment scan
+  auto kern = p.k > 32 ? sct_climb_kernel<SLOTS, ORDER, true> : sct_climb_kernel<SLOTS, ORDER, false>;
   const size_t bytes = sct_smem_bytes(p.n);
   cudaError_t e = prep_smem(kern, bytes);
   if (e != cudaSuccess) return e;

@@ -69,13 +69,15 @@ def fuzz_sct(rng, stats):
     cs = [rng.integers(0, 26, n_len) for _ in range(3)]
     m = 48
     cof = rng.integers(0, 3, m).astype(np.int32)
-    klens = rng.integers(2, min(n_len, 64) + 1, m).astype(np.int32)
+    kmax = int(rng.choice([8, 20, 32, 64]))  # <= 32: narrow kernel variants
+    klens = rng.integers(2, min(n_len, kmax) + 1, m).astype(np.int32)
     seeds, streams = rng.integers(0, 2**63, m).tolist(), rng.integers(0, 2**63, m).tolist()
     p1, p2 = sorted(int(v) for v in rng.integers(0, 101, 2))
     h1, h2 = int(rng.integers(1, 5)), int(rng.integers(1, 5))
     climb = int(rng.choice([0, 1, 50, 400]))
+    spec = bool(rng.integers(0, 2))  # speculative CTA kernel or one warp per worker
     res = engine.sct_climb(cs, cof, philox_keys(seeds, streams), logs, klens, climb, p1=p1, p2=p2,
-                           op1_hop=h1, op2_hop=h2, order=order)
+                           op1_hop=h1, op2_hop=h2, order=order, speculate=spec)
     for i in range(m):
         k = int(klens[i])
         key, score, _ = O.sct_worker(cs[cof[i]], logs, k, climb, seeds[i], streams[i], p1=p1,

@@ -248,8 +248,8 @@ def test_mas_results_independent_of_device_split():
     assert np.array_equal(one.group_best, two.group_best)
 
 
-@pytest.mark.parametrize("order", [2, 3])
-def test_sct_speculative_kernel_matches_warp_kernel(order):
+@pytest.mark.parametrize("order,kmax", [(2, 40), (3, 40), (2, 32), (3, 17)])
+def test_sct_speculative_kernel_matches_warp_kernel(order, kmax):
     """Few workers run on the speculative CTA-per-worker kernel (ccg_sct.cu
     sct_climb_spec_kernel): every output equals the one-warp-per-worker kernel's, for ragged
     key lengths and budgets that are not multiples of the speculation depth."""
@@ -259,7 +259,8 @@ def test_sct_speculative_kernel_matches_warp_kernel(order):
     logs = -rng.random(26**order) * 20 - 1
     m = 40
     cof = rng.integers(0, 3, m).astype(np.int32)
-    klens = rng.integers(2, 41, m).astype(np.int32)
+    klens = rng.integers(2, kmax + 1, m).astype(np.int32)
+    klens[0] = kmax  # the batch maximum picks the warp kernel's narrow (<= 32) or wide variant
     keys = philox_keys([23], list(range(m)))
     for climb in (0, 1, 2, 3, 5, 417):
         kw = dict(order=order, draws_used=True, last_accept=True, tries_done=True)
