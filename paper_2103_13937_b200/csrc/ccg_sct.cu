@@ -61,6 +61,9 @@ __device__ __forceinline__ double ldsf64(uint32_t a) {
 __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
 }
+__device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
@@ -174,6 +177,7 @@ struct Evaluator {
   SlotPlan sp[SLOTS];
   int k, n, base, rem;
   int c0, r0, qs, rs;  // grid position of plaintext position 4*lane; 128 = qs*k + rs
+  int n4, tc, tr;      // n rounded down to 128; grid position of plaintext position n4+lane
   const SumPlan* plan;
 
   // the key length may change per worker (ragged SCT batches)
@@ -185,6 +189,9 @@ struct Evaluator {
     rs = 128 - qs * k;
     r0 = 4 * lane / k;
     c0 = 4 * lane - r0 * k;
+    n4 = n & ~127;
+    tr = (n4 + lane) / k;
+    tc = n4 + lane - tr * k;
   }
 
   __device__ void init(const SumPlan& P, int k_, int n_, int lane) {
@@ -256,7 +263,9 @@ struct Evaluator {
     // buffer's padding and are never read)
     {
       int c = c0, r = r0;
-      for (int t = 4 * lane; t < n; t += 128) {
+      // a remainder of at most 32 positions is one position per lane, not a 4-wide round
+      const int end = n - n4 <= 32 ? n4 : n;
+      for (int t = 4 * lane; t < end; t += 128) {
         uint32_t wd = 0;
         int cc = c, rr = r;
 #pragma unroll
@@ -275,6 +284,8 @@ struct Evaluator {
           ++r;
         }
       }
+      if (end == n4 && n4 + lane < n)
+        sts8(plain + (uint32_t)(n4 + lane), lds8(txt + lds16(colstart + 2u * (uint32_t)tc) + (uint32_t)tr));
     }
     __syncwarp();
 
