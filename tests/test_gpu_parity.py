@@ -834,3 +834,34 @@ def test_batch_solvers_equal_per_ciphertext_solves(golden):
                                                            global_seed=9))
         assert g.per_worker_scores == want.per_worker_scores
         assert np.array_equal(g.best_key, want.best_key)
+
+
+def test_worker_tickets_with_more_workers_than_resident_warps():
+    """Batches larger than the resident grid hand out workers through the ticket counter
+    (ccg_internal.h WorkerTickets): sampled workers of the D-form, n-gram and SCT warp
+    kernels still equal the oracle."""
+    rng = np.random.default_rng(404)
+    n = 12_000
+    sample = rng.choice(n, 48, replace=False)
+    cs = [rng.integers(0, 26, int(L)) for L in rng.integers(30, 200, 50)]
+    cof = rng.integers(0, len(cs), n).astype(np.int32)
+    seeds = [int(v) for v in rng.integers(0, 2**63, n)]
+    streams = [int(v) for v in rng.integers(0, 2**40, n)]
+    keys = philox_keys(seeds, streams)
+    table = rng.integers(0, 900, 676)
+    res = engine.mas_climb(cs, cof, keys, table, 300)
+    s, _ = O.mas_workers(cs, cof[sample], [seeds[i] for i in sample],
+                         [streams[i] for i in sample], table, 300)
+    assert res.scores[sample].tolist() == s.tolist()
+    t3 = rng.integers(0, 60000, 26**3)
+    res = engine.mas_climb(cs, cof, keys, t3, 200, order=3)
+    s, _ = O.ngram_workers(cs, cof[sample], [seeds[i] for i in sample],
+                           [streams[i] for i in sample], 3, t3, 200)
+    assert res.scores[sample].tolist() == s.tolist()
+    sc = [rng.integers(0, 26, 150) for _ in range(4)]
+    scof = rng.integers(0, 4, n).astype(np.int32)
+    logs = -rng.random(676) * 20 - 1
+    res = engine.sct_climb(sc, scof, keys, logs, 9, 40)
+    for i in sample[:16]:
+        _, want, _ = O.sct_worker(sc[scof[i]], logs, 9, 40, seeds[i], streams[i])
+        assert float(res.scores[i]) == want
