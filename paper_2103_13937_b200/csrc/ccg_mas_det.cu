@@ -161,6 +161,7 @@ struct DetShared {
   uint8_t map[32];
   int pivot[2];
   uint32_t present;
+  uint8_t letters[128];  // PIVOT-stream letters int(u*26) of draws wbase .. wbase+127
 };
 
 // T = bigram counts of text[0..n), S = table; returns the score (thread-uniform).
@@ -230,27 +231,48 @@ __global__ void __launch_bounds__(kDetThreads, 5) det_solve_kernel(const MasDetL
   int L = 0, R = 1;
   if (t < kPairs) pair_of(t, L, R);
 
-  // thread 0's PIVOT-stream state (scalar Philox, numpy order)
+  // warp 0 draws the pivots (mas.py:133-137 _draw_present_letter, numpy order) from a
+  // 128-letter window of the PIVOT stream that it refills one Philox block per lane, and
+  // finds each pivot with a ballot over the next 32 draws instead of one draw at a time
   const uint64_t k0 = p.keys[2 * job], k1 = p.keys[2 * job + 1];
-  uint64_t blk[4] = {0, 0, 0, 0};
   uint64_t drawn = 0;  // draws consumed
-  auto next26 = [&]() -> int {
-    if ((drawn & 3) == 0) philox4x64_10(k0, k1, (drawn >> 2) + 1, blk[0], blk[1], blk[2], blk[3]);
-    const uint64_t x = blk[drawn & 3];
-    ++drawn;
-    return (int)int_below_small(x, kAlpha);
+  uint64_t wbase = ~0ull;  // stream index of letters[0] (none yet)
+  auto refill = [&](uint64_t pos) {  // warp 0: window starting at pos & ~3
+    wbase = pos & ~3ull;
+    uint64_t v0, v1, v2, v3;
+    philox4x64_10(k0, k1, (wbase >> 2) + 1 + (uint64_t)t, v0, v1, v2, v3);
+    sh.letters[4 * t] = (uint8_t)int_below_small(v0, kAlpha);
+    sh.letters[4 * t + 1] = (uint8_t)int_below_small(v1, kAlpha);
+    sh.letters[4 * t + 2] = (uint8_t)int_below_small(v2, kAlpha);
+    sh.letters[4 * t + 3] = (uint8_t)int_below_small(v3, kAlpha);
+    __syncwarp();
+  };
+  // the first draw at or after `drawn` whose letter is present (and != skip); consumes
+  // the draws up to and including it
+  auto next_present = [&](uint32_t pres, int skip) -> int {
+    for (;;) {
+      if (wbase == ~0ull || drawn < wbase || drawn + 32 > wbase + 128) refill(drawn);
+      const int L0 = sh.letters[drawn - wbase + (uint64_t)t];
+      const uint32_t ok = __ballot_sync(0xffffffffu, ((pres >> L0) & 1u) && L0 != skip);
+      if (ok) {
+        const int j = __ffs(ok) - 1;
+        drawn += (uint64_t)j + 1;
+        return __shfl_sync(0xffffffffu, L0, j);
+      }
+      drawn += 32;
+    }
   };
   int32_t nh = 0;
   __syncthreads();
   for (int64_t it = 1; it <= p.iterations; ++it) {
-    if (t == 0) {  // mas.py:155-158 via _draw_present_letter (mas.py:133-137)
+    if (t < 32) {
       const uint32_t pres = sh.present;
-      int pl = next26();
-      while (!((pres >> pl) & 1u)) pl = next26();
-      int pr = next26();
-      while (!((pres >> pr) & 1u) || pr == pl) pr = next26();
-      sh.pivot[0] = pl;
-      sh.pivot[1] = pr;
+      const int pl = next_present(pres, -1);
+      const int pr = next_present(pres, pl);
+      if (t == 0) {
+        sh.pivot[0] = pl;
+        sh.pivot[1] = pr;
+      }
     }
     __syncthreads();
     const int pl = sh.pivot[0], pr = sh.pivot[1];
