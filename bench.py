@@ -273,7 +273,7 @@ def config_block(args, world):
 # ------------------------------------------------------------------ GPU leg
 def issue_roofline(evals_per_s: float, clk: dict) -> dict | None:
     """Warp instructions issued per second vs the issue peak (4 per SM per clock), using the
-    warp instructions per evaluation measured by ncu on this kernel (profiles/r1h_ncu.txt)."""
+    warp instructions per evaluation measured by ncu on this kernel (profiles/r1i_ncu.txt)."""
     prof = ROOT / "profiles" / "r1f_ncu.txt"
     try:
         import re
@@ -286,7 +286,7 @@ def issue_roofline(evals_per_s: float, clk: dict) -> dict | None:
     achieved = evals_per_s * inst
     return {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "warp-inst/s",
             "frac": achieved / peak, "inst_per_eval": inst,
-            "source": "ncu smsp__inst_executed.sum / tries (profiles/r1h_ncu.txt); peak = "
+            "source": "ncu smsp__inst_executed.sum / tries (profiles/r1i_ncu.txt); peak = "
                       "4 issue slots x 148 SMs x the median SM clock during the timed steps"}
 
 
