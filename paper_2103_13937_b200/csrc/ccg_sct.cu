@@ -533,7 +533,9 @@ __global__ void __launch_bounds__(P * 32, P >= 32 ? 1 : 32 / P)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const WarpSmem ws(smem, warp, p.n);
   const double* logs = stage_logs<ORDER>(reinterpret_cast<double*>(smem), p.logs);
-  SpecExchange& ex = *reinterpret_cast<SpecExchange*>(smem + kLogsBytes + P * sct_warp_bytes(p.n));
+  // two exchange buffers, alternated by round: a round's writes never meet the previous
+  // round's reads, so a round needs two block barriers instead of three
+  SpecExchange* exb = reinterpret_cast<SpecExchange*>(smem + kLogsBytes + P * sct_warp_bytes(p.n));
 
   Evaluator<SLOTS, ORDER> ev;
   ev.init(plan, p.k, p.n, lane);
@@ -558,6 +560,7 @@ __global__ void __launch_bounds__(P * 32, P >= 32 ? 1 : 32 / P)
     }
     double score = 0.0;
     int64_t last = -1, t = 0;
+    uint32_t rnd = 0;
     bool first = true;  // the first pass scores the start key (one evaluator call site)
     while (first || t < climbings) {
       Key cand = key;
@@ -579,6 +582,7 @@ __global__ void __launch_bounds__(P * 32, P >= 32 ? 1 : 32 / P)
         first = false;
         continue;
       }
+      SpecExchange& ex = exb[rnd++ & 1u];
       if (lane == 0) {
         ex.score[warp] = cs;
         ex.end[warp] = d.position();
@@ -611,7 +615,6 @@ __global__ void __launch_bounds__(P * 32, P >= 32 ? 1 : 32 / P)
         d.o = (uint32_t)(pos - d.base);
       else
         d.start(pos, lane);
-      __syncthreads();  // ex is rewritten by the next round
     }
     if (warp == 0) {
       if (lane < k) p.keys_out[w * kmax + lane] = (uint8_t)key.v0;
@@ -778,7 +781,7 @@ cudaError_t spec_launch(cudaStream_t s, const SctLaunch& p, const SumPlan& plan,
                         bool* launched) {
   *launched = false;
   auto kern = sct_climb_spec_kernel<SLOTS, ORDER, P>;
-  const size_t bytes = kLogsBytes + P * sct_warp_bytes(p.n) + sizeof(SpecExchange);
+  const size_t bytes = kLogsBytes + P * sct_warp_bytes(p.n) + 2 * sizeof(SpecExchange);
   cudaError_t e = prep_smem(kern, bytes);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
