@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(P * 32, P >= 32 ? 1 : 32 / P)
   const WarpSmem ws(smem, warp, p.n);
   const double* logs = stage_logs<ORDER>(reinterpret_cast<double*>(smem), p.logs);
   // two exchange buffers, alternated by round: a round's writes never meet the previous
-  // round's reads, so a round needs two block barriers instead of three
+  // round's reads, so a round needs one block barrier (two when it accepts)
   SpecExchange* exb = reinterpret_cast<SpecExchange*>(smem + kLogsBytes + P * sct_warp_bytes(p.n));
 
   Evaluator<SLOTS, ORDER> ev;
@@ -597,13 +597,13 @@ __global__ void __launch_bounds__(P * 32, P >= 32 ? 1 : 32 / P)
         }
       const int used = acc >= 0 ? acc : avail - 1;  // the last proposal consumed
       const uint64_t pos = ex.end[used];
-      if (acc >= 0 && warp == acc) {
-        if (lane < k) ex.key[lane] = (uint8_t)cand.v0;
-        if (lane + 32 < k) ex.key[lane + 32] = (uint8_t)cand.v1;
-      }
-      const double next_score = acc >= 0 ? ex.score[acc] : score;
-      __syncthreads();
-      if (acc >= 0) {
+      if (acc >= 0) {  // block-uniform: every thread read the same scores
+        if (warp == acc) {
+          if (lane < k) ex.key[lane] = (uint8_t)cand.v0;
+          if (lane + 32 < k) ex.key[lane + 32] = (uint8_t)cand.v1;
+        }
+        const double next_score = ex.score[acc];
+        __syncthreads();
         key.v0 = lane < k ? ex.key[lane] : lane;
         key.v1 = lane + 32 < k ? ex.key[lane + 32] : lane + 32;
         score = next_score;
