@@ -284,3 +284,13 @@ def test_job_histories_are_lazy_lists():
     with pytest.raises(IndexError):
         h[6]
     assert len(engine.JobHistories()) == 0
+
+
+def test_scripts_and_bench_compile():
+    """The measurement and evidence scripts (bench.py, scripts/*.py) at least compile, so a
+    round-end run never dies on a syntax error."""
+    import py_compile
+
+    files = [ROOT / "bench.py", ROOT / "__graft_entry__.py"] + sorted((ROOT / "scripts").glob("*.py"))
+    for f in files:
+        py_compile.compile(str(f), doraise=True)
