@@ -291,6 +291,7 @@ def test_scripts_and_bench_compile():
     round-end run never dies on a syntax error."""
     import py_compile
 
-    files = [ROOT / "bench.py", ROOT / "__graft_entry__.py"] + sorted((ROOT / "scripts").glob("*.py"))
+    files = ([ROOT / "bench.py", ROOT / "__graft_entry__.py"] + sorted((ROOT / "scripts").glob("*.py"))
+             + sorted((ROOT / "tests" / "tools").glob("*.py")))
     for f in files:
         py_compile.compile(str(f), doraise=True)

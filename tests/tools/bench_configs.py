@@ -17,7 +17,7 @@ timed region) after a warm-up call; evals count executed fitness evaluations onl
 column is the C oracle (oracle/cc_oracle.c, a port of the reference algorithm) on all host
 cores over a bounded sample of the same work.
 
-usage: python scripts/bench_configs.py [--quick] [--only C1,C3,...]
+usage: python tests/tools/bench_configs.py [--quick] [--only C1,C3,...]
 """
 from __future__ import annotations
 
@@ -30,7 +30,7 @@ from pathlib import Path
 
 import numpy as np
 
-ROOT = Path(__file__).resolve().parent.parent
+ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 

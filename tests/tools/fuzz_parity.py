@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Randomized parity sweep of every GPU kernel against the CPU oracle for a time budget.
 
-usage: python scripts/fuzz_parity.py [--seconds 300] [--seed 0]
+usage: python tests/tools/fuzz_parity.py [--seconds 300] [--seed 0]
 
 Each round draws random inputs (text lengths, alphabets, tables across magnitudes and kernel
 gates, budgets, stream keys, SCT key lengths / operator mixes, n-gram orders, deterministic
@@ -18,7 +18,7 @@ from pathlib import Path
 
 import numpy as np
 
-ROOT = Path(__file__).resolve().parent.parent
+ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 from oracle import oracle as O  # noqa: E402
 from paper_2103_13937_b200 import engine  # noqa: E402
