@@ -16,8 +16,15 @@ e2e:   the public batch API (engine.mas_climb) from pinned host buffers: H2D of 
 cpu_baseline / --impl reference: the CPU oracle (a C port of the reference algorithm,
   oracle/cc_oracle.c) on every host core over a bounded sample of the same workload.
 
-Multi-GPU (torchrun): weak scaling -- rank r solves its own 10,000-ciphertext batch
-(key seeds offset by r * n_ciphers); no data-path collective; time = max over ranks.
+Multi-GPU: weak scaling -- rank r solves its own 10,000-ciphertext batch (key seeds offset
+by r * n_ciphers); no data-path collective; time = max over ranks (all-reduce MAX).  Under
+torchrun one rank per GPU; a plain `python bench.py --gpus N` re-launches itself under
+torch.distributed.run with N ranks (and fails loudly if fewer than N GPUs are visible).
+
+configs: BASELINE.json's other configurations (C1, C1d, C3, C4, C5) and time-to-recover on
+the reference's acceptance recipes #07/#08, bounded to about a minute, each with the GPU
+rate, the CPU port's rate and a bit-exact parity sample (tests/tools/bench_configs.py);
+rank 0 at N=1 only.
 """
 from __future__ import annotations
 
@@ -58,9 +65,56 @@ def parse_args():
     ap.add_argument("--climbings", type=int, default=10_000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-ciphers", type=int, default=None,
+                    help="ciphertexts the CPU port checks (default: the whole batch)")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the bounded C1/C1d/C3/C4/C5/TTR block")
     ap.add_argument("--profile", action="store_true", help="one warm-up + one step (for ncu)")
     return ap.parse_args()
+
+
+# ------------------------------------------------------------------ launcher
+def visible_gpus() -> int:
+    try:
+        import torch
+
+        return torch.cuda.device_count()
+    except Exception:  # noqa: BLE001
+        return 0
+
+
+def maybe_relaunch(args) -> None:
+    """`python bench.py --gpus N` without torchrun: re-run this script under
+    torch.distributed.run with N ranks, one per GPU (the driver's multi-GPU launch), so both
+    launchers measure N GPUs.  Fails loudly when fewer than N GPUs are visible (except in
+    the CCG_BENCH_SHARE_GPU=1 test mode, where ranks share the visible GPUs over gloo)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    share = os.environ.get("CCG_BENCH_SHARE_GPU") == "1"
+    if args.impl == "ours" and not share:
+        n = visible_gpus()
+        if n < args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} requested but only {n} CUDA "
+                             "device(s) are visible; refusing to report a smaller run\n")
+            sys.exit(2)
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
+def check_world(args, world: int, share: bool) -> None:
+    if world != args.gpus and world > 1:
+        sys.stderr.write(f"bench.py: launched with WORLD_SIZE={world} but --gpus {args.gpus}\n")
+        sys.exit(2)
+    if args.impl == "ours" and not share and world > 1 and visible_gpus() < world:
+        sys.stderr.write(f"bench.py: {world} ranks but only {visible_gpus()} visible GPUs\n")
+        sys.exit(2)
 
 
 # ------------------------------------------------------------------ workload
@@ -199,64 +253,76 @@ def barrier(world: int):
 
 
 # ------------------------------------------------------------------ CPU legs
-def cpu_sample(ciphers, scores, workers, climbings, seconds, rank=0):
-    """Time the C oracle on all host cores over a prefix of the workload, growing the
-    prefix until the run takes >= `seconds` (or the whole batch is used)."""
+def cpu_port(ciphers, scores, workers, climbings, idx, rank=0, n_ciphers=None):
+    """Run the C oracle (a port of stochastic_worker, mas.py:218-244) on every worker of the
+    ciphertexts `idx`, one pthread per host core.  Returns (seconds, {i: best letter map}),
+    the best map of ciphertext i being its first-maximum worker's (search.py:19-25)."""
     from oracle import oracle as O
 
     threads = os.cpu_count() or 1
-    m = max(1, min(len(ciphers), threads // max(1, workers) + 1))
-    while True:
-        n = m * workers
-        cof = np.repeat(np.arange(m, dtype=np.int32), workers)
-        seeds = [7000 + rank * len(ciphers) + i for i in range(m) for _ in range(workers)]
-        streams = [w for _ in range(m) for w in range(workers)]
+    n_ciphers = len(ciphers) if n_ciphers is None else n_ciphers
+    idx = list(idx)
+    best, seconds = {}, 0.0
+    for lo in range(0, len(idx), 1000):  # chunks bound the host memory of the outputs
+        part = idx[lo:lo + 1000]
+        cof = np.repeat(np.arange(len(part), dtype=np.int32), workers)
+        seeds = [7000 + rank * n_ciphers + i for i in part for _ in range(workers)]
+        streams = [w for _ in part for w in range(workers)]
         t0 = time.perf_counter()
-        sc, maps = O.mas_workers(ciphers[:m], cof, seeds, streams, scores, climbings,
-                                 threads=threads)
-        dt = time.perf_counter() - t0
-        if dt >= seconds or m >= len(ciphers):
-            evals = n * climbings
-            best = [int(np.argmax(sc[i * workers:(i + 1) * workers])) for i in range(m)]
-            return {"value": evals / dt, "unit": "evals/s", "cores": threads, "kind": "port",
-                    "sample": f"{m} ciphertexts x {workers} workers x {climbings} climbings "
-                              f"({evals:.3g} evals, {dt:.1f} s) of the bench workload, "
-                              "C oracle (oracle/cc_oracle.c), one pthread per core",
-                    "best_maps": [maps[i * workers + b] for i, b in enumerate(best)]}
-        m = min(len(ciphers), max(m + 1, int(m * max(2.0, 1.3 * seconds / max(dt, 1e-3)))))
+        sc, maps = O.mas_workers([ciphers[i] for i in part], cof, seeds, streams, scores,
+                                 climbings, threads=threads)
+        seconds += time.perf_counter() - t0
+        for j, i in enumerate(part):
+            best[i] = maps[j * workers + int(np.argmax(sc[j * workers:(j + 1) * workers]))]
+    return seconds, best
+
+
+def success_curve(recovered, lengths) -> dict:
+    """Fraction of ciphertexts whose best key decrypts to the plaintext, 50-letter bins."""
+    rec = np.asarray(recovered, dtype=bool)
+    bins = (np.asarray(lengths) // 50) * 50
+    return {f"{b}-{b + 49}": round(float(rec[bins == b].mean()), 4)
+            for b in sorted(set(bins.tolist()))}
 
 
 def run_reference(args):
-    rank, world, local = dist_init(args.gpus)
-    if rank != 0:
+    """The reference arm: the CPU port of the reference algorithm on all host cores.  Step s
+    runs the s-th of `steps` contiguous slices of the 10,000-ciphertext batch (all 64
+    workers x 10,000 climbings of each), so the timed steps together cover the whole
+    workload and the success curve is over exactly the GPU arm's ciphertexts."""
+    if int(os.environ.get("RANK", "0")) != 0:  # under torchrun rank 0 alone runs the port
         return
     plains, ciphers, scores, lengths = make_workload(args.ciphers, 0)
-    samples = []
-    for s in range(args.warmup + args.steps):
-        r = cpu_sample(ciphers, scores, args.workers, args.climbings,
-                       seconds=3.0 if s < args.warmup else args.cpu_seconds)
-        if s >= args.warmup:
-            samples.append(r)
-    value = float(np.mean([r["value"] for r in samples]))
-    # success rate vs length over the reference arm's own sample (same seeds as our arm)
-    maps = samples[-1].pop("best_maps")
-    for r in samples[:-1]:
-        r.pop("best_maps", None)
-    m = len(maps)
-    rec = np.array([np.array_equal(maps[i][ciphers[i]], plains[i]) for i in range(m)])
-    bins = (lengths[:m] // 50) * 50
+    W, K = args.workers, args.climbings
+    threads = os.cpu_count() or 1
+    for s in range(args.warmup):  # warm-up: one ciphertext per step
+        cpu_port(ciphers, scores, W, K, [s % len(ciphers)])
+    chunks = [c.tolist() for c in np.array_split(np.arange(len(ciphers)), max(1, args.steps))]
+    seconds, best = 0.0, {}
+    for ch in chunks:
+        dt, b = cpu_port(ciphers, scores, W, K, ch)
+        seconds += dt
+        best.update(b)
+    evals = len(ciphers) * W * K
+    value = evals / seconds
+    rec = [np.array_equal(best[i][ciphers[i]], plains[i]) for i in range(len(ciphers))]
+    sample = (f"all {len(ciphers)} ciphertexts x {W} workers x {K} climbings ({evals:.3g} "
+              f"evals, {seconds:.1f} s), {args.steps} slices, C oracle (oracle/cc_oracle.c), "
+              "one pthread per core")
     line = {
         "impl": "reference", "metric": "key-candidate fitness evals/sec", "value": value,
         "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": seconds / max(1, args.steps) * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
         "data": "synthetic (corpus windows of the reference's pkg/data, reference key recipe)",
-        "config": config_block(args, world),
-        "cpu_baseline": {**samples[-1], "value": value},
+        "config": config_block(args, args.gpus),
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "port",
+                         "sample": sample},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "success_by_len": {f"{b}-{b + 49}": round(float(rec[bins == b].mean()), 4)
-                           for b in sorted(set(bins.tolist()))},
-        "success_sample": f"first {m} ciphertexts of the workload",
+        "success_by_len": success_curve(rec, lengths),
+        "success_sample": f"all {len(ciphers)} ciphertexts of the workload (the GPU arm's set)",
+        "recovered": int(sum(rec)),
     }
     print(json.dumps(line), flush=True)
 
@@ -271,33 +337,98 @@ def config_block(args, world):
 
 
 # ------------------------------------------------------------------ GPU leg
-def issue_roofline(evals_per_s: float, clk: dict) -> dict | None:
-    """Warp instructions issued per second vs the issue peak (4 per SM per clock), using the
-    warp instructions per evaluation measured by ncu on this kernel (profiles/r1i_ncu.txt)."""
-    prof = ROOT / "profiles" / "r1f_ncu.txt"
-    try:
-        import re
+# The committed ncu --set full capture of the headline kernel (update with the kernel):
+DFORM_PROFILE = "profiles/r1i_ncu.txt"
 
-        inst = float(re.search(r"warp instructions per try = ([0-9.]+)", prof.read_text()).group(1))
-    except Exception:  # noqa: BLE001
+
+def read_ncu_summary(rel: str) -> dict | None:
+    """The counters this line derives from, read from a committed profiles/*_ncu.txt."""
+    import re
+
+    try:
+        txt = (ROOT / rel).read_text()
+    except OSError:
         return None
+
+    def num(pat):
+        m = re.search(pat + r"\s+([0-9.eE+]+)", txt)
+        return float(m.group(1)) if m else None
+
+    tries = num(r"tries in the captured launch:")
+    out = {"file": rel, "tries": tries,
+           "inst": num(r"smsp__inst_executed\.sum"),
+           "smem_wavefronts": num(r"l1tex__data_pipe_lsu_wavefronts_mem_shared\.sum"),
+           "smem_conflicts": num(r"l1tex__data_bank_conflicts_pipe_lsu_mem_shared\.sum"),
+           "smem_pipe_pct": num(r"l1tex__data_pipe_lsu_wavefronts_mem_shared\.sum\.pct_of_peak_sustained_elapsed"),
+           "issue_pct": num(r"smsp__issue_active\.avg\.pct_of_peak_sustained_active")}
+    if not tries or not out["inst"]:
+        return None
+    return out
+
+
+def issue_roofline(evals_per_s: float, clk: dict) -> dict | None:
+    """Warp instructions issued per second vs the issue peak (4 per SM per clock), with the
+    warp instructions per evaluation of the committed ncu capture DFORM_PROFILE."""
+    prof = read_ncu_summary(DFORM_PROFILE)
+    if prof is None:
+        return None
+    inst = prof["inst"] / prof["tries"]
     mhz = clk.get("sm_mhz") or 1965.0
     peak = 4 * 148 * mhz * 1e6
     achieved = evals_per_s * inst
     return {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "warp-inst/s",
             "frac": achieved / peak, "inst_per_eval": inst,
-            "source": "ncu smsp__inst_executed.sum / tries (profiles/r1i_ncu.txt); peak = "
-                      "4 issue slots x 148 SMs x the median SM clock during the timed steps"}
+            "ncu_issue_active_pct": prof["issue_pct"],
+            "source": f"ncu smsp__inst_executed.sum / tries ({DFORM_PROFILE}) x this run's "
+                      "evals/s; peak = 4 issue slots x 148 SMs x the median SM clock during "
+                      "the timed steps"}
+
+
+def smem_pipe_roofline(evals_per_s: float, clk: dict) -> dict | None:
+    """Shared-memory pipe occupancy: wavefronts (including bank-conflict replays) per
+    evaluation from the committed ncu capture x this run's evals/s, against one wavefront
+    per SM per clock -- the counter-based companion of the algorithmic-bytes fraction."""
+    prof = read_ncu_summary(DFORM_PROFILE)
+    if prof is None or not prof["smem_wavefronts"]:
+        return None
+    wpe = prof["smem_wavefronts"] / prof["tries"]
+    mhz = clk.get("sm_mhz") or 1965.0
+    peak = 148 * mhz * 1e6
+    achieved = evals_per_s * wpe
+    return {"bound": "smem-pipe", "achieved": achieved, "peak": peak, "unit": "wavefronts/s",
+            "frac": achieved / peak, "wavefronts_per_eval": wpe,
+            "conflict_wavefronts_per_eval": (prof["smem_conflicts"] or 0.0) / prof["tries"],
+            "ncu_pct_of_peak": prof["smem_pipe_pct"],
+            "source": f"ncu l1tex__data_pipe_lsu_wavefronts_mem_shared.sum / tries "
+                      f"({DFORM_PROFILE}) x this run's evals/s; peak = 1 wavefront per SM per "
+                      "clock at the median SM clock during the timed steps"}
+
+
+def run_configs() -> dict | None:
+    """BASELINE.json's other configurations, bounded (tests/tools/bench_configs.py)."""
+    sys.path.insert(0, str(ROOT / "tests" / "tools"))
+    try:
+        import bench_configs
+    except Exception as e:  # noqa: BLE001
+        return {"error": f"{type(e).__name__}: {e}"}
+    t0 = time.perf_counter()
+    out = bench_configs.run_all(bounded=True)
+    out["wall_s"] = round(time.perf_counter() - t0, 1)
+    return out
 
 
 def main():
     args = parse_args()
+    maybe_relaunch(args)
+    share = os.environ.get("CCG_BENCH_SHARE_GPU") == "1"
     if args.impl == "reference":
         run_reference(args)
         return
     if args.profile:
         args.steps, args.warmup, args.no_e2e, args.no_cpu = 1, 1, True, True
+        args.no_configs = True
     rank, world, local = dist_init(args.gpus)
+    check_world(args, world, share)
 
     import ctypes as C
 
@@ -308,7 +439,7 @@ def main():
     device = local if world > 1 else 0
     # CCG_BENCH_SHARE_GPU=1 (testing only, with CCG_BENCH_BACKEND=gloo): ranks share the
     # visible GPUs round-robin, so the multi-rank path can be exercised on a 1-GPU box
-    if os.environ.get("CCG_BENCH_SHARE_GPU") == "1":
+    if share:
         device = local % torch.cuda.device_count()
     torch.cuda.set_device(device)
     engine.set_devices([device])
@@ -455,21 +586,35 @@ def main():
                       "pinned host memory)"}
         assert np.array_equal(res.scores, sc), "e2e and device-resident runs disagree"
         # success rate vs length (the C2 quality metric), 50-letter bins
-        rec = np.array([np.array_equal(res.keys[i * W + int(res.group_best[i])].astype(np.int64)
-                                       [ciphers[i]], plains[i]) for i in range(len(ciphers))])
-        bins = (lengths // 50) * 50
-        success = {f"{b}-{b + 49}": round(float(rec[bins == b].mean()), 4)
-                   for b in sorted(set(bins.tolist()))}
+        gpu_best = [res.keys[i * W + int(res.group_best[i])].astype(np.int64)
+                    for i in range(len(ciphers))]
+        success = success_curve([np.array_equal(gpu_best[i][ciphers[i]], plains[i])
+                                 for i in range(len(ciphers))], lengths)
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
-        cpu = cpu_sample(ciphers, scores, W, K, args.cpu_seconds)
-        cpu_maps = cpu.pop("best_maps")
-        # the same per-ciphertext outcome as the CPU port on its whole sample (bit-exact parity)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        # the CPU port over the whole batch (or --cpu-ciphers of it): the CPU baseline and
+        # the key-recovery agreement of every ciphertext
+        m = len(ciphers) if args.cpu_ciphers is None else min(len(ciphers), args.cpu_ciphers)
+        dt, cpu_best = cpu_port(ciphers, scores, W, K, range(m))
+        evals = m * W * K
+        cpu = {"value": evals / dt, "unit": "evals/s", "cores": os.cpu_count() or 1,
+               "kind": "port",
+               "sample": f"{m} ciphertexts x {W} workers x {K} climbings ({evals:.3g} evals, "
+                         f"{dt:.1f} s) of the bench workload, C oracle (oracle/cc_oracle.c), "
+                         "one pthread per core"}
         if e2e is not None:
-            cpu["agrees_with_gpu"] = all(
-                np.array_equal(res.keys[i * W + int(res.group_best[i])].astype(np.int64)[ciphers[i]],
-                               cpu_maps[i][ciphers[i]]) for i in range(len(cpu_maps)))
+            agree = sum(bool(np.array_equal(gpu_best[i][ciphers[i]], cpu_best[i][ciphers[i]]))
+                        for i in range(m))
+            cpu["agrees_with_gpu"] = agree == m
+            cpu["agreement"] = f"{agree}/{m} ciphertexts: identical best decryption"
+            cpu["success_by_len"] = success_curve(
+                [np.array_equal(cpu_best[i][ciphers[i]], plains[i]) for i in range(m)],
+                lengths[:m])
+
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        configs = run_configs()
 
     if rank == 0:
         line = {
@@ -496,11 +641,13 @@ def main():
             # the binding resource: warp-instruction issue (4 schedulers per SM), with the
             # instructions per evaluation of the committed ncu capture of this kernel
             "issue_roofline": issue_roofline(value / world, clk),
+            "smem_pipe_roofline": smem_pipe_roofline(value / world, clk),
             "cpu_baseline": cpu,
             "clocks": clk,
             "gpu_launches": launches,
             "evals_per_step": evals_per_step,
             "success_by_len": success,
+            "configs": configs,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -295,3 +295,51 @@ def test_scripts_and_bench_compile():
              + sorted((ROOT / "tests" / "tools").glob("*.py")))
     for f in files:
         py_compile.compile(str(f), doraise=True)
+
+
+def _bench(*argv, env=None, timeout=300):
+    import os
+    import subprocess
+    import sys
+
+    e = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        e.pop(k, None)
+    e.update(env or {})
+    return subprocess.run([sys.executable, str(ROOT / "bench.py"), *argv], capture_output=True,
+                          text=True, env=e, timeout=timeout)
+
+
+def test_bench_gpus_n_fails_loudly_without_n_devices():
+    """A plain `bench.py --gpus N` re-launches itself with N ranks, and refuses to run (exit 2,
+    clear message) when fewer than N GPUs are visible -- it never silently measures one."""
+    r = _bench("--gpus", "2", "--ciphers", "4", env={"CUDA_VISIBLE_DEVICES": ""})
+    assert r.returncode == 2, r.stderr
+    assert "--gpus 2 requested but only 0 CUDA device(s)" in r.stderr
+
+
+def test_bench_reference_arm_covers_the_whole_batch():
+    """--impl reference: the timed steps are disjoint slices that together cover every
+    ciphertext, so its success curve is over the GPU arm's exact set; n_gpus is --gpus under
+    either launcher, and under torchrun only rank 0 prints."""
+    import json
+
+    r = _bench("--impl", "reference", "--ciphers", "12", "--workers", "4", "--climbings", "500",
+               "--steps", "5", "--warmup", "1")
+    assert r.returncode == 0, r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["n_gpus"] == 1
+    assert line["cpu_baseline"]["sample"].startswith("all 12 ciphertexts")
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
+    # the same ciphertexts, workers and streams as the GPU arm: recovery from the oracle directly
+    import bench
+
+    plains, ciphers, scores, lengths = bench.make_workload(12)
+    _, best = bench.cpu_port(ciphers, scores, 4, 500, range(12))
+    rec = [np.array_equal(best[i][ciphers[i]], plains[i]) for i in range(12)]
+    assert line["success_by_len"] == bench.success_curve(rec, lengths)
+    r2 = _bench("--impl", "reference", "--gpus", "2", "--ciphers", "6", "--workers", "2",
+                "--climbings", "200", "--steps", "2", "--warmup", "1")
+    assert r2.returncode == 0, r2.stderr
+    lines = [json.loads(x) for x in r2.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2
