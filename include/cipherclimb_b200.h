@@ -28,6 +28,9 @@
  *                                                rng.py:91-97 permutation(k) on KEYGEN streams (test sets)
  *   ccg_sct_climb[_dev]                          sct.py:173-176 _sct_task -> sct.py:148-170 sct_worker,
  *                                                for a whole batch (sct.py:194-200) + max_element
+ *   ccg_sct_fast_climb                           sct.py:148-170 sct_worker with an int32-quantised
+ *                                                fitness scored incrementally (opt-in fast mode;
+ *                                                not bit-exact with the reference by design)
  *
  * Conventions: plain pointers and sizes only.  Letters are uint8 in [0,26).  Ragged
  * text batches are (concatenated letters, int64 offsets[n+1]).  Philox keys are the
@@ -79,6 +82,15 @@ enum {
  * evaluate consecutive proposals speculatively (identical results, lower latency); this
  * flag forces the one-warp-per-worker kernel instead. */
 #define CCG_FLAG_SCT_NO_SPEC 0x100u
+/* SCT kernel selection (identical results; for tests and benchmarks).  Automatic: few workers
+ * of one text length -> the speculative CTA-per-worker kernel; mixed text lengths or large
+ * bigram batches (>= 32768 workers, where one worker per lane fills the GPU) -> one worker per
+ * LANE (ccg_sct_lane.cu); otherwise one warp per worker.  CCG_FLAG_SCT_KERNEL_WARP /
+ * CCG_FLAG_SCT_KERNEL_LANE force a family; CCG_FLAG_SCT_TABLE_L2 keeps the lane kernel's
+ * trigram table in L2 instead of shared memory. */
+#define CCG_FLAG_SCT_KERNEL_WARP 0x200u
+#define CCG_FLAG_SCT_TABLE_L2 0x400u
+#define CCG_FLAG_SCT_KERNEL_LANE 0x800u
 
 typedef struct ccg_ctx ccg_ctx;
 
@@ -261,6 +273,42 @@ int ccg_sct_score_ngram_batch(ccg_ctx *ctx, const uint8_t *ciphers, const int64_
 
 int ccg_sct_climb(ccg_ctx *ctx, const ccg_sct_climb_args *args);
 int ccg_sct_climb_dev(ccg_ctx *ctx, const ccg_sct_climb_args *args);
+
+/* Opt-in fast SCT mode (north_star "incremental (delta) ... scoring"): sct.py:148-170
+ * sct_worker -- same start key, operators, draws and strict-greater acceptance -- with the
+ * fitness replaced by the INTEGER sum of a quantised log table over the order-gram windows of
+ * the decryption (table[i] = round(logs[i] * 2^shift), Python ngrams.quantize_sct_table).
+ * Integer addition is associative, so a candidate is scored by re-reading only the windows
+ * that touch a column whose ciphertext segment moved.  Results are bit-exact with the fast
+ * mode's own oracle (oracle/cc_oracle.c cco_sct_fast_worker), not with the reference's
+ * float64 climb; the Python layer reports the key agreement with the parity mode.
+ * Texts may have any mix of lengths; (n - order + 1) * max|table| must stay below 2^31. */
+typedef struct {
+  const uint8_t *ciphers;
+  const int64_t *offsets;
+  int64_t n_ciphers;
+  const int32_t *cipher_of;
+  const uint64_t *keys;       /* [2 * n_workers] */
+  const uint64_t *skips;
+  int64_t n_workers;
+  int32_t key_length;         /* keys_out stride; every worker's key length if key_lengths NULL */
+  int64_t climbings;
+  int32_t p1, p2, op1_hop, op2_hop;
+  int32_t order;              /* 2, 3 or 4 */
+  const int32_t *table;       /* [26^order] quantised log table, entries <= 0 */
+  int64_t *scores;            /* quantised fitness of each worker's final key */
+  uint8_t *keys_out;          /* [key_length * n_workers] */
+  uint64_t *draws_used;
+  int64_t *last_accept;
+  int64_t *tries_done;
+  int32_t group_size;
+  int64_t *group_best;
+  const int32_t *key_lengths; /* [n_workers] or NULL */
+  int64_t *lookups;           /* [n_workers] table lookups of the incremental rescoring, or NULL */
+  uint32_t flags;
+} ccg_sct_fast_args;
+
+int ccg_sct_fast_climb(ccg_ctx *ctx, const ccg_sct_fast_args *args);
 
 /* Device-side test-set generation for a ragged batch of plaintexts:
  * kind 0 = MAS (ciphers.py:46-49 mas_encrypt), 1 = SCT (ciphers.py:89-104 sct_encrypt,

@@ -27,6 +27,8 @@
  *   ciphers.py:71-86  transposition_gather_map;  ciphers.py:107-113 sct_decrypt
  *   sct.py:69-135     select_operator / apply_element_swaps / apply_block_swaps / apply_block_shift
  *   sct.py:148-170    sct_worker
+ *                     (+ cco_sct_fast_worker: the same climb on a quantised integer fitness,
+ *                      the definition of the opt-in fast mode -- not a reference function)
  *   search.py:19-25   max_element (first maximum)
  *
  * n-gram extension (orders 3 and 4; BASELINE.json configs 3-5).  The reference implements
@@ -493,6 +495,46 @@ double cco_sct_worker(const int64_t *cipher, int64_t n, const double *logs, cons
     return score;
 }
 
+/* The opt-in fast SCT mode (ccg_sct_fast_climb): sct.py:148-170 with the candidate score
+ * replaced by the INTEGER sum of a quantised table over the order-gram windows of the full
+ * decryption (q[i] = round(logs[i] * 2^shift), ngrams.quantize_sct_table).  Same stream,
+ * start key, operators and strict acceptance as cco_sct_worker; the score is recomputed from
+ * scratch for every candidate -- the definition the GPU's incremental rescoring must match. */
+int64_t cco_sct_fast_worker(const int64_t *cipher, int64_t n, const int64_t *q, const int64_t *cfgv,
+                            uint64_t seed, uint64_t stream, int64_t skip, int64_t *out_key,
+                            int64_t *out_last_accept) {
+    sct_cfg cfg = {cfgv[0], cfgv[1], cfgv[2], cfgv[3], cfgv[4], cfgv[5], cfgv[6]};
+    int64_t k = cfg.k;
+    int order = (int)cfg.order;
+    orng g; orng_init(&g, seed, stream);
+    for (int64_t i = 0; i < skip; i++) orng_next_u64(&g);
+    int64_t *plain = (int64_t *)malloc(sizeof(int64_t) * n);
+    int64_t *map = (int64_t *)malloc(sizeof(int64_t) * n);
+    int64_t key[256], cand[256];
+    orng_permutation(&g, k, key);
+    cco_sct_decrypt(cipher, n, key, k, plain, map);
+    int64_t score = cco_ngram_score_text(plain, n, order, q);
+    int64_t last = -1;
+    for (int64_t t = 0; t < cfg.climbings; t++) {
+        int64_t u = orng_int_below(&g, 100);
+        memcpy(cand, key, sizeof(int64_t) * k);
+        if (u < cfg.p1) op_element_swaps(cand, k, &g, cfg.op1_hop);
+        else if (u < cfg.p2) op_block_swaps(cand, k, &g, cfg.op2_hop);
+        else op_block_shift(cand, k, &g);
+        cco_sct_decrypt(cipher, n, cand, k, plain, map);
+        int64_t cs = cco_ngram_score_text(plain, n, order, q);
+        if (cs > score) {
+            memcpy(key, cand, sizeof(int64_t) * k);
+            score = cs;
+            last = t;
+        }
+    }
+    memcpy(out_key, key, sizeof(int64_t) * k);
+    if (out_last_accept) *out_last_accept = last;
+    free(plain); free(map);
+    return score;
+}
+
 double cco_sct_score(const int64_t *cipher, int64_t n, const double *logs, const int64_t *key,
                      int64_t k, int order) {
     int64_t *plain = (int64_t *)malloc(sizeof(int64_t) * n);
@@ -510,7 +552,7 @@ double cco_sct_score(const int64_t *cipher, int64_t n, const double *logs, const
 #include <pthread.h>
 
 typedef struct {
-    int kind;  /* 0 = MAS, 1 = SCT, 2 = MAS order-n */
+    int kind;  /* 0 = MAS, 1 = SCT, 2 = MAS order-n, 3 = SCT fast (quantised) */
     int order;
     const int64_t *ciphers, *offsets;
     const int32_t *cipher_of;
@@ -542,6 +584,10 @@ static void *batch_thread(void *arg) {
                                                       J->streams[w], 0, NULL,
                                                       J->out_keys ? J->out_keys + 26 * w : NULL,
                                                       NULL);
+        } else if (J->kind == 3) {
+            int64_t k = J->cfgv[0];
+            J->out_iscores[w] = cco_sct_fast_worker(txt, n, J->S, J->cfgv, J->seeds[w],
+                                                    J->streams[w], 0, J->out_keys + k * w, NULL);
         } else {
             int64_t k = J->cfgv[0];
             J->out_fscores[w] = cco_sct_worker(txt, n, J->logs, J->cfgv, J->seeds[w], J->streams[w],
@@ -595,5 +641,17 @@ void cco_ngram_workers(const int64_t *ciphers, const int64_t *offsets, const int
     J.kind = 2; J.order = order; J.ciphers = ciphers; J.offsets = offsets; J.cipher_of = cipher_of;
     J.seeds = seeds; J.streams = streams; J.n_workers = n_workers; J.S = S;
     J.climbings = climbings; J.out_iscores = out_scores; J.out_keys = out_maps;
+    run_batch(&J, nthreads);
+}
+
+void cco_sct_fast_workers(const int64_t *ciphers, const int64_t *offsets, const int32_t *cipher_of,
+                          const uint64_t *seeds, const uint64_t *streams, int64_t n_workers,
+                          const int64_t *q, const int64_t *cfgv, int64_t *out_scores,
+                          int64_t *out_keys, int nthreads) {
+    batch_job J;
+    memset(&J, 0, sizeof J);
+    J.kind = 3; J.ciphers = ciphers; J.offsets = offsets; J.cipher_of = cipher_of;
+    J.seeds = seeds; J.streams = streams; J.n_workers = n_workers; J.S = q; J.cfgv = cfgv;
+    J.out_iscores = out_scores; J.out_keys = out_keys;
     run_batch(&J, nthreads);
 }

@@ -21,6 +21,10 @@ ALPHA = 26
 CCG_OK, CCG_ERR_INVALID, CCG_ERR_CUDA, CCG_ERR_NO_DEVICE, CCG_ERR_UNSUPPORTED = 0, -1, -2, -3, -4
 FLAG_EARLY_EXIT = 1
 FLAG_SCT_NO_SPEC = 0x100  # SCT: never use the speculative CTA-per-worker kernel
+FLAG_SCT_KERNEL_WARP = 0x200  # SCT: one warp per worker instead of one lane per worker
+FLAG_SCT_TABLE_L2 = 0x400  # SCT lane kernel: trigram table read through L2, not shared memory
+FLAG_SCT_KERNEL_LANE = 0x800  # SCT: one worker per lane
+SCT_KERNEL_FLAGS = {"auto": 0, "lane": FLAG_SCT_KERNEL_LANE, "warp": FLAG_SCT_KERNEL_WARP}
 KERNEL_FLAGS = {"auto": 0, "dform": 0x10, "tform": 0x20, "packed": 0x30, "dtable": 0x40}
 
 
@@ -50,6 +54,17 @@ class SctClimbArgs(C.Structure):
         ("scores", _P), ("keys_out", _P), ("draws_used", _P), ("last_accept", _P),
         ("tries_done", _P), ("group_size", _i32), ("group_best", _P), ("text_len", _i64),
         ("flags", _u32), ("order", _i32), ("key_lengths", _P),
+    ]
+
+
+class SctFastArgs(C.Structure):
+    _fields_ = [
+        ("ciphers", _P), ("offsets", _P), ("n_ciphers", _i64), ("cipher_of", _P), ("keys", _P),
+        ("skips", _P), ("n_workers", _i64), ("key_length", _i32), ("climbings", _i64),
+        ("p1", _i32), ("p2", _i32), ("op1_hop", _i32), ("op2_hop", _i32), ("order", _i32),
+        ("table", _P), ("scores", _P), ("keys_out", _P), ("draws_used", _P),
+        ("last_accept", _P), ("tries_done", _P), ("group_size", _i32), ("group_best", _P),
+        ("key_lengths", _P), ("lookups", _P), ("flags", _u32),
     ]
 
 
@@ -109,6 +124,7 @@ EXPORTS = {
     "ccg_sct_score_ngram_batch": (C.c_int, [_P, _P, _P, _i64, _P, _P, _i32, _i64, _i32, _P, _P]),
     "ccg_sct_climb": (C.c_int, [_P, C.POINTER(SctClimbArgs)]),
     "ccg_sct_climb_dev": (C.c_int, [_P, C.POINTER(SctClimbArgs)]),
+    "ccg_sct_fast_climb": (C.c_int, [_P, C.POINTER(SctFastArgs)]),
     "ccg_encrypt_batch": (C.c_int, [_P, _i32, _P, _P, _i64, _P, _P, _i32, _P, _P]),
     "ccg_bench_smem_bandwidth": (C.c_int, [_P, _P]),
 }

@@ -1053,7 +1053,11 @@ static int sct_check(const ccg_sct_climb_args* a) {
   return check_logs(a->logs);
 }
 
-static int sct_launch(ccg_ctx* ctx, const ccg_sct_climb_args* a, int64_t n) {
+// The warp-per-worker family (ccg_sct.cu): the speculative latency kernel for few workers,
+// else one warp per worker.  Needs one common text length n.
+static int sct_launch_warp(ccg_ctx* ctx, const ccg_sct_climb_args* a, int64_t n) {
+  if (n < 0)
+    return fail(CCG_ERR_INVALID, "the warp SCT kernels need one common ciphertext length per call");
   if (n < a->key_length && !a->key_lengths)
     return fail(CCG_ERR_INVALID, "ciphertext shorter than the key");
   if (n > kSctMaxLen)
@@ -1092,10 +1096,79 @@ static int sct_launch(ccg_ctx* ctx, const ccg_sct_climb_args* a, int64_t n) {
   ctx->launches++;
   cudaError_t e = launch_sct_climb(ctx->stream, p, plan, ctx->sm_count);
   if (e != cudaSuccess) return cuda_fail(e, "sct_climb kernel");
+  return CCG_OK;
+}
+
+// One worker per lane (ccg_sct_lane.cu), parity (mode 0) or fast (mode 1) scoring; texts of
+// any mix of lengths up to max_len.
+static int sct_launch_lane(ccg_ctx* ctx, SctLaneLaunch& p) {
+  if (p.mode == 0 && p.max_len > kSctMaxLen)
+    return fail(CCG_ERR_UNSUPPORTED, "ciphertext of %lld letters exceeds the engine limit %lld",
+                (long long)p.max_len, (long long)kSctMaxLen);
+  if (p.mode == 1 && p.max_len > 65535)
+    return fail(CCG_ERR_UNSUPPORTED, "ciphertext of %lld letters exceeds the fast-mode limit 65535",
+                (long long)p.max_len);
+  if (sct_lane_smem_bytes(p.mode, p.kmax, p.max_len) > 200 * 1024)
+    return fail(CCG_ERR_UNSUPPORTED, "ciphertext of %lld letters does not fit the per-lane SCT "
+                "kernel's shared memory", (long long)p.max_len);
+  if (int rc = ctx->tickets(&p.tickets)) return rc;
+  ctx->launches++;
+  cudaError_t e = launch_sct_lane(ctx->stream, p, ctx->sm_count);
+  if (e != cudaSuccess) return cuda_fail(e, "sct_lane kernel");
+  return CCG_OK;
+}
+
+static bool sct_use_warp_family(ccg_ctx* ctx, uint32_t flags, int64_t n_workers, int64_t n_common,
+                                int order) {
+  if (flags & CCG_FLAG_SCT_KERNEL_WARP) return true;
+  if ((flags & CCG_FLAG_SCT_KERNEL_LANE) || n_common < 0) return false;
+  // latency mode: few workers of one text length -> the speculative CTA-per-worker kernel
+  if (!(flags & CCG_FLAG_SCT_NO_SPEC) && n_workers <= 4 * (int64_t)ctx->sm_count) return true;
+  // one worker per lane needs ~32k workers to fill 148 SMs; below that, and for the larger
+  // (L1/L2-resident) trigram/quadgram tables, one warp per worker is as fast or faster
+  // (profiles/r2_sct_*: k=10, n=400 -- bigram 1.6e9 vs 1.1e9 at 65k workers, 0.5e9 vs 1.05e9
+  // at 16k; trigram equal at 65k)
+  return !(order == 2 && n_workers >= 32768);
+}
+
+// n_common: the common text length (-1: mixed lengths); max_len: the longest text
+static int sct_launch(ccg_ctx* ctx, const ccg_sct_climb_args* a, int64_t n_common, int64_t max_len) {
+  int rc;
+  if (sct_use_warp_family(ctx, a->flags, a->n_workers, n_common, a->order == 0 ? 2 : a->order)) {
+    if ((rc = sct_launch_warp(ctx, a, n_common))) return rc;
+  } else {
+    if (max_len < a->key_length && !a->key_lengths)
+      return fail(CCG_ERR_INVALID, "ciphertext shorter than the key");
+    SctLaneLaunch p{};
+    p.mode = 0;
+    p.ciphers = a->ciphers;
+    p.offsets = a->offsets;
+    p.cipher_of = a->cipher_of;
+    p.keys = a->keys;
+    p.skips = a->skips;
+    p.n_workers = a->n_workers;
+    p.kmax = a->key_length;
+    p.max_len = (int32_t)max_len;
+    p.climbings = a->climbings;
+    p.p1 = a->p1;
+    p.p2 = a->p2;
+    p.op1_hop = a->op1_hop;
+    p.op2_hop = a->op2_hop;
+    p.order = a->order == 0 ? 2 : a->order;
+    p.key_lengths = a->key_lengths;
+    p.logs = a->logs;
+    p.scores = a->scores;
+    p.keys_out = a->keys_out;
+    p.draws_used = a->draws_used;
+    p.last_accept = a->last_accept;
+    p.tries_done = a->tries_done;
+    p.flags = a->flags;
+    if ((rc = sct_launch_lane(ctx, p))) return rc;
+  }
   if (a->group_size > 0 && a->group_best) {
     ctx->launches++;
-    e = launch_group_best_f64(ctx->stream, a->scores, a->n_workers / a->group_size, a->group_size,
-                              a->group_best);
+    cudaError_t e = launch_group_best_f64(ctx->stream, a->scores, a->n_workers / a->group_size,
+                                          a->group_size, a->group_best);
     if (e != cudaSuccess) return cuda_fail(e, "group_best kernel");
   }
   return CCG_OK;
@@ -1107,7 +1180,35 @@ int ccg_sct_climb_dev(ccg_ctx* ctx, const ccg_sct_climb_args* a) {
   if (!a) return fail(CCG_ERR_INVALID, "null args");
   if ((rc = sct_check(a))) return rc;
   if (a->n_workers == 0) return CCG_OK;
-  return sct_launch(ctx, a, a->text_len);
+  return sct_launch(ctx, a, a->text_len, a->text_len);
+}
+
+// Host-side checks shared by ccg_sct_climb and ccg_sct_fast_climb: cipher indices, per-worker
+// key lengths; returns the common text length (-1 if mixed) and the longest text.
+static int sct_scan_workers(const uint8_t* ciphers, const int64_t* offsets, int64_t n_ciphers,
+                            const int32_t* cipher_of, const int32_t* key_lengths, int32_t key_length,
+                            int64_t nw, int64_t* n_common, int64_t* max_len) {
+  int rc;
+  if ((rc = check_ragged(ciphers, offsets, n_ciphers, "sct_climb", nullptr))) return rc;
+  int64_t n = -2, m = 0;
+  for (int64_t i = 0; i < nw; ++i) {
+    const int32_t c = cipher_of[i];
+    if (c < 0 || c >= n_ciphers) return fail(CCG_ERR_INVALID, "cipher_of[%lld] out of range", (long long)i);
+    const int64_t L = offsets[c + 1] - offsets[c];
+    if (n == -2) n = L;
+    else if (L != n) n = -1;
+    m = std::max(m, L);
+    const int32_t kw = key_lengths ? key_lengths[i] : key_length;
+    if (key_lengths) {
+      if (kw < 2) return fail(CCG_ERR_INVALID, "key_length must be at least 2");
+      if (kw > key_length)
+        return fail(CCG_ERR_INVALID, "key_lengths[%lld] exceeds key_length", (long long)i);
+    }
+    if (kw > L) return fail(CCG_ERR_INVALID, "ciphertext shorter than the key");
+  }
+  *n_common = n < 0 ? -1 : n;
+  *max_len = m;
+  return CCG_OK;
 }
 
 int ccg_sct_climb(ccg_ctx* ctx, const ccg_sct_climb_args* a) {
@@ -1118,22 +1219,13 @@ int ccg_sct_climb(ccg_ctx* ctx, const ccg_sct_climb_args* a) {
   if ((rc = check_ragged(a->ciphers, a->offsets, a->n_ciphers, "sct_climb", nullptr))) return rc;
   const int64_t nw = a->n_workers;
   if (nw == 0) return CCG_OK;
-  int64_t n = -1;
-  for (int64_t i = 0; i < nw; ++i) {
-    const int32_t c = a->cipher_of[i];
-    if (c < 0 || c >= a->n_ciphers) return fail(CCG_ERR_INVALID, "cipher_of[%lld] out of range", (long long)i);
-    const int64_t L = a->offsets[c + 1] - a->offsets[c];
-    if (n < 0) n = L;
-    if (L != n)
-      return fail(CCG_ERR_INVALID, "all ciphertexts of one sct_climb call must have the same length");
-    if (a->key_lengths) {
-      const int32_t kw = a->key_lengths[i];
-      if (kw < 2) return fail(CCG_ERR_INVALID, "key_length must be at least 2");
-      if (kw > a->key_length)
-        return fail(CCG_ERR_INVALID, "key_lengths[%lld] exceeds key_length", (long long)i);
-      if (kw > L) return fail(CCG_ERR_INVALID, "ciphertext shorter than the key");
-    }
-  }
+  int64_t n = -1, max_len = 0;
+  if ((rc = sct_scan_workers(a->ciphers, a->offsets, a->n_ciphers, a->cipher_of, a->key_lengths,
+                             a->key_length, nw, &n, &max_len)))
+    return rc;
+  if (n < 0 && (a->flags & CCG_FLAG_SCT_KERNEL_WARP))
+    return fail(CCG_ERR_INVALID, "all ciphertexts of one sct_climb call must have the same length "
+                "for the warp kernel");
   ccg_sct_climb_args d = *a;
   void* p;
   const int k = a->key_length;
@@ -1167,7 +1259,7 @@ int ccg_sct_climb(ccg_ctx* ctx, const ccg_sct_climb_args* a) {
   const int64_t ng = a->group_size > 0 ? nw / a->group_size : 0;
   if (a->group_best && ng) { if ((rc = ctx->buf(11, (size_t)ng * 8, &p))) return rc; d.group_best = (int64_t*)p; }
   else d.group_best = nullptr;
-  if ((rc = sct_launch(ctx, &d, n))) return rc;
+  if ((rc = sct_launch(ctx, &d, n, max_len))) return rc;
   if ((rc = download(ctx, a->scores, d.scores, (size_t)nw * 8))) return rc;
   if ((rc = download(ctx, a->keys_out, d.keys_out, (size_t)nw * k))) return rc;
   if (a->draws_used && (rc = download(ctx, a->draws_used, d.draws_used, (size_t)nw * 8))) return rc;
@@ -1175,6 +1267,97 @@ int ccg_sct_climb(ccg_ctx* ctx, const ccg_sct_climb_args* a) {
   if (a->tries_done && (rc = download(ctx, a->tries_done, d.tries_done, (size_t)nw * 8))) return rc;
   if (d.group_best && (rc = download(ctx, a->group_best, d.group_best, (size_t)ng * 8))) return rc;
   return finish(ctx, cudaSuccess, "sct_climb");
+}
+
+int ccg_sct_fast_climb(ccg_ctx* ctx, const ccg_sct_fast_args* a) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (!a) return fail(CCG_ERR_INVALID, "null args");
+  if ((rc = check_climb_common(a->n_workers, a->climbings, a->group_size, a->scores, a->keys,
+                               a->cipher_of)))
+    return rc;
+  if (a->key_length < 2) return fail(CCG_ERR_INVALID, "key_length must be at least 2");
+  if (a->key_length > kSctMaxKey)
+    return fail(CCG_ERR_UNSUPPORTED, "key length %d exceeds the engine limit %d", a->key_length, kSctMaxKey);
+  if (!(0 <= a->p1 && a->p1 <= a->p2 && a->p2 <= 100))
+    return fail(CCG_ERR_INVALID, "thresholds must satisfy 0 <= p1 <= p2 <= 100");
+  if (a->op1_hop < 1 || a->op2_hop < 1) return fail(CCG_ERR_INVALID, "op hops must be at least 1");
+  if (a->order < 2 || a->order > 4)
+    return fail(CCG_ERR_UNSUPPORTED, "n-gram order %d: the engine supports 2..4", a->order);
+  if (!a->table) return fail(CCG_ERR_INVALID, "null table");
+  const int64_t nw = a->n_workers;
+  if (nw == 0) return CCG_OK;
+  if (!a->keys_out) return fail(CCG_ERR_INVALID, "keys_out is required");
+  int64_t n = -1, max_len = 0;
+  if ((rc = sct_scan_workers(a->ciphers, a->offsets, a->n_ciphers, a->cipher_of, a->key_lengths,
+                             a->key_length, nw, &n, &max_len)))
+    return rc;
+  int64_t T = 1;
+  for (int q = 0; q < a->order; ++q) T *= kAlpha;
+  int64_t amax = 0;
+  for (int64_t i = 0; i < T; ++i) amax = std::max(amax, (int64_t)std::abs((int64_t)a->table[i]));
+  const int64_t windows = max_len >= a->order ? max_len - a->order + 1 : 0;
+  if (amax > 0 && windows > (int64_t)2147483647 / amax)
+    return fail(CCG_ERR_UNSUPPORTED, "quantised table too coarse-scaled: %lld windows x max |entry| "
+                "%lld overflow the int32 fitness (use a smaller shift)", (long long)windows,
+                (long long)amax);
+  void* p;
+  SctLaneLaunch L{};
+  L.mode = 1;
+  if ((rc = upload(ctx, 0, a->ciphers, (size_t)a->offsets[a->n_ciphers], &p))) return rc;
+  L.ciphers = (const uint8_t*)p;
+  if ((rc = upload(ctx, 1, a->offsets, (size_t)(a->n_ciphers + 1) * 8, &p))) return rc;
+  L.offsets = (const int64_t*)p;
+  if ((rc = upload(ctx, 2, a->cipher_of, (size_t)nw * 4, &p))) return rc;
+  L.cipher_of = (const int32_t*)p;
+  if ((rc = upload(ctx, 3, a->keys, (size_t)nw * 16, &p))) return rc;
+  L.keys = (const uint64_t*)p;
+  if (a->skips) {
+    if ((rc = upload(ctx, 4, a->skips, (size_t)nw * 8, &p))) return rc;
+    L.skips = (const uint64_t*)p;
+  }
+  if ((rc = upload(ctx, 5, a->table, (size_t)T * 4, &p))) return rc;
+  L.qtable = (const int32_t*)p;
+  if ((rc = ctx->buf(6, (size_t)nw * 8, &p))) return rc;
+  L.iscores = (int64_t*)p;
+  const int k = a->key_length;
+  if ((rc = ctx->buf(7, (size_t)nw * k, &p))) return rc;
+  L.keys_out = (uint8_t*)p;
+  if (a->key_lengths) {
+    if ((rc = upload(ctx, 12, a->key_lengths, (size_t)nw * 4, &p))) return rc;
+    L.key_lengths = (const int32_t*)p;
+  }
+  if (a->draws_used) { if ((rc = ctx->buf(8, (size_t)nw * 8, &p))) return rc; L.draws_used = (uint64_t*)p; }
+  if (a->last_accept) { if ((rc = ctx->buf(9, (size_t)nw * 8, &p))) return rc; L.last_accept = (int64_t*)p; }
+  if (a->tries_done) { if ((rc = ctx->buf(10, (size_t)nw * 8, &p))) return rc; L.tries_done = (int64_t*)p; }
+  if (a->lookups) { if ((rc = ctx->buf(13, (size_t)nw * 8, &p))) return rc; L.lookups = (int64_t*)p; }
+  const int64_t ng = a->group_size > 0 ? nw / a->group_size : 0;
+  int64_t* d_best = nullptr;
+  if (a->group_best && ng) { if ((rc = ctx->buf(11, (size_t)ng * 8, &p))) return rc; d_best = (int64_t*)p; }
+  L.n_workers = nw;
+  L.kmax = k;
+  L.max_len = (int32_t)max_len;
+  L.climbings = a->climbings;
+  L.p1 = a->p1;
+  L.p2 = a->p2;
+  L.op1_hop = a->op1_hop;
+  L.op2_hop = a->op2_hop;
+  L.order = a->order;
+  L.flags = a->flags;
+  if ((rc = sct_launch_lane(ctx, L))) return rc;
+  if (d_best) {
+    ctx->launches++;
+    cudaError_t e = launch_group_best_i64(ctx->stream, L.iscores, ng, a->group_size, d_best);
+    if (e != cudaSuccess) return cuda_fail(e, "group_best kernel");
+  }
+  if ((rc = download(ctx, a->scores, L.iscores, (size_t)nw * 8))) return rc;
+  if ((rc = download(ctx, a->keys_out, L.keys_out, (size_t)nw * k))) return rc;
+  if (a->draws_used && (rc = download(ctx, a->draws_used, L.draws_used, (size_t)nw * 8))) return rc;
+  if (a->last_accept && (rc = download(ctx, a->last_accept, L.last_accept, (size_t)nw * 8))) return rc;
+  if (a->tries_done && (rc = download(ctx, a->tries_done, L.tries_done, (size_t)nw * 8))) return rc;
+  if (a->lookups && (rc = download(ctx, a->lookups, L.lookups, (size_t)nw * 8))) return rc;
+  if (d_best && (rc = download(ctx, a->group_best, d_best, (size_t)ng * 8))) return rc;
+  return finish(ctx, cudaSuccess, "sct_fast_climb");
 }
 
 // ------------------------------------------------------------------ test-set generation

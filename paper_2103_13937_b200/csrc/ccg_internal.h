@@ -115,6 +115,37 @@ struct SctLaunch {
   unsigned long long* tickets;  // worker ticket counter, zero at launch (or NULL)
 };
 
+// SCT climb with one worker per lane (ccg_sct_lane.cu).  mode 0 = parity (float64 log table,
+// numpy pairwise order, bit-exact with sct.py:158-160); mode 1 = fast (int32-quantised table,
+// incremental rescoring of the windows of moved columns; ccg_sct_fast_climb).
+constexpr int kSctLaneWarps = 8;
+struct SctLaneLaunch {
+  int32_t mode;
+  const uint8_t* ciphers;
+  const int64_t* offsets;  // ragged: any mix of text lengths <= max_len
+  const int32_t* cipher_of;
+  const uint64_t* keys;
+  const uint64_t* skips;
+  int64_t n_workers;
+  int32_t kmax;     // key length (or the largest per-worker key length); keys_out stride
+  int32_t max_len;  // longest ciphertext of the launch
+  int64_t climbings;
+  int32_t p1, p2, op1_hop, op2_hop;
+  int32_t order;
+  const int32_t* key_lengths;
+  const double* logs;     // mode 0: [26^order] float64
+  const int32_t* qtable;  // mode 1: [26^order] int32
+  double* scores;         // mode 0
+  int64_t* iscores;       // mode 1
+  uint8_t* keys_out;
+  uint64_t* draws_used;
+  int64_t* last_accept;
+  int64_t* tries_done;
+  int64_t* lookups;       // mode 1: table lookups of the incremental rescoring, per worker
+  uint32_t flags;
+  unsigned long long* tickets;
+};
+
 #ifdef __CUDACC__
 // Worker scheduling for the persistent climb kernels: a warp's first worker is static
 // (warp index), later ones are tickets from a global counter zeroed before the launch, so a
@@ -186,6 +217,9 @@ cudaError_t launch_sct_score_long(cudaStream_t s, const uint8_t* ciphers, const 
                                   int64_t n_keys, int order, const double* logs, double* out);
 cudaError_t launch_sct_climb(cudaStream_t s, const SctLaunch& p, const SumPlan& plan,
                              int sm_count);
+
+cudaError_t launch_sct_lane(cudaStream_t s, const SctLaneLaunch& p, int sm_count);
+size_t sct_lane_smem_bytes(int mode, int kmax, int64_t max_len);
 
 cudaError_t launch_encrypt(cudaStream_t s, int kind, const uint8_t* texts, const int64_t* offsets,
                            int64_t n, const uint64_t* keygen, const int32_t* key_lengths,

@@ -74,6 +74,7 @@ class ClimbResult:
     launches: int
     accepts: np.ndarray | None = None   # accepted interchanges per worker (bigram MAS kernels)
     computed: np.ndarray | None = None  # n-gram kernel: deltas computed by position walks
+    lookups: np.ndarray | None = None   # fast SCT: table lookups of the incremental rescoring
 
 
 def _run_sharded(n_workers, group_size, devs, fn):
@@ -193,14 +194,16 @@ def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, 
 
 def sct_climb(ciphers, cipher_of, keys, logs, key_length, climbings, *, p1=33, p2=66, op1_hop=3,
               op2_hop=3, skips=None, group_size=0, draws_used=False, last_accept=False,
-              tries_done=False, order=2, speculate=True, devices_=None) -> ClimbResult:
-    """Run sct_worker (sct.py:148-170) for every worker on the GPU(s).  All ciphertexts
-    referenced by one call must share a length (the numpy pairwise-sum plan is per length).
-    logs: float64[26**order] (order 2 = the reference's bigram table).  key_length may be an
-    int or one length per worker (a ragged batch in one launch); keys come back as
-    uint8[n, max key length], row i valid in its first key_length[i] entries.  With at most
-    one worker per SM the engine evaluates consecutive proposals of a worker on several warps
-    at once (identical results, lower latency); speculate=False forces one warp per worker."""
+              tries_done=False, order=2, speculate=True, kernel="auto", table_l2=False,
+              devices_=None) -> ClimbResult:
+    """Run sct_worker (sct.py:148-170) for every worker on the GPU(s).  logs:
+    float64[26**order] (order 2 = the reference's bigram table).  key_length may be an int or
+    one length per worker (a ragged batch in one launch); keys come back as
+    uint8[n, max key length], row i valid in its first key_length[i] entries.  Ciphertexts
+    may have any mix of lengths.  Kernels (identical results): with at most a few workers per
+    SM and one common text length, each worker gets a CTA of warps that evaluate consecutive
+    proposals speculatively (speculate=False turns this off); otherwise one worker per lane
+    (kernel="lane"); kernel="warp" forces the one-warp-per-worker kernel (one text length)."""
     flat, off = _lib.ragged(ciphers)
     cof = np.ascontiguousarray(cipher_of, dtype=np.int32).reshape(-1)
     keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, 2)
@@ -247,7 +250,8 @@ def sct_climb(ciphers, cipher_of, keys, logs, key_length, climbings, *, p1=33, p
         a.tries_done = _lib.ptr(out.tries_done)
         a.group_size, a.group_best = int(group_size), _lib.ptr(out.group_best)
         a.order = int(order)
-        a.flags = 0 if speculate else _lib.FLAG_SCT_NO_SPEC
+        a.flags = ((0 if speculate else _lib.FLAG_SCT_NO_SPEC) | _lib.SCT_KERNEL_FLAGS[kernel]
+                   | (_lib.FLAG_SCT_TABLE_L2 if table_l2 else 0))
         kl = None if klens is None else np.ascontiguousarray(klens[lo:hi])
         a.key_lengths = _lib.ptr(kl)
         ctx = _lib.context(dev)
@@ -263,6 +267,78 @@ def sct_climb(ciphers, cipher_of, keys, logs, key_length, climbings, *, p1=33, p
         group_best=_concat(parts, "group_best"), draws_used=_concat(parts, "draws_used"),
         last_accept=_concat(parts, "last_accept"), tries_done=_concat(parts, "tries_done"),
         launches=sum(p.launches for p in parts),
+    )
+
+
+def sct_fast_climb(ciphers, cipher_of, keys, table, key_length, climbings, *, p1=33, p2=66,
+                   op1_hop=3, op2_hop=3, skips=None, group_size=0, draws_used=False,
+                   last_accept=False, tries_done=False, lookups=True, devices_=None) -> ClimbResult:
+    """The opt-in fast SCT mode (ccg_sct_fast_climb): sct_worker (sct.py:148-170) with the
+    fitness replaced by the integer sum of a quantised log table (ngrams.quantize_sct_table:
+    `table` is a QuantizedSctTable or its int32[26**order] entries plus `order` attribute),
+    scored incrementally over the windows of the columns a candidate moves.  Same draws,
+    operators and strict acceptance as the reference; scores come back as int64 quantised
+    fitness.  `lookups` reports the table lookups each worker's incremental rescoring made."""
+    flat, off = _lib.ragged(ciphers)
+    cof = np.ascontiguousarray(cipher_of, dtype=np.int32).reshape(-1)
+    keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, 2)
+    order = int(getattr(table, "order", 0)) or {676: 2, 17576: 3, 456976: 4}.get(np.size(table), 0)
+    tab = np.ascontiguousarray(getattr(table, "table", table), dtype=np.int32).reshape(-1)
+    if order not in (2, 3, 4) or tab.size != 26**order:
+        raise ValueError("the fast SCT table must have 26**order int32 entries, order 2..4")
+    n = cof.size
+    klens = None
+    if np.ndim(key_length):
+        klens = np.ascontiguousarray(key_length, dtype=np.int32).reshape(-1)
+        if klens.size != n:
+            raise ValueError("one key length per worker required")
+        k = int(klens.max()) if n else 2
+    else:
+        k = int(key_length)
+    if keys.shape[0] != n:
+        raise ValueError("one Philox key per worker required")
+    sk = None if skips is None else np.ascontiguousarray(skips, dtype=np.uint64).reshape(-1)
+    devs = devices_ or devices()
+
+    def run(dev, lo, hi):
+        m = hi - lo
+        out = ClimbResult(
+            scores=np.empty(m, dtype=np.int64), keys=np.empty((m, k), dtype=np.uint8),
+            group_best=np.empty(m // group_size, dtype=np.int64) if group_size > 0 else None,
+            draws_used=np.empty(m, dtype=np.uint64) if draws_used else None,
+            last_accept=np.empty(m, dtype=np.int64) if last_accept else None,
+            tries_done=np.empty(m, dtype=np.int64) if tries_done else None, launches=0,
+            lookups=np.empty(m, dtype=np.int64) if lookups else None)
+        if m == 0:
+            return out
+        c_of = np.ascontiguousarray(cof[lo:hi])
+        kk = np.ascontiguousarray(keys[lo:hi])
+        s = None if sk is None else np.ascontiguousarray(sk[lo:hi])
+        kl = None if klens is None else np.ascontiguousarray(klens[lo:hi])
+        a = _lib.SctFastArgs()
+        a.ciphers, a.offsets, a.n_ciphers = _lib.ptr(flat), _lib.ptr(off), off.size - 1
+        a.cipher_of, a.keys, a.skips = _lib.ptr(c_of), _lib.ptr(kk), _lib.ptr(s)
+        a.n_workers, a.key_length, a.climbings = m, k, int(climbings)
+        a.p1, a.p2, a.op1_hop, a.op2_hop = int(p1), int(p2), int(op1_hop), int(op2_hop)
+        a.order, a.table = order, _lib.ptr(tab)
+        a.scores, a.keys_out = _lib.ptr(out.scores), _lib.ptr(out.keys)
+        a.draws_used, a.last_accept = _lib.ptr(out.draws_used), _lib.ptr(out.last_accept)
+        a.tries_done = _lib.ptr(out.tries_done)
+        a.group_size, a.group_best = int(group_size), _lib.ptr(out.group_best)
+        a.key_lengths, a.lookups, a.flags = _lib.ptr(kl), _lib.ptr(out.lookups), 0
+        ctx = _lib.context(dev)
+        with ctx.lock:
+            before = ctx.launches()
+            _lib.check(_lib.load().ccg_sct_fast_climb(ctx.handle, a), "sct_fast_climb")
+            out.launches = ctx.launches() - before
+        return out
+
+    parts = _run_sharded(n, group_size, devs, run)
+    return ClimbResult(
+        scores=_concat(parts, "scores"), keys=_concat(parts, "keys"),
+        group_best=_concat(parts, "group_best"), draws_used=_concat(parts, "draws_used"),
+        last_accept=_concat(parts, "last_accept"), tries_done=_concat(parts, "tries_done"),
+        launches=sum(p.launches for p in parts), lookups=_concat(parts, "lookups"),
     )
 
 

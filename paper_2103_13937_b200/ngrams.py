@@ -301,6 +301,34 @@ def quantize_log_table(table, max_value: int = 65535) -> NgramTable:
     return NgramTable(t.order, np.clip(q, 0, int(max_value)))
 
 
+@dataclass(frozen=True)
+class QuantizedSctTable:
+    """Integer fitness of the opt-in fast SCT mode (engine.sct_fast_climb): table[i] =
+    round(logs[i] * 2**shift), int32, <= 0.  Integer sums are exact and associative, which is
+    what lets the climb re-score only the windows a candidate changes; the float64 parity
+    path (sct.py:158-160) cannot be updated incrementally and stay bit-exact."""
+
+    order: int
+    table: np.ndarray
+    shift: int
+
+
+def quantize_sct_table(table, text_len: int = 4096, max_shift: int = 16) -> QuantizedSctTable:
+    """Quantise a log table (LogBigramTable / LogNgramTable) for the fast SCT mode with the
+    largest shift <= max_shift whose fitness cannot overflow int32 for texts of up to
+    `text_len` letters: (text_len - order + 1) * max|entry| < 2**31."""
+    t = as_log_ngram_table(table)
+    windows = max(1, int(text_len) - t.order + 1)
+    worst = float(np.max(np.abs(t.logs))) if t.logs.size else 0.0
+    shift = int(max_shift)
+    while shift > 0 and windows * np.rint(worst * 2.0**shift) >= 2**31:
+        shift -= 1
+    if windows * np.rint(worst * 2.0**shift) >= 2**31:
+        raise ValueError("log table too large to quantise for this text length")
+    q = np.rint(t.logs * 2.0**shift).astype(np.int64)
+    return QuantizedSctTable(t.order, q.astype(np.int32), shift)
+
+
 def ngram_score_text_batch(texts, table) -> np.ndarray:
     """Integer n-gram fitness of many texts in one GPU call."""
     t = as_ngram_table(table)

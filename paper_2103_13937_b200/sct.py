@@ -158,9 +158,10 @@ def solve_sct(cipher: MappedText, logs: LogBigramTable, cfg: SctSolverConfig, jo
 
 def solve_sct_batch(ciphers, logs, cfg: SctSolverConfig, restart: int = 0, seeds=None,
                     key_lengths=None) -> list[SolveResult]:
-    """One restart of solve_sct (sct.py:179-210) for many equal-length ciphertexts in one GPU
-    launch; key_lengths (default cfg.key_length) may differ per ciphertext.  Ciphertext i
-    uses the streams (restart << 32) | w of seed `seeds[i]` (default cfg.global_seed)."""
+    """One restart of solve_sct (sct.py:179-210) for many ciphertexts (any mix of lengths) in
+    one GPU launch; key_lengths (default cfg.key_length) may differ per ciphertext.
+    Ciphertext i uses the streams (restart << 32) | w of seed `seeds[i]` (default
+    cfg.global_seed)."""
     texts = [np.asarray(c, dtype=np.int64) for c in ciphers]
     n, W = len(texts), cfg.workers
     if n == 0:

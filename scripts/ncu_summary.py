@@ -108,6 +108,21 @@ def full(tag: str, tries: float) -> str:
             out.append(f"  {int(r['Instructions Executed']) / tries:8.4f} "
                        f"{100 * int(r.get('Warp Stall Sampling (All Samples)') or 0) / tot_samples:6.2f}%  "
                        f"{r['Source'].strip()[:80]}")
+        # where the issued instructions go: opcode histogram weighted by executions, and the
+        # most executed SASS lines
+        ops = collections.Counter()
+        for r in body:
+            txt = r["Source"].strip()
+            op = txt.split()[0] if not txt.startswith("@") else txt.split()[1]
+            ops[op.split(".")[0]] += int(r["Instructions Executed"])
+        tot_exec = sum(ops.values()) or 1
+        out += ["", "executed warp instructions by opcode (per unit, share):"]
+        for op, c in ops.most_common(24):
+            out.append(f"  {op:12s} {c / tries:9.3f} {100 * c / tot_exec:6.2f}%")
+        body.sort(key=lambda r: -int(r["Instructions Executed"]))
+        out += ["", "top 30 SASS instructions by executions (per unit, instruction):"]
+        for r in body[:30]:
+            out.append(f"  {int(r['Instructions Executed']) / tries:8.4f}  {r['Source'].strip()[:90]}")
     except Exception as e:  # noqa: BLE001
         out.append(f"(source page unavailable: {e})")
     return "\n".join(out) + "\n"

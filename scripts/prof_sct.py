@@ -22,6 +22,7 @@ ap.add_argument("--k", type=int, default=10)
 ap.add_argument("--workers", type=int, default=16384)
 ap.add_argument("--climbings", type=int, default=2000)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--kernel", default="auto", help="auto / lane / warp / fast")
 a = ap.parse_args()
 corpus = "".join(chr(97 + int(x)) for x in G.corpus())
 if a.order == 2:
@@ -32,8 +33,20 @@ plain = G.plain_sct(400)
 cipher = cc.sct_encrypt(plain, np.random.default_rng(3).permutation(a.k))
 keys = philox_keys([11], list(range(a.workers)))
 cof = np.zeros(a.workers, np.int32)
+if a.kernel == "fast":
+    lt = cc.LogNgramTable(a.order, logs, float(np.min(logs))) if a.order > 2 else \
+        cc.LogBigramTable(logs, -24.0)
+    q = cc.quantize_sct_table(lt, text_len=400)
 for r in range(a.reps):
     t0 = time.perf_counter()
-    res = engine.sct_climb([cipher], cof, keys, logs, a.k, a.climbings, order=a.order)
+    if a.kernel == "fast":
+        res = engine.sct_fast_climb([cipher], cof, keys, q, a.k, a.climbings)
+    else:
+        res = engine.sct_climb([cipher], cof, keys, logs, a.k, a.climbings, order=a.order,
+                               kernel=a.kernel)
     dt = time.perf_counter() - t0
-    print(f"order {a.order} k {a.k}: {a.workers * a.climbings / dt:.4g} evals/s ({dt:.3f} s)")
+    extra = ""
+    if res.lookups is not None:
+        extra = f", {res.lookups.sum() / (a.workers * a.climbings):.1f} lookups/eval"
+    print(f"{a.kernel} order {a.order} k {a.k}: {a.workers * a.climbings / dt:.4g} evals/s "
+          f"({dt:.3f} s{extra})")

@@ -1,0 +1,194 @@
+"""GPU parity of the one-worker-per-lane SCT kernels (csrc/ccg_sct_lane.cu) through the C ABI.
+
+Parity mode (the default throughput path of ccg_sct_climb): every per-worker output --
+float64 score (numpy pairwise order), key, draws consumed, last accepted try -- must equal the
+oracle's sct_worker (oracle/cc_oracle.c, pinned to the reference by tests/test_oracle_golden.py)
+and the warp / speculative kernels' bit for bit.
+
+Fast mode (opt-in, ccg_sct_fast_climb): the quantised integer fitness with incremental
+rescoring must equal its own oracle (cco_sct_fast_worker, full rescore) bit for bit, and on a
+dyadic log table -- where the quantisation is exact and every float64 sum is exact too -- it
+must reproduce the reference algorithm's climb key for key.
+"""
+import numpy as np
+import pytest
+
+import paper_2103_13937_b200 as cc
+from paper_2103_13937_b200 import engine
+from paper_2103_13937_b200.rng import philox_keys
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    from paper_2103_13937_b200 import _lib
+
+    if _lib.device_count() == 0:
+        pytest.fail("no CUDA device visible: GPU tests must run on the B200 box")
+
+
+def _oracle_parity(ciphers, cof, klens, seed, streams, logs, climbings, order, **kw):
+    """Per-worker oracle outputs for a ragged batch (the oracle's batch API takes one k)."""
+    n = len(cof)
+    scores = np.empty(n)
+    keys = [None] * n
+    last = np.empty(n, np.int64)
+    for i in range(n):
+        k, sc, la = O.sct_worker(ciphers[cof[i]], logs, int(klens[i]), climbings, seed,
+                                 streams[i], order=order, **kw)
+        keys[i], scores[i], last[i] = k, sc, la
+    return scores, keys, last
+
+
+@pytest.mark.parametrize("order", [2, 3, 4])
+def test_lane_kernel_vs_oracle(order):
+    """Ragged text lengths AND key lengths in one launch, chunks of 32 workers spanning
+    several ciphertexts (extra passes), keys up to 64 positions (the wide variant)."""
+    rng = np.random.default_rng(500 + order)
+    logs = -rng.random(26**order) * 20 - 1
+    lens = [400, 137, 596, 64, 400, 9, 1000, 251]
+    ciphers = [rng.integers(0, 26, L) for L in lens]
+    m = 70
+    cof = rng.integers(0, len(ciphers), m).astype(np.int32)
+    cof[:32] = 0  # one full chunk of one ciphertext
+    klens = np.array([int(rng.integers(2, min(64, lens[c]) + 1)) for c in cof], np.int32)
+    klens[5] = min(64, lens[cof[5]])
+    streams = [int(s) for s in rng.integers(0, 2**40, m)]
+    seed = 4242
+    keys = philox_keys([seed], streams)
+    for climb in (0, 1, 377):
+        res = engine.sct_climb(ciphers, cof, keys, logs, klens, climb, order=order, kernel="lane",
+                               draws_used=True, last_accept=True, tries_done=True)
+        want_s, want_k, want_last = _oracle_parity(ciphers, cof, klens, seed, streams, logs, climb,
+                                                   order)
+        assert res.scores.tolist() == want_s.tolist(), climb
+        for i in range(m):
+            assert np.array_equal(res.keys[i, :klens[i]].astype(np.int64), want_k[i]), (climb, i)
+        assert np.array_equal(res.last_accept, want_last), climb
+        assert (res.tries_done == climb).all()
+
+
+@pytest.mark.parametrize("order,kmax", [(2, 20), (3, 40), (4, 12)])
+def test_lane_warp_and_speculative_kernels_agree(order, kmax):
+    """All three SCT kernels give identical per-worker outputs, draws consumed included."""
+    rng = np.random.default_rng(600 + order)
+    logs = -rng.random(26**order) * 20 - 1
+    cs = [rng.integers(0, 26, 333) for _ in range(3)]
+    m = 96
+    cof = np.repeat(np.arange(3, dtype=np.int32), 32)
+    klens = rng.integers(2, kmax + 1, m).astype(np.int32)
+    keys = philox_keys([99], list(range(m)))
+    kw = dict(order=order, draws_used=True, last_accept=True, tries_done=True)
+    lane = engine.sct_climb(cs, cof, keys, logs, klens, 700, kernel="lane", **kw)
+    warp = engine.sct_climb(cs, cof, keys, logs, klens, 700, kernel="warp", speculate=False, **kw)
+    spec = engine.sct_climb(cs, cof, keys, logs, klens, 700, kernel="warp", **kw)
+    for other in (warp, spec):
+        assert lane.scores.tolist() == other.scores.tolist()
+        assert np.array_equal(lane.keys, other.keys)
+        assert np.array_equal(lane.draws_used, other.draws_used)
+        assert np.array_equal(lane.last_accept, other.last_accept)
+
+
+def test_lane_kernel_skips_and_trigram_table_in_l2():
+    rng = np.random.default_rng(77)
+    logs = -rng.random(26**3) * 20 - 1
+    cipher = rng.integers(0, 26, 400)
+    m = 40
+    keys = philox_keys([5], list(range(m)))
+    skips = rng.integers(0, 50, m).astype(np.uint64)
+    a = engine.sct_climb([cipher], np.zeros(m, np.int32), keys, logs, 13, 500, order=3,
+                         kernel="lane", skips=skips, draws_used=True)
+    b = engine.sct_climb([cipher], np.zeros(m, np.int32), keys, logs, 13, 500, order=3,
+                         kernel="lane", skips=skips, draws_used=True, table_l2=True)
+    assert np.array_equal(a.scores, b.scores) and np.array_equal(a.keys, b.keys)
+    for i in (0, 7, 39):
+        k, s, _ = O.sct_worker(cipher, logs, 13, 500, 5, i, skip=int(skips[i]), order=3)
+        assert float(a.scores[i]) == s and np.array_equal(a.keys[i].astype(np.int64), k)
+
+
+def test_lane_kernel_golden_acceptance_08(golden):
+    """The reference's own solve_sct output for acceptance #08's input (64 workers x 15,000,
+    frozen in tests/golden) reproduced by the lane kernel, worker by worker."""
+    g = golden.load("sct_solve")
+    cipher = g["cipher"].astype(np.int64)
+    keys = philox_keys([8000], list(range(64)))
+    res = engine.sct_climb([cipher], np.zeros(64, np.int32), keys, golden.english_logs(), 10,
+                           15_000, kernel="lane", group_size=64)
+    assert res.scores.tolist() == g["per_worker"].tolist()
+    assert np.array_equal(res.keys[int(res.group_best[0])], g["best_key"])
+
+
+# ------------------------------------------------------------------ fast mode
+def _fast_oracle(ciphers, cof, klens, seed, streams, q, order, climbings):
+    n = len(cof)
+    scores = np.empty(n, np.int64)
+    keys = [None] * n
+    for i in range(n):
+        k, s, _ = O.sct_fast_worker(ciphers[cof[i]], q, order, int(klens[i]), climbings, seed,
+                                    streams[i])
+        keys[i], scores[i] = k, s
+    return scores, keys
+
+
+@pytest.mark.parametrize("order", [2, 3, 4])
+def test_fast_mode_vs_its_oracle(order):
+    rng = np.random.default_rng(700 + order)
+    lt = cc.LogNgramTable(order, -rng.random(26**order) * 20 - 1, -24.0) if order > 2 else \
+        cc.LogBigramTable(-rng.random(676) * 20 - 1, -24.0)
+    q = cc.quantize_sct_table(lt, text_len=1000)
+    lens = [400, 137, 596, 1000, 33]
+    ciphers = [rng.integers(0, 26, L) for L in lens]
+    m = 80
+    cof = rng.integers(0, len(ciphers), m).astype(np.int32)
+    cof[:32] = 2
+    klens = np.array([int(rng.integers(2, min(64, lens[c]) + 1)) for c in cof], np.int32)
+    streams = list(range(m))
+    keys = philox_keys([31], streams)
+    for climb in (0, 250):
+        res = engine.sct_fast_climb(ciphers, cof, keys, q, klens, climb, group_size=0,
+                                    last_accept=True, draws_used=True)
+        want_s, want_k = _fast_oracle(ciphers, cof, klens, 31, streams, q.table, order, climb)
+        assert res.scores.tolist() == want_s.tolist(), climb
+        for i in range(m):
+            assert np.array_equal(res.keys[i, :klens[i]].astype(np.int64), want_k[i]), (climb, i)
+        # the same stream positions as the parity climb (identical proposals)
+        par = engine.sct_climb(ciphers, cof, keys, lt.logs, klens, climb, order=order,
+                               kernel="lane", draws_used=True)
+        assert np.array_equal(res.draws_used, par.draws_used)
+        if climb:
+            full = np.array([len(ciphers[c]) - order + 1 for c in cof]) * climb
+            assert (res.lookups > 0).all() and (res.lookups <= full).all()
+
+
+@pytest.mark.parametrize("order", [2, 3])
+def test_fast_mode_reduces_to_reference_climb_on_a_dyadic_table(order):
+    """With log-probabilities that are multiples of 2^-10 (>= -24), quantising at shift 10 is
+    exact and every float64 partial sum is exact, so the fast mode's integer fitness is the
+    reference's float64 fitness times 2^10: both climbs take identical decisions."""
+    rng = np.random.default_rng(800 + order)
+    logs = -rng.integers(1, 24 * 1024, 26**order) / 1024.0
+    lt = cc.LogNgramTable(order, logs, -24.0) if order > 2 else cc.LogBigramTable(logs, -24.0)
+    q = cc.quantize_sct_table(lt, text_len=600, max_shift=10)
+    assert q.shift == 10 and np.array_equal(q.table.astype(np.float64), logs * 1024)
+    ciphers = [rng.integers(0, 26, 400), rng.integers(0, 26, 596)]
+    cof = np.repeat(np.array([0, 1], np.int32), 32)
+    klens = np.repeat(np.array([10, 15], np.int32), 32)
+    keys = philox_keys([17], list(range(64)))
+    fast = engine.sct_fast_climb(ciphers, cof, keys, q, klens, 2000, group_size=32)
+    par = engine.sct_climb(ciphers, cof, keys, logs, klens, 2000, order=order, group_size=32)
+    assert np.array_equal(fast.keys, par.keys)
+    assert np.array_equal(fast.scores.astype(np.float64), par.scores * 1024)
+    assert np.array_equal(fast.group_best, par.group_best)
+
+
+def test_fast_mode_validates():
+    lt = cc.LogBigramTable(np.full(676, -10.0), -24.0)
+    q = cc.quantize_sct_table(lt, text_len=100)
+    keys = philox_keys([1], [0])
+    with pytest.raises(ValueError):
+        engine.sct_fast_climb([np.zeros(5, np.int64)], [0], keys, q, 6, 10)  # shorter than key
+    big = cc.QuantizedSctTable(2, np.full(676, -(2**30), np.int32), 30)
+    with pytest.raises(cc.engine._lib.EngineError):
+        engine.sct_fast_climb([np.zeros(50, np.int64)], [0], keys, big, 5, 10)  # int32 overflow

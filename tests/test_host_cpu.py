@@ -343,3 +343,37 @@ def test_bench_reference_arm_covers_the_whole_batch():
     assert r2.returncode == 0, r2.stderr
     lines = [json.loads(x) for x in r2.stdout.splitlines() if x.startswith("{")]
     assert len(lines) == 1 and lines[0]["n_gpus"] == 2
+
+
+def test_quantize_sct_table_shift_and_range():
+    import paper_2103_13937_b200 as cc
+
+    lt = cc.LogBigramTable(-np.random.default_rng(3).random(676) * 20 - 1, -24.0)
+    q = cc.quantize_sct_table(lt, text_len=400)
+    assert q.order == 2 and q.shift == 16 and q.table.dtype == np.int32
+    assert np.array_equal(q.table, np.rint(lt.logs * 2**16).astype(np.int32))
+    assert 399 * int(np.abs(q.table).max()) < 2**31
+    long = cc.quantize_sct_table(lt, text_len=60_000)
+    assert long.shift < 16 and 59_999 * int(np.abs(long.table).max()) < 2**31
+
+
+@pytest.mark.parametrize("order", [2, 3])
+def test_fast_sct_oracle_reduces_to_reference_climb_on_dyadic_tables(order):
+    """The fast mode's definition (cco_sct_fast_worker: quantised integer fitness) takes the
+    reference climb's decisions exactly when the quantisation is exact and float64 sums are
+    exact (log-probabilities that are multiples of 2^-10): keys equal, scores scaled by 2^10.
+    The parity oracle itself is pinned to the reference by test_oracle_golden.py."""
+    import paper_2103_13937_b200 as cc
+
+    rng = np.random.default_rng(90 + order)
+    logs = -rng.integers(1, 24 * 1024, 26**order) / 1024.0
+    lt = cc.LogNgramTable(order, logs, -24.0) if order > 2 else cc.LogBigramTable(logs, -24.0)
+    q = cc.quantize_sct_table(lt, text_len=600, max_shift=10)
+    for k, n in [(5, 200), (10, 400), (17, 333)]:
+        cipher = rng.integers(0, 26, n)
+        fk, fs, fl = O.sct_fast_worker(cipher, q.table, order, k, 1500, 11, k)
+        pk, ps, pl = O.sct_worker(cipher, logs, k, 1500, 11, k, order=order)
+        assert np.array_equal(fk, pk) and fl == pl and fs == ps * 1024
+        # the returned score is the integer fitness of the returned key
+        plain = O.sct_decrypt(cipher, fk)
+        assert fs == O.ngram_score_text(plain, order, q.table)

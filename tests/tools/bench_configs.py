@@ -8,8 +8,8 @@
   C1d the deterministic best-neighbour solver on the same ciphertext (mas.py:140-169),
       R restarts x 500 iterations x 325 candidates.
   C3  SCT, key lengths 5..20, 1,000 ciphertexts of 400 letters, trigram log table (parity
-      mode: float64, numpy pairwise order) -- and, when built, the opt-in quantised
-      incremental mode (engine.sct_climb(..., fast=True)) with its key agreement.
+      mode: float64, numpy pairwise order) -- and the opt-in quantised incremental mode
+      (engine.sct_fast_climb) with its key agreement against the parity mode.
   C4  MAS, 60-100 letter ciphertexts, quadgram (uint16 quantised log table, read via L2),
       one worker per restart.
   C5  evals/s vs workers and n-gram order 2/3/4.
@@ -169,7 +169,7 @@ def c3(bounded=False, quick=False):
     l3 = cc.build_log_ngram_table(cc.build_ngram_table_from_corpus(corpus_text(), 3))
     ciphers, plains, kofc = c3_inputs()
     n_c = len(ciphers)
-    W, K = (8, 1000) if quick else (32, 15_000)  # climbings 15,000
+    W, K = (8, 1000) if quick else (64, 15_000)  # SctSolverConfig defaults (sct.py:47-48)
     cof = np.repeat(np.arange(n_c, dtype=np.int32), W)
     klens = np.repeat(np.array(kofc, dtype=np.int32), W)
     keys = philox_keys([9000], list(range(cof.size)))
