@@ -1123,7 +1123,7 @@ static bool sct_use_warp_family(ccg_ctx* ctx, uint32_t flags, int64_t n_workers,
   if (flags & CCG_FLAG_SCT_KERNEL_WARP) return true;
   if ((flags & CCG_FLAG_SCT_KERNEL_LANE) || n_common < 0) return false;
   // latency mode: few workers of one text length -> the speculative CTA-per-worker kernel
-  if (!(flags & CCG_FLAG_SCT_NO_SPEC) && n_workers <= 4 * (int64_t)ctx->sm_count) return true;
+  if (!(flags & CCG_FLAG_SCT_NO_SPEC) && n_workers <= 16 * (int64_t)ctx->sm_count) return true;
   // one worker per lane needs ~32k workers to fill 148 SMs; below that, and for the larger
   // (L1/L2-resident) trigram/quadgram tables, one warp per worker is as fast or faster
   // (profiles/r2_sct_*: k=10, n=400 -- bigram 1.6e9 vs 1.1e9 at 65k workers, 0.5e9 vs 1.05e9

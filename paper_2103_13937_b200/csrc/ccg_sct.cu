@@ -864,7 +864,7 @@ template <int ORDER>
 static cudaError_t climb_order(cudaStream_t s, const SctLaunch& p, const SumPlan& plan,
                                int sm_count) {
   // latency mode: few enough workers that each can get a CTA of speculating warps
-  if (p.n_workers <= 4 * (int64_t)sm_count && !(p.flags & CCG_FLAG_SCT_NO_SPEC)) {
+  if (p.n_workers <= 16 * (int64_t)sm_count && !(p.flags & CCG_FLAG_SCT_NO_SPEC)) {
     bool launched = false;
     cudaError_t e;
     switch (slots_for(plan)) {

@@ -119,11 +119,16 @@ def solve_stochastic(cipher: MappedText, table: BigramTable, cfg: MasSolverConfi
 
 
 def _batched_restarts(make_batch, restarts: int, workers: int, stop):
-    """Lazily evaluate restarts in device-sized chunks, fold them in order (search.py:61-86).
-    Results equal the sequential reference: restarts are independent of each other and of
-    `stop`, which is still applied restart by restart.  With a `stop` callback the chunks
-    grow 1, 2, 4, ... restarts (a solve usually stops after its first restart, and a small
-    launch finishes sooner); without one, every chunk is a full wave."""
+    """Evaluate restarts in launches of several restarts and fold them in order
+    (search.py:61-86).  Results equal the sequential reference: restarts are independent of
+    each other and of `stop`, which is applied restart by restart in order.
+
+    With a `stop` callback the launches grow 1, 2, 4, ... restarts: a solve usually stops
+    after its first restart, so the first launch is a single restart, and at most one launch
+    ever computes restarts past the stopping one (they are discarded, never reported).
+    Without `stop` every launch is about one full wave.  RestartSummary.elapsed is the wall
+    time of the launch that computed the restart (its restarts ran concurrently for that
+    long), the analogue of the reference's per-restart timing (search.py:75-78)."""
     target = 8192 * max(1, len(engine.devices()))  # workers per chunk: ~one full wave
     chunk = max(1, min(restarts, target // max(1, workers)))
 
@@ -135,7 +140,7 @@ def _batched_restarts(make_batch, restarts: int, workers: int, stop):
             size = min(chunk, 2 * size)
             t0 = time.perf_counter()
             results = make_batch(rs)
-            dt = (time.perf_counter() - t0) / len(rs)
+            dt = time.perf_counter() - t0
             for res in results:
                 yield res, dt
             r += len(rs)

@@ -377,3 +377,26 @@ def test_fast_sct_oracle_reduces_to_reference_climb_on_dyadic_tables(order):
         # the returned score is the integer fitness of the returned key
         plain = O.sct_decrypt(cipher, fk)
         assert fs == O.ngram_score_text(plain, order, q.table)
+
+
+def test_restarts_with_stop_compute_nothing_past_the_stop():
+    """mas._batched_restarts (solve_with_restarts / solve_sct): with `stop`, launches grow
+    1, 2, 4, ... restarts, so at most the stopping restart's launch computes restarts past it
+    (never reported); each elapsed is its launch's wall time (search.py:61-86)."""
+    import time as _t
+
+    from paper_2103_13937_b200.mas import _batched_restarts
+
+    calls = []
+
+    def make_batch(rs):
+        calls.append(list(rs))
+        _t.sleep(0.002 * len(rs))
+        return [cc.SolveResult(np.array([r]), 10 - abs(r - 3), [10 - abs(r - 3)], []) for r in rs]
+
+    best, runs = _batched_restarts(make_batch, 50, 64, stop=lambda res: res.best_score == 10)
+    assert calls == [[0], [1, 2], [3, 4, 5, 6]] and len(runs) == 4 and best.restart_index == 3
+    assert all(r.elapsed >= 0.0015 for r in runs) and runs[3].elapsed >= 0.007
+    calls.clear()
+    best, runs = _batched_restarts(make_batch, 50, 64, stop=None)
+    assert len(runs) == 50 and len(calls) < 50 and best.restart_index == 3
