@@ -1102,6 +1102,9 @@ static int sct_launch_warp(ccg_ctx* ctx, const ccg_sct_climb_args* a, int64_t n)
 // One worker per lane (ccg_sct_lane.cu), parity (mode 0) or fast (mode 1) scoring; texts of
 // any mix of lengths up to max_len.
 static int sct_launch_lane(ccg_ctx* ctx, SctLaneLaunch& p) {
+  if (p.op1_hop > kSctLaneMaxHops || p.op2_hop > kSctLaneMaxHops)
+    return fail(CCG_ERR_UNSUPPORTED, "op hops above %d are not supported by the per-lane SCT "
+                "kernels (one warp per worker takes any)", kSctLaneMaxHops);
   if (p.mode == 0 && p.max_len > kSctMaxLen)
     return fail(CCG_ERR_UNSUPPORTED, "ciphertext of %lld letters exceeds the engine limit %lld",
                 (long long)p.max_len, (long long)kSctMaxLen);
@@ -1119,8 +1122,9 @@ static int sct_launch_lane(ccg_ctx* ctx, SctLaneLaunch& p) {
 }
 
 static bool sct_use_warp_family(ccg_ctx* ctx, uint32_t flags, int64_t n_workers, int64_t n_common,
-                                int order) {
+                                int order, int max_hops) {
   if (flags & CCG_FLAG_SCT_KERNEL_WARP) return true;
+  if (max_hops > kSctLaneMaxHops && n_common >= 0) return true;  // lane kernel's event queue
   if ((flags & CCG_FLAG_SCT_KERNEL_LANE) || n_common < 0) return false;
   // latency mode: few workers of one text length -> the speculative CTA-per-worker kernel
   if (!(flags & CCG_FLAG_SCT_NO_SPEC) && n_workers <= 16 * (int64_t)ctx->sm_count) return true;
@@ -1134,7 +1138,8 @@ static bool sct_use_warp_family(ccg_ctx* ctx, uint32_t flags, int64_t n_workers,
 // n_common: the common text length (-1: mixed lengths); max_len: the longest text
 static int sct_launch(ccg_ctx* ctx, const ccg_sct_climb_args* a, int64_t n_common, int64_t max_len) {
   int rc;
-  if (sct_use_warp_family(ctx, a->flags, a->n_workers, n_common, a->order == 0 ? 2 : a->order)) {
+  if (sct_use_warp_family(ctx, a->flags, a->n_workers, n_common, a->order == 0 ? 2 : a->order,
+                          std::max(a->op1_hop, a->op2_hop))) {
     if ((rc = sct_launch_warp(ctx, a, n_common))) return rc;
   } else {
     if (max_len < a->key_length && !a->key_lengths)

@@ -48,6 +48,7 @@ constexpr int kDS = 32;  // D row stride (int32): D[a][b] sits in bank b
 template <bool TABLE>
 struct alignas(16) DWarp {
   uint64_t rk[22];  // Philox round keys of the current worker's stream (+ M0*k0)
+  int2 uv[kAlpha];  // accept: the (u_x, v_x) row factors of the N update, read by broadcast
   int16_t T[kAlpha * kTS];
   int N[kAlpha * kNS];
   int D[TABLE ? kAlpha * kDS : 4];
@@ -257,13 +258,17 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
       const int na = W.N[a * kNS + y], nb = W.N[b * kNS + y];
       const int ua = __shfl_sync(kFull, u, a), va = __shfl_sync(kFull, v, a);
       const int ub = __shfl_sync(kFull, u, b), vb = __shfl_sync(kFull, v, b);
+      if (lane < kAlpha) W.uv[lane] = make_int2(u, v);
+      // rows whose factors are both zero keep their N row (T is sparse: most letters never
+      // meet a or b); rows a, b are rewritten below from the saved old rows
+      uint32_t rows = __ballot_sync(kFull, lane < kAlpha && (u | v) != 0) & ~((1u << a) | (1u << b));
       __syncwarp();
-      // N'[x][y] = N[sigma x][y] + u_x sb_y + v_x sc_y: rows other than a, b in place,
-      // rows a, b from the saved old rows
-#pragma unroll
-      for (int xx = 0; xx < kAlpha; ++xx) {
-        const int ux = __shfl_sync(kFull, u, xx), vx = __shfl_sync(kFull, v, xx);
-        if (lane < kAlpha) W.N[xx * kNS + y] += ux * sb + vx * sc;
+      // N'[x][y] = N[sigma x][y] + u_x sb_y + v_x sc_y: rows other than a, b in place
+      while (rows) {
+        const int xx = __ffs(rows) - 1;
+        rows &= rows - 1;
+        const int2 q = W.uv[xx];
+        if (lane < kAlpha) W.N[xx * kNS + y] += q.x * sb + q.y * sc;
       }
       if (lane < kAlpha) {
         W.N[a * kNS + y] = nb + ua * sb + va * sc;
@@ -315,9 +320,14 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
       const uint32_t wd = win.round_letters(lane);
       const int c0 = (int)(wd & 0xffu), c1 = (int)((wd >> 8) & 0xffu), c2 = (int)((wd >> 16) & 0xffu);
       // (o <= 128, so all 32 pairs and their redraw partners lie in the 256-draw window)
+      // Lane j + 1's first two letters: after a second redraw the pairs realign on even
+      // draws again, one lane further on (lane 31 has no successor: R <= 31 then).
+      const uint32_t wn = __shfl_down_sync(kFull, wd, 1);
+      const int n0 = (int)(wn & 0xffu), n1 = (int)((wn >> 8) & 0xffu);
       const uint32_t eqA = __ballot_sync(kFull, c0 == c1);
       const uint32_t r0 = eqA ? (uint32_t)(__ffs(eqA) - 1) : 32u;
       uint32_t R = 32u;    // pairs in this round
+      uint32_t r1 = 32u;   // the second redraw pair (shifted alignment), if handled
       bool seq = false;    // the round stopped at a pair that needs the sequential path
       if (r0 < 32u) {
         const int c2r = __shfl_sync(kFull, c2, (int)r0), c0r = __shfl_sync(kFull, c0, (int)r0);
@@ -325,10 +335,22 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
           R = r0;
           seq = true;
         } else {
-          // a second redraw ends the round; the next round starts at that pair, which it
-          // handles as its first-segment redraw (no sequential try needed)
           const uint32_t eqB = __ballot_sync(kFull, c1 == c2) & ~((2u << r0) - 1u);
-          if (eqB) R = (uint32_t)(__ffs(eqB) - 1);
+          if (eqB) {
+            // the second redraw: pair rb = (c1[rb], c1[rb + 1]) unless that is a double
+            // redraw or rb is lane 31 -- then the round ends at rb and the next round
+            // handles it as its first-segment redraw
+            const uint32_t rb = (uint32_t)(__ffs(eqB) - 1);
+            const int a1 = __shfl_sync(kFull, c1, (int)rb), b1 = __shfl_sync(kFull, n1, (int)rb);
+            if (rb == 31u || b1 == a1) {
+              R = rb;
+            } else {
+              r1 = rb;
+              // third segment: lane j > r1 pairs (n0, n1) up to the next redraw
+              const uint32_t eqC = __ballot_sync(kFull, n0 == n1) & ~((2u << r1) - 1u);
+              R = eqC ? min((uint32_t)(__ffs(eqC) - 1), 31u) : 31u;
+            }
+          }
         }
       }
       if (R > climbings - t) {
@@ -336,8 +358,8 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
         seq = false;
       }
       const uint32_t j = (uint32_t)lane;
-      const int pa = j <= r0 ? c0 : c1;
-      const int pb = j < r0 ? c1 : c2;
+      const int pa = j <= r0 ? c0 : (j <= r1 ? c1 : n0);
+      const int pb = j < r0 ? c1 : (j < r1 ? c2 : n1);
       int d;
       if (TABLE) {
         d = j < R ? W.D[pa * kDS + pb] : 0;
@@ -348,7 +370,7 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
       const uint32_t acc = __ballot_sync(kFull, d > 0);
       if (acc == 0) {  // the common case: R rejections
         t += R;
-        win.o += 2u * R + (R > r0 ? 1u : 0u);
+        win.o += 2u * R + (R > r0 ? 1u : 0u) + (R > r1 ? 1u : 0u);
         if (seq && t < climbings) {  // one try through the sequential redraw path
           int a2, b2;
           win.pair(lane, a2, b2);
@@ -367,7 +389,7 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
       const int ak = __shfl_sync(kFull, pa, (int)k), bk = __shfl_sync(kFull, pb, (int)k);
       const int dk = __shfl_sync(kFull, d, (int)k);
       t += k;
-      win.o += 2u * (k + 1u) + (k + 1u > r0 ? 1u : 0u);
+      win.o += 2u * (k + 1u) + (k + 1u > r0 ? 1u : 0u) + (k + 1u > r1 ? 1u : 0u);
       accept(ak, bk, dk);
       last = (int)t;
       ++nacc;

@@ -45,7 +45,11 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kRing = 32;  // draws buffered per lane (power of two)
 constexpr int kParseSteps = 16;  // proposal-parser steps (draws) per lane per round, < kRing - 3
-constexpr int kQueueBytes = 4 * 4 * 4 * 32;  // 4 parsed proposals x 4 words per lane
+// parsed-proposal queue per lane: kQSlots proposals of a header word + up to kSctLaneMaxHops
+// position events (one per swap / block swap; a shift is one event)
+constexpr int kQSlots = 2;
+constexpr int kQWords = 1 + kSctLaneMaxHops;
+constexpr int kQueueBytes = kQSlots * kQWords * 4 * 32;
 
 constexpr int pow26(int o) { return o == 2 ? 676 : o == 3 ? 17576 : 456976; }
 
@@ -441,13 +445,13 @@ __global__ void __launch_bounds__(kSctLaneWarps * 32)
       int st = S_OP, hops = 0, pa = 0, plen = 0, pm = 2, nev = 0, pop = 0;
       int q_head = 0, q_cnt = 0;
       int64_t parsed = 0, done_t = 0, last = -1;
-      auto qword = [&](int slot, int word) -> uint32_t& { return qp[32 * (4 * slot + word)]; };
+      auto qword = [&](int slot, int word) -> uint32_t& { return qp[32 * (kQWords * slot + word)]; };
       auto emit = [&](int x, int y, int l) {
-        qword((q_head + q_cnt) & 3, 1 + nev) = (uint32_t)x | ((uint32_t)y << 8) | ((uint32_t)l << 16);
+        qword((q_head + q_cnt) % kQSlots, 1 + nev) = (uint32_t)x | ((uint32_t)y << 8) | ((uint32_t)l << 16);
         ++nev;
       };
       auto finish = [&]() {
-        qword((q_head + q_cnt) & 3, 0) = (uint32_t)pop | ((uint32_t)nev << 4);
+        qword((q_head + q_cnt) % kQSlots, 0) = (uint32_t)pop | ((uint32_t)nev << 4);
         ++q_cnt;
         ++parsed;
         st = S_OP;
@@ -507,7 +511,7 @@ __global__ void __launch_bounds__(kSctLaneWarps * 32)
         // parse: up to kParseSteps draws per lane (the ring holds more than that after top_up)
         d.top_up(mine && parsed < climbings);
         for (int s = 0; s < kParseSteps; ++s)
-          if (mine && parsed < climbings && q_cnt < 4) step();
+          if (mine && parsed < climbings && q_cnt < kQSlots) step();
         if (!(mine && done_t < climbings && q_cnt > 0)) continue;
         // evaluate the oldest parsed proposal: apply its events to cand
         const uint32_t hdr = qword(q_head, 0);
@@ -542,7 +546,7 @@ __global__ void __launch_bounds__(kSctLaneWarps * 32)
             }
           }
         }
-        q_head = (q_head + 1) & 3;
+        q_head = (q_head + 1) % kQSlots;
         --q_cnt;
         const int64_t t = done_t++;
         // colstart of the candidate: only key positions in [lo, hi) move (the candidate

@@ -192,3 +192,28 @@ def test_fast_mode_validates():
     big = cc.QuantizedSctTable(2, np.full(676, -(2**30), np.int32), 30)
     with pytest.raises(cc.engine._lib.EngineError):
         engine.sct_fast_climb([np.zeros(50, np.int64)], [0], keys, big, 5, 10)  # int32 overflow
+
+
+def test_lane_kernels_take_any_reference_hop_count():
+    """op1_hop / op2_hop up to 7 run on the per-lane kernels (bit-exact); larger hop counts
+    (valid for the reference, sct.py:57-66) take the warp kernel automatically, and the fast
+    mode refuses them loudly."""
+    rng = np.random.default_rng(901)
+    logs = -rng.random(676) * 20 - 1
+    cipher = rng.integers(0, 26, 300)
+    keys = philox_keys([3], list(range(40)))
+    for h1, h2 in [(7, 1), (1, 7), (5, 6)]:
+        res = engine.sct_climb([cipher], np.zeros(40, np.int32), keys, logs, 17, 300, op1_hop=h1,
+                               op2_hop=h2, kernel="lane")
+        want, wk = O.sct_workers([cipher], np.zeros(40, np.int32), [3] * 40, list(range(40)), logs,
+                                 17, 300, op1_hop=h1, op2_hop=h2)
+        assert res.scores.tolist() == want.tolist()
+        assert np.array_equal(res.keys.astype(np.int64), wk)
+    res = engine.sct_climb([cipher], np.zeros(40, np.int32), keys, logs, 17, 300, op1_hop=9,
+                           op2_hop=12)
+    want, _ = O.sct_workers([cipher], np.zeros(40, np.int32), [3] * 40, list(range(40)), logs, 17,
+                            300, op1_hop=9, op2_hop=12)
+    assert res.scores.tolist() == want.tolist()
+    q = cc.quantize_sct_table(cc.LogBigramTable(logs, -24.0), text_len=300)
+    with pytest.raises(cc.engine._lib.EngineError):
+        engine.sct_fast_climb([cipher], np.zeros(40, np.int32), keys, q, 17, 10, op1_hop=9)

@@ -37,7 +37,7 @@ def fuzz_mas(rng, stats):
     cof = rng.integers(0, len(cs), n).astype(np.int32)
     seeds, streams = rng.integers(0, 2**63, n).tolist(), rng.integers(0, 2**63, n).tolist()
     climb = int(rng.choice([1, 2, 17, 500, 2000, 6000]))
-    kern = str(rng.choice(["auto", "dtable", "tform", "packed"]))
+    kern = str(rng.choice(["auto", "dform", "dtable", "tform", "packed"]))
     res = engine.mas_climb(cs, cof, philox_keys(seeds, streams), table, climb, kernel=kern)
     s, m = O.mas_workers(cs, cof, seeds, streams, table, climb)
     if res.scores.tolist() != s.tolist() or not np.array_equal(res.keys.astype(np.int64), m):
@@ -63,28 +63,66 @@ def fuzz_ngram(rng, stats):
 
 
 def fuzz_sct(rng, stats):
-    order = int(rng.choice([2, 2, 3]))
-    n_len = int(rng.choice([6, 64, 129, 400, 777]))
+    order = int(rng.choice([2, 2, 3, 4]))
+    # kernel: speculative CTA / one warp per worker (one text length) or one worker per lane
+    # (any mix of lengths)
+    kernel = str(rng.choice(["warp", "warp", "lane"]))
+    lens = [6, 64, 129, 400, 777]
+    if kernel == "lane":
+        cs = [rng.integers(0, 26, int(rng.choice(lens))) for _ in range(3)]
+    else:
+        n_len = int(rng.choice(lens))
+        cs = [rng.integers(0, 26, n_len) for _ in range(3)]
     logs = -rng.random(26**order) * 20 - 1
-    cs = [rng.integers(0, 26, n_len) for _ in range(3)]
-    m = 48
+    m = int(rng.choice([48, 80]))
     cof = rng.integers(0, 3, m).astype(np.int32)
     kmax = int(rng.choice([8, 20, 32, 64]))  # <= 32: narrow kernel variants
-    klens = rng.integers(2, min(n_len, kmax) + 1, m).astype(np.int32)
+    klens = np.array([int(rng.integers(2, min(cs[c].size, kmax) + 1)) for c in cof], np.int32)
     seeds, streams = rng.integers(0, 2**63, m).tolist(), rng.integers(0, 2**63, m).tolist()
     p1, p2 = sorted(int(v) for v in rng.integers(0, 101, 2))
-    h1, h2 = int(rng.integers(1, 5)), int(rng.integers(1, 5))
+    hmax = 8 if kernel == "lane" else 10  # the lane kernels take up to 7 hops
+    h1, h2 = int(rng.integers(1, hmax)), int(rng.integers(1, hmax))
     climb = int(rng.choice([0, 1, 50, 400]))
     spec = bool(rng.integers(0, 2))  # speculative CTA kernel or one warp per worker
     res = engine.sct_climb(cs, cof, philox_keys(seeds, streams), logs, klens, climb, p1=p1, p2=p2,
-                           op1_hop=h1, op2_hop=h2, order=order, speculate=spec)
+                           op1_hop=h1, op2_hop=h2, order=order, speculate=spec, kernel=kernel)
     for i in range(m):
         k = int(klens[i])
         key, score, _ = O.sct_worker(cs[cof[i]], logs, k, climb, seeds[i], streams[i], p1=p1,
                                      p2=p2, op1_hop=h1, op2_hop=h2, order=order)
         if float(res.scores[i]) != score or not np.array_equal(res.keys[i, :k].astype(np.int64), key):
-            raise AssertionError(f"SCT mismatch: order={order} n={n_len} k={k} climb={climb}")
+            raise AssertionError(f"SCT mismatch: kernel={kernel} order={order} k={k} climb={climb}")
     stats["sct_workers"] += m
+    stats["sct_lane_workers" if kernel == "lane" else "sct_warp_workers"] += m
+
+
+def fuzz_sct_fast(rng, stats):
+    """The opt-in fast SCT mode (quantised, incremental) vs its full-rescore oracle."""
+    import paper_2103_13937_b200 as cc
+
+    order = int(rng.choice([2, 3, 4]))
+    logs = -rng.random(26**order) * float(rng.choice([2, 20])) - 1
+    lt = cc.LogNgramTable(order, logs, -30.0) if order > 2 else cc.LogBigramTable(logs, -30.0)
+    q = cc.quantize_sct_table(lt, text_len=1000, max_shift=int(rng.choice([4, 10, 16])))
+    cs = [rng.integers(0, int(rng.choice([3, 26])), int(rng.choice([5, 64, 129, 400, 1000])))
+          for _ in range(3)]
+    m = 64
+    cof = rng.integers(0, 3, m).astype(np.int32)
+    kmax = int(rng.choice([8, 20, 64]))
+    klens = np.array([int(rng.integers(2, min(cs[c].size, kmax) + 1)) for c in cof], np.int32)
+    seeds, streams = rng.integers(0, 2**63, m).tolist(), rng.integers(0, 2**63, m).tolist()
+    p1, p2 = sorted(int(v) for v in rng.integers(0, 101, 2))
+    h1, h2 = int(rng.integers(1, 8)), int(rng.integers(1, 8))
+    climb = int(rng.choice([0, 1, 60, 400]))
+    res = engine.sct_fast_climb(cs, cof, philox_keys(seeds, streams), q, klens, climb, p1=p1,
+                                p2=p2, op1_hop=h1, op2_hop=h2)
+    for i in range(m):
+        k = int(klens[i])
+        key, score, _ = O.sct_fast_worker(cs[cof[i]], q.table, order, k, climb, seeds[i],
+                                          streams[i], p1=p1, p2=p2, op1_hop=h1, op2_hop=h2)
+        if int(res.scores[i]) != score or not np.array_equal(res.keys[i, :k].astype(np.int64), key):
+            raise AssertionError(f"SCT fast mismatch: order={order} k={k} climb={climb}")
+    stats["sct_fast_workers"] += m
 
 
 def fuzz_det(rng, stats):
@@ -111,10 +149,10 @@ def main():
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     stats = {"rounds": 0, "mas_workers": 0, "mas_tries": 0, "ngram_workers": 0, "sct_workers": 0,
-             "det_jobs": 0}
+             "sct_warp_workers": 0, "sct_lane_workers": 0, "sct_fast_workers": 0, "det_jobs": 0}
     t0 = time.time()
     while time.time() - t0 < a.seconds:
-        for f in (fuzz_mas, fuzz_ngram, fuzz_sct, fuzz_det):
+        for f in (fuzz_mas, fuzz_ngram, fuzz_sct, fuzz_sct_fast, fuzz_det):
             f(rng, stats)
         stats["rounds"] += 1
     stats["seconds"] = round(time.time() - t0, 1)
