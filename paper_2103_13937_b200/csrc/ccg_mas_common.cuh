@@ -125,8 +125,21 @@ struct ByteWindow2 {
       philox4x64_10_rk(rk, block + 1, v0, v1, v2, v3);
     else
       philox4x64_10(__ldg(key), __ldg(key + 1), block + 1, v0, v1, v2, v3);
-    return int_below_tiny(v0, 26) | (int_below_tiny(v1, 26) << 8) |
-           (int_below_tiny(v2, 26) << 16) | (int_below_tiny(v3, 26) << 24);
+    return letters4(v0, v1, v2, v3);
+  }
+  // int(u*26) of four words, one byte each: the 32-bit products decide all four unless one
+  // lies within 26 of wrapping (probability ~2^-25 per word), when the exact path runs
+  __device__ __forceinline__ static uint32_t letters4(uint64_t v0, uint64_t v1, uint64_t v2,
+                                                      uint64_t v3) {
+    const uint64_t A0 = (uint64_t)(uint32_t)(v0 >> 32) * 26u, A1 = (uint64_t)(uint32_t)(v1 >> 32) * 26u;
+    const uint64_t A2 = (uint64_t)(uint32_t)(v2 >> 32) * 26u, A3 = (uint64_t)(uint32_t)(v3 >> 32) * 26u;
+    const uint32_t hi = max(max((uint32_t)A0, (uint32_t)A1), max((uint32_t)A2, (uint32_t)A3));
+    if (hi >= 0u - 26u)
+      return int_below_tiny(v0, 26) | (int_below_tiny(v1, 26) << 8) |
+             (int_below_tiny(v2, 26) << 16) | (int_below_tiny(v3, 26) << 24);
+    const uint32_t q01 = __byte_perm((uint32_t)(A0 >> 32), (uint32_t)(A1 >> 32), 0x0040);
+    const uint32_t q23 = __byte_perm((uint32_t)(A2 >> 32), (uint32_t)(A3 >> 32), 0x0040);
+    return __byte_perm(q01, q23, 0x5410);
   }
   __device__ __forceinline__ void start(uint64_t pos, int lane) {
     base = pos & ~3ULL;

@@ -40,7 +40,11 @@ namespace {
 
 constexpr int kDWarps = 8;
 constexpr int kTS = 34;  // T row stride (int16): column walks are conflict-free (17 words/row)
-constexpr int kNS = 33;  // N row stride (int32)
+constexpr int kNS = 33;  // S row stride (int32)
+// N is stored TRANSPOSED: lane y's column N[.][y] is the contiguous row NT[y][.], stride 36
+// words (16-byte aligned), so the accept's rank-2 update streams it with 128-bit loads and
+// stores (each 8-lane phase of an LDS.128 hits distinct banks: 4y + x mod 32)
+constexpr int kNT = 36;
 constexpr int kDS = 32;  // D row stride (int32): D[a][b] sits in bank b
 
 // TABLE = true keeps D in shared memory (rebuilt on every accept); TABLE = false computes
@@ -48,9 +52,9 @@ constexpr int kDS = 32;  // D row stride (int32): D[a][b] sits in bank b
 template <bool TABLE>
 struct alignas(16) DWarp {
   uint64_t rk[22];  // Philox round keys of the current worker's stream (+ M0*k0)
-  int2 uv[kAlpha];  // accept: the (u_x, v_x) row factors of the N update, read by broadcast
-  int16_t T[kAlpha * kTS];
-  int N[kAlpha * kNS];
+  int2 uv[28];      // accept: the (u_x, v_x) row factors of the N update (x < 26; 26, 27 pad)
+  int16_t T[kAlpha * kTS + 4];  // (+4: N starts 16-byte aligned)
+  int N[kAlpha * kNT];          // N[x][y] at N[y * kNT + x]
   int D[TABLE ? kAlpha * kDS : 4];
 };
 template <bool TABLE>
@@ -64,8 +68,8 @@ struct DBlock {
 // ciphertext), computed once per ciphertext by dform_init_kernel when several workers share
 // a ciphertext: T and N in the shared-memory layout, and the score.
 struct alignas(16) CipherInit {
-  int16_t T[kAlpha * kTS];
-  int N[kAlpha * kNS];
+  int16_t T[kAlpha * kTS + 4];
+  int N[kAlpha * kNT];
   int score;
   int pad_[3];
 };
@@ -89,12 +93,12 @@ template <class BT, class WT>
 __device__ __forceinline__ void rebuild_D(const BT& B, WT& W, int lane) {
   __syncwarp();
   const int y = lane < kAlpha ? lane : 0;
-  const int tyy = t_at(W, y, y), nyy = W.N[y * kNS + y];
+  const int tyy = t_at(W, y, y), nyy = W.N[y * kNT + y];
 #pragma unroll
   for (int x = 0; x < kAlpha; ++x) {
     const int txx = __shfl_sync(kFull, tyy, x), nxx = __shfl_sync(kFull, nyy, x);
     const int kt = txx + tyy - t_at(W, x, y) - t_at(W, y, x);
-    const int dv = kt * B.KS[x * kDS + y] - nxx - nyy + W.N[x * kNS + y] + W.N[y * kNS + x];
+    const int dv = kt * B.KS[x * kDS + y] - nxx - nyy + W.N[y * kNT + x] + W.N[x * kNT + y];
     if (lane < kAlpha) W.D[x * kDS + y] = dv;
   }
   __syncwarp();
@@ -108,7 +112,7 @@ __device__ __forceinline__ int delta_at(uint32_t ks_s, const WT& W, int tdg, int
   const int kt = ta + tb - t_at(W, a, b) - t_at(W, b, a);
   // ks through a 32-bit shared address (a generic B.KS access recomputes the window base)
   const int ks = (int)lds_u32(ks_s + 4u * (uint32_t)(a * kDS + b));
-  return kt * ks - na - nb + W.N[a * kNS + b] + W.N[b * kNS + a];
+  return kt * ks - na - nb + W.N[b * kNT + a] + W.N[a * kNT + b];
 }
 
 // max over the 325 on-demand deltas; lane y scans column y
@@ -148,7 +152,7 @@ __device__ __forceinline__ int64_t initial_state(const BT& B, WT& W, const uint8
       int acc = 0;
       for (int q = 0; q < kAlpha; ++q)
         acc += t_at(W, x, q) * B.S[y * kNS + q] + t_at(W, q, x) * B.S[q * kNS + y];
-      W.N[x * kNS + y] = acc;
+      W.N[y * kNT + x] = acc;
       part += t_at(W, x, y) * B.S[x * kNS + y];
     }
   }
@@ -232,7 +236,7 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
     } else {
       __syncwarp();
       tdg = t_at(W, y, y);
-      ndg = W.N[y * kNS + y];
+      ndg = W.N[y * kNT + y];
     }
 
     int pv = lane < kAlpha ? lane : 0;  // pi(lane): cipher letter -> plaintext letter
@@ -255,24 +259,28 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
       // lane y: S-column factors of its N column
       const int sb = B.S[y * kNS + b] - B.S[y * kNS + a];
       const int sc = B.S[b * kNS + y] - B.S[a * kNS + y];
-      const int na = W.N[a * kNS + y], nb = W.N[b * kNS + y];
+      const int na = W.N[y * kNT + a], nb = W.N[y * kNT + b];
       const int ua = __shfl_sync(kFull, u, a), va = __shfl_sync(kFull, v, a);
       const int ub = __shfl_sync(kFull, u, b), vb = __shfl_sync(kFull, v, b);
-      if (lane < kAlpha) W.uv[lane] = make_int2(u, v);
-      // rows whose factors are both zero keep their N row (T is sparse: most letters never
-      // meet a or b); rows a, b are rewritten below from the saved old rows
-      uint32_t rows = __ballot_sync(kFull, lane < kAlpha && (u | v) != 0) & ~((1u << a) | (1u << b));
+      if (lane < 28) W.uv[lane] = lane < kAlpha ? make_int2(u, v) : make_int2(0, 0);
       __syncwarp();
-      // N'[x][y] = N[sigma x][y] + u_x sb_y + v_x sc_y: rows other than a, b in place
-      while (rows) {
-        const int xx = __ffs(rows) - 1;
-        rows &= rows - 1;
-        const int2 q = W.uv[xx];
-        if (lane < kAlpha) W.N[xx * kNS + y] += q.x * sb + q.y * sc;
-      }
+      // N'[x][y] = N[sigma x][y] + u_x sb_y + v_x sc_y: lane y streams its column 4 entries
+      // at a time (entries a, b are rewritten below from the saved old values)
       if (lane < kAlpha) {
-        W.N[a * kNS + y] = nb + ua * sb + va * sc;
-        W.N[b * kNS + y] = na + ub * sb + vb * sc;
+        int4* col = reinterpret_cast<int4*>(W.N + y * kNT);
+        const int4* f = reinterpret_cast<const int4*>(W.uv);
+#pragma unroll
+        for (int c = 0; c < 7; ++c) {
+          int4 nv = col[c];
+          const int4 q0 = f[2 * c], q1 = f[2 * c + 1];
+          nv.x += q0.x * sb + q0.y * sc;
+          nv.y += q0.z * sb + q0.w * sc;
+          nv.z += q1.x * sb + q1.y * sc;
+          nv.w += q1.z * sb + q1.w * sc;
+          col[c] = nv;
+        }
+        W.N[y * kNT + a] = nb + ua * sb + va * sc;
+        W.N[y * kNT + b] = na + ub * sb + vb * sc;
       }
       // swap rows a, b then columns a, b of T
       int16_t ra = 0, rb = 0;
@@ -300,7 +308,7 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
       } else {
         __syncwarp();
         tdg = t_at(W, y, y);
-        ndg = W.N[y * kNS + y];
+        ndg = W.N[y * kNT + y];
       }
     };
     auto optimum = [&]() {
