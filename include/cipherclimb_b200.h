@@ -190,6 +190,8 @@ typedef struct {
   uint32_t flags;
   int64_t *computed;          /* [n_workers] deltas computed by a position walk (the other tries
                                  read the delta cache of the unchanged state), or NULL */
+  int64_t *lookups;           /* [n_workers] n-gram table reads (walks + accepted refreshes), or
+                                 NULL -- the roofline's per-eval traffic for L2-resident tables */
 } ccg_mas_ngram_args;
 
 int ccg_mas_ngram_climb(ccg_ctx *ctx, const ccg_mas_ngram_args *args);
@@ -322,6 +324,9 @@ int ccg_encrypt_batch(ccg_ctx *ctx, int32_t kind, const uint8_t *texts, const in
 
 /* Roofline denominator: measured shared-memory (LDS) bandwidth of this device, bytes/s. */
 int ccg_bench_smem_bandwidth(ccg_ctx *ctx, double *out_bytes_per_s);
+/* Roofline denominator of L2-resident tables (the quadgram MAS climb): random 16-bit gathers
+ * per second from a table of `table_entries` uint16 (26^4 for quadgrams, 914 KB). */
+int ccg_bench_l2_gather(ccg_ctx *ctx, int64_t table_entries, double *out_gathers_per_s);
 
 #ifdef __cplusplus
 }

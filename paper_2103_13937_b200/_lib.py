@@ -74,7 +74,7 @@ class MasNgramArgs(C.Structure):
         ("skips", _P), ("n_workers", _i64), ("climbings", _i64), ("order", _i32), ("table", _P),
         ("scores", _P), ("maps", _P), ("draws_used", _P), ("last_accept", _P),
         ("tries_done", _P), ("group_size", _i32), ("group_best", _P), ("max_len", _i64),
-        ("flags", _u32), ("computed", _P),
+        ("flags", _u32), ("computed", _P), ("lookups", _P),
     ]
 
 
@@ -127,6 +127,7 @@ EXPORTS = {
     "ccg_sct_fast_climb": (C.c_int, [_P, C.POINTER(SctFastArgs)]),
     "ccg_encrypt_batch": (C.c_int, [_P, _i32, _P, _P, _i64, _P, _P, _i32, _P, _P]),
     "ccg_bench_smem_bandwidth": (C.c_int, [_P, _P]),
+    "ccg_bench_l2_gather": (C.c_int, [_P, _i64, _P]),
 }
 
 _lib = None

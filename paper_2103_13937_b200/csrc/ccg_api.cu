@@ -712,6 +712,7 @@ static int ngram_launch(ccg_ctx* ctx, const ccg_mas_ngram_args* a, int64_t max_l
   p.last_accept = a->last_accept;
   p.tries_done = a->tries_done;
   p.computed = a->computed;
+  p.lookups = a->lookups;
   p.flags = a->flags;
   if (int rc = ctx->tickets(&p.tickets)) return rc;
   ctx->launches++;
@@ -794,6 +795,10 @@ int ccg_mas_ngram_climb(ccg_ctx* ctx, const ccg_mas_ngram_args* a) {
     if ((rc = ctx->buf(12, (size_t)nw * 8, &p))) return rc;
     d.computed = (int64_t*)p;
   }
+  if (a->lookups) {
+    if ((rc = ctx->buf(13, (size_t)nw * 8, &p))) return rc;
+    d.lookups = (int64_t*)p;
+  }
   const int64_t ng = a->group_size > 0 ? nw / a->group_size : 0;
   if (a->group_best && ng) {
     if ((rc = ctx->buf(11, (size_t)ng * 8, &p))) return rc;
@@ -809,6 +814,7 @@ int ccg_mas_ngram_climb(ccg_ctx* ctx, const ccg_mas_ngram_args* a) {
     return rc;
   if (a->tries_done && (rc = download(ctx, a->tries_done, d.tries_done, (size_t)nw * 8))) return rc;
   if (a->computed && (rc = download(ctx, a->computed, d.computed, (size_t)nw * 8))) return rc;
+  if (a->lookups && (rc = download(ctx, a->lookups, d.lookups, (size_t)nw * 8))) return rc;
   if (ng && a->group_best && (rc = download(ctx, a->group_best, d.group_best, (size_t)ng * 8)))
     return rc;
   return finish(ctx, cudaSuccess, "mas_ngram_climb");
@@ -1421,6 +1427,17 @@ int ccg_bench_smem_bandwidth(ccg_ctx* ctx, double* out_bytes_per_s) {
   ctx->launches += 2;
   cudaError_t e = bench_smem_bandwidth(ctx->stream, ctx->sm_count, out_bytes_per_s);
   if (e != cudaSuccess) return cuda_fail(e, "smem bandwidth kernel");
+  return CCG_OK;
+}
+
+int ccg_bench_l2_gather(ccg_ctx* ctx, int64_t table_entries, double* out_gathers_per_s) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (!out_gathers_per_s || table_entries < 1 || table_entries > (int64_t)1 << 31)
+    return fail(CCG_ERR_INVALID, "bad arguments");
+  ctx->launches += 2;
+  cudaError_t e = bench_l2_gather(ctx->stream, ctx->sm_count, table_entries, out_gathers_per_s);
+  if (e != cudaSuccess) return cuda_fail(e, "L2 gather kernel");
   return CCG_OK;
 }
 

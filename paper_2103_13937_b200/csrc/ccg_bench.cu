@@ -34,7 +34,61 @@ __global__ void __launch_bounds__(kBenchThreads) smem_bw_kernel(int iters, uint3
   if (acc == 0x12345678u) sink[blockIdx.x] = acc;
 }
 
+// Random 16-bit gathers from a global table (the quadgram table of the n-gram climb: 26^4
+// uint16 = 914 KB, L2-resident, larger than L1): every thread walks 8 independent
+// xorshift index streams so the L1/L2 request queues stay full.  Reported as gathers/s
+// (each touches one 32-byte sector).
+__global__ void __launch_bounds__(256) l2_gather_kernel(const uint16_t* __restrict__ tab, uint32_t n,
+                                                        int iters, uint32_t* sink) {
+  uint32_t x[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) x[u] = (blockIdx.x * blockDim.x + threadIdx.x) * 8u + u + 0x9e3779b9u;
+  uint32_t acc = 0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      x[u] ^= x[u] << 13;
+      x[u] ^= x[u] >> 17;
+      x[u] ^= x[u] << 5;
+      acc += __ldg(tab + __umulhi(x[u], n));
+    }
+  }
+  if (acc == 0x12345678u) sink[blockIdx.x] = acc;
+}
+
 }  // namespace
+
+cudaError_t bench_l2_gather(cudaStream_t s, int sm_count, int64_t entries, double* gathers_per_s) {
+  uint16_t* tab = nullptr;
+  uint32_t* sink = nullptr;
+  cudaError_t e = cudaMalloc(&tab, (size_t)entries * 2);
+  if (e != cudaSuccess) return e;
+  e = cudaMalloc(&sink, sizeof(uint32_t) * sm_count * 8);
+  if (e != cudaSuccess) {
+    cudaFree(tab);
+    return e;
+  }
+  cudaMemsetAsync(tab, 1, (size_t)entries * 2, s);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int grid = sm_count * 8;  // 8 x 256 threads = full occupancy
+  const int iters = 512;
+  l2_gather_kernel<<<grid, 256, 0, s>>>(tab, (uint32_t)entries, 16, sink);  // warm-up: table into L2
+  cudaEventRecord(a, s);
+  l2_gather_kernel<<<grid, 256, 0, s>>>(tab, (uint32_t)entries, iters, sink);
+  cudaEventRecord(b, s);
+  e = cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  *gathers_per_s = (double)grid * 256 * iters * 8 / (ms * 1e-3);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  cudaFree(tab);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return e;
+}
 
 cudaError_t bench_smem_bandwidth(cudaStream_t s, int sm_count, double* bytes_per_s) {
   uint32_t* sink = nullptr;

@@ -59,6 +59,7 @@ struct MasNgramLaunch {
   uint32_t flags;
   int64_t* computed;
   unsigned long long* tickets;  // worker ticket counter, zero at launch (or NULL)
+  int64_t* lookups;             // table reads per worker (or NULL)
 };
 
 // Deterministic best-neighbour MAS (ccg_mas_det.cu): one job = one (ciphertext, restart).
@@ -227,5 +228,6 @@ cudaError_t launch_encrypt(cudaStream_t s, int kind, const uint8_t* texts, const
                            uint8_t* keys, int kmax, uint8_t* out);
 
 cudaError_t bench_smem_bandwidth(cudaStream_t s, int sm_count, double* bytes_per_s);
+cudaError_t bench_l2_gather(cudaStream_t s, int sm_count, int64_t entries, double* gathers_per_s);
 
 }  // namespace ccg

@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
     for (int i = lane; i < 676 / 2; i += 32) reinterpret_cast<uint32_t*>(dtag)[i] = 0u;
     uint32_t epoch = 1;
     int64_t walks = 0;  // deltas computed by a position walk (the rest came from the cache)
+    uint32_t reads = 0;  // this lane's table reads (G per walked position / refreshed window)
     __syncwarp();
 
     ByteWindow2 win;
@@ -265,8 +266,10 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
       const uint32_t arep = ma * 0x01010101u, brep = mb * 0x01010101u;
       walks += __popc(__ballot_sync(kFull, valid));
       int d = 0;
-      for (int j = lane - lo_lane; j < mcnt; j += hi_lane - lo_lane)
+      for (int j = lane - lo_lane; j < mcnt; j += hi_lane - lo_lane) {
         d += st.position_delta(st.touched(j, msa, mna, msb), arep, brep);
+        reads += G;
+      }
       // per-walk sums: an inclusive warp scan, differenced at each walk's lane range
       int sc = d;
 #pragma unroll
@@ -297,7 +300,10 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
       if (dtag[key] == epoch) return dcache[key];
       ++walks;
       int d = 0;
-      for (int j = lane; j < na + nb; j += 32) d += st.position_delta(st.touched(j, sa, na, sb), arep, brep);
+      for (int j = lane; j < na + nb; j += 32) {
+        d += st.position_delta(st.touched(j, sa, na, sb), arep, brep);
+        reads += G;
+      }
       d = (int)__reduce_add_sync(kFull, (uint32_t)d);
       __syncwarp();  // every lane's tag read precedes the write
       if (lane == 0) {
@@ -329,6 +335,7 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
 #pragma unroll
             for (int q = 0; q < G; ++q) idx = idx * kAlpha + text[4 + s0 + q];
             ws[s0] = (uint16_t)st.lookup(idx);
+            ++reads;
           }
         }
       }
@@ -444,7 +451,9 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
       }
     }
     if (lane < kAlpha && p.maps) p.maps[w * kAlpha + pinv] = (uint8_t)lane;
+    const uint32_t all_reads = p.lookups ? __reduce_add_sync(kFull, reads) : 0u;
     if (lane == 0) {
+      if (p.lookups) p.lookups[w] = (int64_t)all_reads;
       p.scores[w] = score;
       if (p.draws_used) p.draws_used[w] = win.position();
       if (p.last_accept) p.last_accept[w] = last;

@@ -96,7 +96,7 @@ def _concat(parts, name):
 def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, group_size=0,
               draws_used=False, last_accept=False, tries_done=False, early_exit=False,
               order=2, ngram_kernel=False, kernel="auto", accepts=False, computed=False,
-              out: ClimbResult | None = None, devices_=None) -> ClimbResult:
+              lookups=False, out: ClimbResult | None = None, devices_=None) -> ClimbResult:
     """Run stochastic_worker (mas.py:218-244) for every worker on the GPU(s).
 
     ciphers: list of letter arrays; cipher_of: int per worker; keys: uint64[n, 2] Philox
@@ -151,6 +151,7 @@ def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, 
                 launches=0,
                 accepts=np.empty(m, dtype=np.int64) if (accepts and not use_ng) else None,
                 computed=np.empty(m, dtype=np.int64) if (computed and use_ng) else None,
+                lookups=np.empty(m, dtype=np.int64) if (lookups and use_ng) else None,
             )
         if m == 0:
             return out
@@ -171,6 +172,7 @@ def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, 
         if use_ng:
             a.order = order
             a.computed = _lib.ptr(out.computed)
+            a.lookups = _lib.ptr(out.lookups)
         ctx = _lib.context(dev)
         with ctx.lock:
             before = ctx.launches()
@@ -188,7 +190,7 @@ def mas_climb(ciphers, cipher_of, keys, table_scores, climbings, *, skips=None, 
         group_best=_concat(parts, "group_best"), draws_used=_concat(parts, "draws_used"),
         last_accept=_concat(parts, "last_accept"), tries_done=_concat(parts, "tries_done"),
         launches=sum(p.launches for p in parts), accepts=_concat(parts, "accepts"),
-        computed=_concat(parts, "computed"),
+        computed=_concat(parts, "computed"), lookups=_concat(parts, "lookups"),
     )
 
 
@@ -419,6 +421,30 @@ def mas_det_step_batch(texts, pivots, table_scores) -> np.ndarray:
                                                       off.size - 1, _lib.ptr(pv), _lib.ptr(table),
                                                       _lib.ptr(out)), "det_step")
     return out
+
+
+def bench_smem_bandwidth(device=None) -> float:
+    """Measured conflict-free LDS bandwidth of the device, bytes/s (roofline denominator)."""
+    import ctypes as C
+
+    out = C.c_double(0.0)
+    ctx = _lib.context(default_device() if device is None else device)
+    with ctx.lock:
+        _lib.check(_lib.load().ccg_bench_smem_bandwidth(ctx.handle, C.byref(out)), "smem bench")
+    return out.value
+
+
+def bench_l2_gather(entries: int = 26**4, device=None) -> float:
+    """Measured random uint16 gathers/s from an L2-resident table of `entries` entries (the
+    quadgram table by default): the roofline denominator of the n-gram climb at order 4."""
+    import ctypes as C
+
+    out = C.c_double(0.0)
+    ctx = _lib.context(default_device() if device is None else device)
+    with ctx.lock:
+        _lib.check(_lib.load().ccg_bench_l2_gather(ctx.handle, int(entries), C.byref(out)),
+                   "L2 gather bench")
+    return out.value
 
 
 class JobHistories(collections.abc.Sequence):

@@ -865,3 +865,18 @@ def test_worker_tickets_with_more_workers_than_resident_warps():
     for i in sample[:16]:
         _, want, _ = O.sct_worker(sc[scof[i]], logs, 9, 40, seeds[i], streams[i])
         assert float(res.scores[i]) == want
+
+
+def test_ngram_lookups_counter_and_l2_microbench():
+    """The n-gram climb's table-read counter (the C4 roofline numerator) is consistent with its
+    walk counter, does not change any result, and the L2 gather microbenchmark runs."""
+    rng = np.random.default_rng(4040)
+    table = rng.integers(0, 65536, 26**4)
+    cs = [rng.integers(0, 26, int(L)) for L in (60, 80, 100)]
+    cof = np.repeat(np.arange(3, dtype=np.int32), 64)
+    keys = philox_keys([9], list(range(cof.size)))
+    a = engine.mas_climb(cs, cof, keys, table, 2000, order=4, computed=True, lookups=True)
+    b = engine.mas_climb(cs, cof, keys, table, 2000, order=4)
+    assert np.array_equal(a.scores, b.scores) and np.array_equal(a.keys, b.keys)
+    assert (a.lookups >= 4 * a.computed).all() and a.lookups.sum() > 0
+    assert engine.bench_l2_gather(26**4) > 1e10

@@ -273,7 +273,7 @@ def c4(bounded=False, quick=False):
     cof = np.repeat(np.arange(n_c, dtype=np.int32), R)
     keys = philox_keys([4000], list(range(cof.size)))
     res, dt = timed(lambda: engine.mas_climb(ciphers, cof, keys, q4.scores, K, order=4,
-                                             group_size=R, computed=True))
+                                             group_size=R, computed=True, lookups=True))
     evals = cof.size * K
     ok = sum(np.array_equal(res.keys[j * R + int(res.group_best[j])].astype(np.int64)[ciphers[j]],
                             plains[j]) for j in range(n_c))
@@ -288,10 +288,19 @@ def c4(bounded=False, quick=False):
     exact = bool(np.array_equal(ws, res.scores[idx])
                  and np.array_equal(wm, res.keys[idx].astype(np.int64)))
     walks = float(res.computed.sum() / evals)
+    lpe = float(res.lookups.sum() / evals)
+    peak = engine.bench_l2_gather(26**4)
+    roof = {"bound": "l2-gather", "lookups_per_eval": lpe, "achieved": evals / dt * lpe,
+            "peak": peak, "unit": "gathers/s", "frac": evals / dt * lpe / peak,
+            "peak_source": "ccg_bench_l2_gather: random uint16 gathers from a 26^4-entry "
+                           "(914 KB) table at full occupancy, measured in this run",
+            "note": "quadgram table reads executed by the climb (position walks of cache "
+                    "misses + window refreshes after accepts, counted on the device); the "
+                    "wall time also includes the H2D/D2H of the public API call"}
     return {"config": "C4", "what": "MAS 60-100 letters, quadgram uint16 table via L2, one "
                                     "worker per restart", "ciphers": n_c,
             "restarts_per_cipher": R, "climbings": K, "evals": evals, "seconds": dt,
-            "evals_per_s": evals / dt, "computed_by_walk": walks,
+            "evals_per_s": evals / dt, "computed_by_walk": walks, "roofline": roof,
             "recovered": int(ok), "of": n_c, "cpu_evals_per_s": rate_cpu, "cpu_cores": THREADS,
             "cpu_kind": "port (full rescore per try)",
             "parity": {"bit_exact": exact, "sample": "512 workers (first 256 of the first and "
