@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Small runs of every climb kernel for compute-sanitizer (memcheck / racecheck / synccheck):
-D-form / T-form / packed MAS, n-gram orders 2-4, deterministic MAS, SCT warp and speculative
-kernels.  Checks results against the oracle as well."""
+D-form / T-form / packed MAS, n-gram orders 2-4 (with the table-read counter), deterministic
+MAS, SCT warp / speculative / per-lane kernels (ragged text lengths, orders 2-4) and the fast
+SCT mode; the L2 / smem microbenchmarks.  Checks results against the oracle as well."""
 import sys
 from pathlib import Path
 
@@ -42,6 +43,28 @@ for spec in (True, False):
     for i in range(4):
         _, s, _ = O.sct_worker(sc_c[sc_cof[i]], logs, 9, 60, 4, i)
         assert float(r.scores[i]) == s, (spec, i)
+# per-lane SCT kernels: parity (orders 2-4, ragged lengths, a chunk spanning ciphertexts) and
+# the fast mode
+lane_c = [rng.integers(0, 26, int(L)) for L in (200, 57, 333)]
+lane_cof = np.array([0] * 20 + [1, 2] * 10 + [2] * 5, np.int32)
+lane_k = np.array([int(rng.integers(2, 12)) for _ in lane_cof], np.int32)
+lane_keys = philox_keys([6] * lane_cof.size, list(range(lane_cof.size)))
+for order in (2, 3, 4):
+    lg = -rng.random(26**order) * 20 - 1
+    r = engine.sct_climb(lane_c, lane_cof, lane_keys, lg, lane_k, 40, order=order, kernel="lane")
+    for i in (0, 21, 44):
+        _, s, _ = O.sct_worker(lane_c[lane_cof[i]], lg, int(lane_k[i]), 40, 6, i, order=order)
+        assert float(r.scores[i]) == s, (order, i)
+    import paper_2103_13937_b200 as cc  # noqa: E402
+    lt = cc.LogNgramTable(order, lg, -30.0) if order > 2 else cc.LogBigramTable(lg, -30.0)
+    q = cc.quantize_sct_table(lt, text_len=400)
+    r = engine.sct_fast_climb(lane_c, lane_cof, lane_keys, q, lane_k, 40)
+    for i in (0, 21, 44):
+        _, s, _ = O.sct_fast_worker(lane_c[lane_cof[i]], q.table, order, int(lane_k[i]), 40, 6, i)
+        assert int(r.scores[i]) == s, (order, i)
+t4 = rng.integers(0, 60000, 26**4)
+engine.mas_climb(cs, cof, keys, t4, 200, order=4, computed=True, lookups=True)
+engine.bench_l2_gather(26**4)
 # scoring / delta / test-set kernels
 from paper_2103_13937_b200 import ciphers as C  # noqa: E402
 from paper_2103_13937_b200 import rng as R  # noqa: E402
