@@ -1134,11 +1134,11 @@ static bool sct_use_warp_family(ccg_ctx* ctx, uint32_t flags, int64_t n_workers,
   if ((flags & CCG_FLAG_SCT_KERNEL_LANE) || n_common < 0) return false;
   // latency mode: few workers of one text length -> the speculative CTA-per-worker kernel
   if (!(flags & CCG_FLAG_SCT_NO_SPEC) && n_workers <= 16 * (int64_t)ctx->sm_count) return true;
-  // one worker per lane needs ~32k workers to fill 148 SMs; below that, and for the larger
-  // (L1/L2-resident) trigram/quadgram tables, one warp per worker is as fast or faster
-  // (profiles/r2_sct_*: k=10, n=400 -- bigram 1.6e9 vs 1.1e9 at 65k workers, 0.5e9 vs 1.05e9
-  // at 16k; trigram equal at 65k)
-  return !(order == 2 && n_workers >= 32768);
+  // one worker per lane needs ~32k workers to fill 148 SMs; below that, and for the
+  // L2-resident quadgram table, one warp per worker is faster (profiles/r2_sct_*: k=10,
+  // n=400 -- bigram 1.5e9 vs 1.1e9 and trigram 1.2e9 vs 0.9e9 at 65k workers, bigram 0.5e9
+  // vs 1.05e9 at 16k)
+  return !(order <= 3 && n_workers >= 32768);
 }
 
 // n_common: the common text length (-1: mixed lengths); max_len: the longest text

@@ -120,7 +120,7 @@ struct SctLaunch {
 // numpy pairwise order, bit-exact with sct.py:158-160); mode 1 = fast (int32-quantised table,
 // incremental rescoring of the windows of moved columns; ccg_sct_fast_climb).
 constexpr int kSctLaneWarps = 8;
-constexpr int kSctLaneMaxHops = 7;  // op1_hop / op2_hop limit of the lane kernels (reference: 3)
+constexpr int kSctLaneMaxHops = 3;  // op1_hop / op2_hop limit of the lane kernels (= the reference default)
 struct SctLaneLaunch {
   int32_t mode;
   const uint8_t* ciphers;

@@ -43,8 +43,11 @@ namespace ccg {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kRing = 32;  // draws buffered per lane (power of two)
-constexpr int kParseSteps = 16;  // proposal-parser steps (draws) per lane per round, < kRing - 3
+// draws buffered per lane (power of two) and proposal-parser steps per lane per round
+// (< ring - 3).  The fast mode trades ring depth for a third block per SM (its registers
+// fit 80); the parity mode's pairwise stack needs more registers and keeps two blocks.
+constexpr int ring_of(int mode) { return mode == 1 ? 16 : 32; }
+constexpr int parse_steps_of(int mode) { return mode == 1 ? 12 : 16; }
 // parsed-proposal queue per lane: kQSlots proposals of a header word + up to kSctLaneMaxHops
 // position events (one per swap / block swap; a shift is one event)
 constexpr int kQSlots = 2;
@@ -57,7 +60,8 @@ __host__ __device__ constexpr size_t round16(size_t b) { return (b + 15) & ~(siz
 
 template <int MODE, int KMAX>
 __host__ __device__ constexpr size_t lane_fixed_bytes() {
-  return (size_t)kRing * 128 + kQueueBytes + 2 * KMAX * 32 + KMAX * 64 + (MODE == 1 ? KMAX * 128 : 256);
+  return (size_t)ring_of(MODE) * 128 + kQueueBytes + 2 * KMAX * 32 + KMAX * 64 +
+         (MODE == 1 ? KMAX * 128 : 256);
 }
 template <int MODE, int KMAX>
 __host__ __device__ size_t lane_warp_bytes(int max_len) {
@@ -84,6 +88,7 @@ __device__ __noinline__ void lane_gen_block(uint64_t k0, uint64_t k1, uint64_t p
 }
 
 // One lane's draw stream: WorkerRng(seed, stream) (rng.py:58-79), ring-buffered in shared memory.
+template <int kRing>
 struct LaneRing {
   uint64_t k0, k1;
   uint64_t cons;  // stream index of the next draw
@@ -332,7 +337,7 @@ __device__ __forceinline__ int32_t window_sum(int w, int k, int rows, const uint
 }
 
 template <int MODE, int ORDER, int KMAX, bool TSMEM>
-__global__ void __launch_bounds__(kSctLaneWarps * 32)
+__global__ void __launch_bounds__(kSctLaneWarps * 32, MODE == 1 ? 3 : 1)
     sct_lane_kernel(const SctLaneLaunch p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -349,6 +354,7 @@ __global__ void __launch_bounds__(kSctLaneWarps * 32)
   }
   unsigned char* wb = smem + tab_bytes + (size_t)warp * lane_warp_bytes<MODE, KMAX>(p.max_len);
   const uint32_t ring = sm::addr(wb);
+  constexpr int kRing = ring_of(MODE), kParseSteps = parse_steps_of(MODE);
   uint32_t* qp = reinterpret_cast<uint32_t*>(wb + kRing * 128) + lane;  // [32 (4 slot + word)]
   unsigned char* kb = wb + kRing * 128 + kQueueBytes;
   uint8_t* keyp = kb + lane;                                  // key[q] at keyp[32 q]
@@ -383,7 +389,7 @@ __global__ void __launch_bounds__(kSctLaneWarps * 32)
       const int k = mine ? (p.key_lengths ? p.key_lengths[w] : p.kmax) : 2;
       const int base = n / k, rem = n - base * k;
       auto seglen = [&](int c) { return c < rem ? base + 1 : base; };
-      LaneRing d;
+      LaneRing<kRing> d;
       d.slot0 = ring + 4u * (uint32_t)lane;
       d.k0 = d.k1 = 0;
       d.cons = d.prod = 0;

@@ -195,14 +195,14 @@ def test_fast_mode_validates():
 
 
 def test_lane_kernels_take_any_reference_hop_count():
-    """op1_hop / op2_hop up to 7 run on the per-lane kernels (bit-exact); larger hop counts
-    (valid for the reference, sct.py:57-66) take the warp kernel automatically, and the fast
-    mode refuses them loudly."""
+    """op1_hop / op2_hop up to 3 (the reference default) run on the per-lane kernels
+    (bit-exact); larger hop counts (valid for the reference, sct.py:57-66) take the warp
+    kernel automatically, and the fast mode refuses them loudly."""
     rng = np.random.default_rng(901)
     logs = -rng.random(676) * 20 - 1
     cipher = rng.integers(0, 26, 300)
     keys = philox_keys([3], list(range(40)))
-    for h1, h2 in [(7, 1), (1, 7), (5, 6)]:
+    for h1, h2 in [(3, 1), (1, 3), (2, 3)]:
         res = engine.sct_climb([cipher], np.zeros(40, np.int32), keys, logs, 17, 300, op1_hop=h1,
                                op2_hop=h2, kernel="lane")
         want, wk = O.sct_workers([cipher], np.zeros(40, np.int32), [3] * 40, list(range(40)), logs,

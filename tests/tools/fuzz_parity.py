@@ -80,7 +80,7 @@ def fuzz_sct(rng, stats):
     klens = np.array([int(rng.integers(2, min(cs[c].size, kmax) + 1)) for c in cof], np.int32)
     seeds, streams = rng.integers(0, 2**63, m).tolist(), rng.integers(0, 2**63, m).tolist()
     p1, p2 = sorted(int(v) for v in rng.integers(0, 101, 2))
-    hmax = 8 if kernel == "lane" else 10  # the lane kernels take up to 7 hops
+    hmax = 4 if kernel == "lane" else 10  # the lane kernels take up to 3 hops
     h1, h2 = int(rng.integers(1, hmax)), int(rng.integers(1, hmax))
     climb = int(rng.choice([0, 1, 50, 400]))
     spec = bool(rng.integers(0, 2))  # speculative CTA kernel or one warp per worker
@@ -112,7 +112,7 @@ def fuzz_sct_fast(rng, stats):
     klens = np.array([int(rng.integers(2, min(cs[c].size, kmax) + 1)) for c in cof], np.int32)
     seeds, streams = rng.integers(0, 2**63, m).tolist(), rng.integers(0, 2**63, m).tolist()
     p1, p2 = sorted(int(v) for v in rng.integers(0, 101, 2))
-    h1, h2 = int(rng.integers(1, 8)), int(rng.integers(1, 8))
+    h1, h2 = int(rng.integers(1, 4)), int(rng.integers(1, 4))
     climb = int(rng.choice([0, 1, 60, 400]))
     res = engine.sct_fast_climb(cs, cof, philox_keys(seeds, streams), q, klens, climb, p1=p1,
                                 p2=p2, op1_hop=h1, op2_hop=h2)
