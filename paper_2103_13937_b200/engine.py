@@ -274,7 +274,8 @@ def sct_climb(ciphers, cipher_of, keys, logs, key_length, climbings, *, p1=33, p
 
 def sct_fast_climb(ciphers, cipher_of, keys, table, key_length, climbings, *, p1=33, p2=66,
                    op1_hop=3, op2_hop=3, skips=None, group_size=0, draws_used=False,
-                   last_accept=False, tries_done=False, lookups=True, devices_=None) -> ClimbResult:
+                   last_accept=False, tries_done=False, lookups=True, table_l2=False,
+                   devices_=None) -> ClimbResult:
     """The opt-in fast SCT mode (ccg_sct_fast_climb): sct_worker (sct.py:148-170) with the
     fitness replaced by the integer sum of a quantised log table (ngrams.quantize_sct_table:
     `table` is a QuantizedSctTable or its int32[26**order] entries plus `order` attribute),
@@ -327,7 +328,8 @@ def sct_fast_climb(ciphers, cipher_of, keys, table, key_length, climbings, *, p1
         a.draws_used, a.last_accept = _lib.ptr(out.draws_used), _lib.ptr(out.last_accept)
         a.tries_done = _lib.ptr(out.tries_done)
         a.group_size, a.group_best = int(group_size), _lib.ptr(out.group_best)
-        a.key_lengths, a.lookups, a.flags = _lib.ptr(kl), _lib.ptr(out.lookups), 0
+        a.key_lengths, a.lookups = _lib.ptr(kl), _lib.ptr(out.lookups)
+        a.flags = _lib.FLAG_SCT_TABLE_L2 if table_l2 else 0
         ctx = _lib.context(dev)
         with ctx.lock:
             before = ctx.launches()
