@@ -195,8 +195,18 @@ def c3(bounded=False, quick=False):
                                                    [9000] * (m * THREADS), list(range(m * THREADS)),
                                                    l3.logs, 20, 200, order=3, threads=THREADS),
                            lambda m: m * THREADS * 200, budget_s=2.0 if bounded else 4.0)
+    # the SCT climb reads, per evaluation, every plaintext letter through the column starts
+    # (n shared-memory gathers) and every window's table entry (n - 2 gathers): the
+    # reference algorithm's O(n) lookups, against the LDS lane-lookup peak
+    lpe = 400 + 398
+    peak = 148 * 32 * 1.965e9
+    roof = {"bound": "smem-lookups", "lookups_per_eval": lpe,
+            "achieved": total_evals / total_s * lpe, "peak": peak, "unit": "lookups/s",
+            "frac": total_evals / total_s * lpe / peak,
+            "peak_source": "148 SMs x 32 lane lookups per clock x 1965 MHz (SURVEY 8d formula)"}
     out = [{"config": "C3", "what": "SCT k=5..20, 1000 ciphertexts x 400 letters, trigram log "
                                     "table, parity mode (float64, numpy pairwise order)",
+            "roofline": roof,
             "workers_per_cipher": W, "climbings": K, "launches": "one (ragged key lengths)",
             "evals": total_evals, "seconds": total_s, "evals_per_s": total_evals / total_s,
             "recovered": int(sum(rec)), "of": n_c,
