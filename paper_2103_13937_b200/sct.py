@@ -1,9 +1,11 @@
 """Single-columnar-transposition attack (reference sct.py:1-210), GPU-backed.
 
-sct_worker / solve_sct run on the GPU: one warp per worker, candidate keys mutated in
-registers, decryption by index arithmetic, float64 scoring in numpy's pairwise order
-(csrc/ccg_sct.cu).  The operator functions below are the reference's host-side helpers,
-drawing from a (GPU-generated) WorkerRng stream; the climb itself never calls them.
+sct_worker / solve_sct run on the GPU: decryption by index arithmetic, float64 scoring in
+numpy's pairwise order, one warp per worker (csrc/ccg_sct.cu) or one worker per lane for
+large batches (csrc/ccg_sct_lane.cu).  The operator functions below are the reference's
+host-side helpers, drawing from a (GPU-generated) WorkerRng stream; the climb itself never
+calls them.  solve_sct_fast is the opt-in fast mode (quantised fitness, incremental
+rescoring; not bit-exact with the reference by design).
 
 n-gram extension: sct_worker / solve_sct also accept an ngrams.LogNgramTable of order 3 or
 4 (BASELINE.json config 3: trigram scoring); the candidate score is then the pairwise sum of
@@ -19,7 +21,7 @@ import numpy as np
 from . import engine
 from .ciphers import sct_decrypt
 from .codec import MappedText
-from .ngrams import LogBigramTable, as_log_ngram_table
+from .ngrams import LogBigramTable, as_log_ngram_table, quantize_sct_table
 from .rng import WorkerRng, philox_keys, worker_stream_index
 from .search import RestartSummary, SolveResult
 from .mas import _batched_restarts
@@ -191,3 +193,39 @@ def solve_sct_batch(ciphers, logs, cfg: SctSolverConfig, restart: int = 0, seeds
                                per_worker_scores=[float(v) for v in sc], history=[],
                                best_key=key))
     return out
+
+
+def solve_sct_fast(cipher: MappedText, logs: LogBigramTable, cfg: SctSolverConfig, jobs: int = 1,
+                   stop=None, shift: int | None = None) -> tuple[SolveResult, list[RestartSummary]]:
+    """solve_sct (sct.py:179-210) in the opt-in fast mode: the same workers, streams,
+    operators and restart rules, with the fitness replaced by the int32-quantised log table
+    (ngrams.quantize_sct_table; `shift` defaults to the largest safe one) and candidates
+    scored incrementally on the GPU (engine.sct_fast_climb).  Scores are
+    reported as quantised sums / 2^shift (log2 units); decisions can differ from the
+    reference's float64 climb where two candidates' scores are within the rounding."""
+    text = np.asarray(cipher, dtype=np.int64)
+    if text.size < cfg.key_length:
+        raise ValueError("ciphertext shorter than the key")
+    lt = as_log_ngram_table(logs)
+    q = quantize_sct_table(lt, text_len=max(text.size, lt.order), **(
+        {} if shift is None else {"max_shift": int(shift)}))
+    scale = 2.0 ** -q.shift
+    W = cfg.workers
+
+    def batch(restarts):
+        streams = [worker_stream_index(r, w) for r in restarts for w in range(W)]
+        res = engine.sct_fast_climb([text], np.zeros(len(streams), np.int32),
+                                    philox_keys([cfg.global_seed], streams), q, cfg.key_length,
+                                    cfg.climbings, p1=cfg.p1, p2=cfg.p2, op1_hop=cfg.op1_hop,
+                                    op2_hop=cfg.op2_hop, group_size=W, lookups=False)
+        out = []
+        for i, _ in enumerate(restarts):
+            sc = res.scores[i * W:(i + 1) * W]
+            best = int(res.group_best[i])
+            key = res.keys[i * W + best].astype(np.int64)
+            out.append(SolveResult(best_text=sct_decrypt(text, key), best_score=float(sc[best]) * scale,
+                                   per_worker_scores=[float(v) * scale for v in sc], history=[],
+                                   best_key=key))
+        return out
+
+    return _batched_restarts(batch, cfg.restarts, W, stop)

@@ -217,3 +217,22 @@ def test_lane_kernels_take_any_reference_hop_count():
     q = cc.quantize_sct_table(cc.LogBigramTable(logs, -24.0), text_len=300)
     with pytest.raises(cc.engine._lib.EngineError):
         engine.sct_fast_climb([cipher], np.zeros(40, np.int32), keys, q, 17, 10, op1_hop=9)
+
+
+def test_solve_sct_fast_public_api(golden):
+    """solve_sct_fast: the reference's solve_sct restart loop in the fast mode, through the
+    public API; recovers the acceptance #08 (k = 10) key and matches its oracle per worker."""
+    plain = golden.plain_sct(596)
+    logs = cc.LogBigramTable(golden.english_logs(), -24.0)
+    cipher = cc.sct_encrypt(plain, O.permutation(800, golden.KEYGEN_STREAM, 10))
+    cfg = cc.SctSolverConfig(key_length=10, workers=64, climbings=15_000, restarts=5,
+                             global_seed=8000)
+    best, runs = cc.solve_sct_fast(cipher, logs, cfg,
+                                   stop=lambda r: bool(np.array_equal(r.best_text, plain)))
+    assert np.array_equal(best.best_text, plain)
+    q = cc.quantize_sct_table(logs, text_len=596)
+    want, _ = O.sct_fast_workers([cipher], np.zeros(64, np.int32), [8000] * 64, list(range(64)),
+                                 q.table, 2, 10, 15_000)
+    first = cc.solve_sct_fast(cipher, logs, cc.SctSolverConfig(key_length=10, workers=64,
+                                                               global_seed=8000))[0]
+    assert [int(round(v * 2.0**q.shift)) for v in first.per_worker_scores] == want.tolist()
