@@ -1105,6 +1105,55 @@ static int sct_launch_warp(ccg_ctx* ctx, const ccg_sct_climb_args* a, int64_t n)
   return CCG_OK;
 }
 
+extern "C++" {
+// A trigram log table has few distinct entries (they are log2 of small counts: 65 for the
+// corpus table), so the per-lane kernel can hold it exactly as a byte index per entry plus the
+// distinct values (17.6 KB of shared memory instead of 140 KB).  Returns false (no
+// compression) beyond 256 distinct bit patterns.  O(n) with a 512-slot open-addressing set.
+template <typename V>
+static bool compress_table(const V* t, int64_t n, std::vector<uint8_t>& idx, std::vector<V>& vals) {
+  static_assert(sizeof(V) <= 8, "");
+  uint64_t keys[512];
+  int16_t at[512];
+  for (int i = 0; i < 512; ++i) at[i] = -1;
+  idx.resize((size_t)n);
+  vals.clear();
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t bits = 0;
+    memcpy(&bits, &t[i], sizeof(V));
+    uint64_t h = bits * 0x9E3779B97F4A7C15ULL;
+    int slot = (int)(h >> 55);  // 9 bits
+    while (at[slot] >= 0 && keys[slot] != bits) slot = (slot + 1) & 511;
+    if (at[slot] < 0) {
+      if (vals.size() == 256) return false;
+      keys[slot] = bits;
+      at[slot] = (int16_t)vals.size();
+      vals.push_back(t[i]);
+    }
+    idx[(size_t)i] = (uint8_t)at[slot];
+  }
+  return true;
+}
+
+// Upload a compressed order-3 table into the launch (scratch slots 16, 17) when it compresses.
+template <typename V>
+static int attach_compressed(ccg_ctx* ctx, const V* host_table, int order, SctLaneLaunch& p) {
+  if (order != 3 || !host_table) return CCG_OK;
+  std::vector<uint8_t> idx;
+  std::vector<V> vals;
+  if (!compress_table(host_table, 17576, idx, vals)) return CCG_OK;
+  void* d;
+  int rc;
+  if ((rc = upload(ctx, 16, idx.data(), idx.size(), &d))) return rc;
+  p.cidx = (const uint8_t*)d;
+  if ((rc = upload(ctx, 17, vals.data(), vals.size() * sizeof(V), &d))) return rc;
+  p.cvals = d;
+  p.n_cvals = (int32_t)vals.size();
+  return CCG_OK;
+}
+
+}  // extern "C++"
+
 // One worker per lane (ccg_sct_lane.cu), parity (mode 0) or fast (mode 1) scoring; texts of
 // any mix of lengths up to max_len.
 static int sct_launch_lane(ccg_ctx* ctx, SctLaneLaunch& p) {
@@ -1141,8 +1190,10 @@ static bool sct_use_warp_family(ccg_ctx* ctx, uint32_t flags, int64_t n_workers,
   return !(order <= 3 && n_workers >= 32768);
 }
 
-// n_common: the common text length (-1: mixed lengths); max_len: the longest text
-static int sct_launch(ccg_ctx* ctx, const ccg_sct_climb_args* a, int64_t n_common, int64_t max_len) {
+// n_common: the common text length (-1: mixed lengths); max_len: the longest text; host_logs:
+// the log table on the host (NULL for the _dev entry point), for the compressed trigram table
+static int sct_launch(ccg_ctx* ctx, const ccg_sct_climb_args* a, int64_t n_common, int64_t max_len,
+                      const double* host_logs = nullptr) {
   int rc;
   if (sct_use_warp_family(ctx, a->flags, a->n_workers, n_common, a->order == 0 ? 2 : a->order,
                           std::max(a->op1_hop, a->op2_hop))) {
@@ -1174,6 +1225,7 @@ static int sct_launch(ccg_ctx* ctx, const ccg_sct_climb_args* a, int64_t n_commo
     p.last_accept = a->last_accept;
     p.tries_done = a->tries_done;
     p.flags = a->flags;
+    if ((rc = attach_compressed(ctx, host_logs, p.order, p))) return rc;
     if ((rc = sct_launch_lane(ctx, p))) return rc;
   }
   if (a->group_size > 0 && a->group_best) {
@@ -1270,7 +1322,7 @@ int ccg_sct_climb(ccg_ctx* ctx, const ccg_sct_climb_args* a) {
   const int64_t ng = a->group_size > 0 ? nw / a->group_size : 0;
   if (a->group_best && ng) { if ((rc = ctx->buf(11, (size_t)ng * 8, &p))) return rc; d.group_best = (int64_t*)p; }
   else d.group_best = nullptr;
-  if ((rc = sct_launch(ctx, &d, n, max_len))) return rc;
+  if ((rc = sct_launch(ctx, &d, n, max_len, a->logs))) return rc;
   if ((rc = download(ctx, a->scores, d.scores, (size_t)nw * 8))) return rc;
   if ((rc = download(ctx, a->keys_out, d.keys_out, (size_t)nw * k))) return rc;
   if (a->draws_used && (rc = download(ctx, a->draws_used, d.draws_used, (size_t)nw * 8))) return rc;
@@ -1355,6 +1407,7 @@ int ccg_sct_fast_climb(ccg_ctx* ctx, const ccg_sct_fast_args* a) {
   L.op2_hop = a->op2_hop;
   L.order = a->order;
   L.flags = a->flags;
+  if ((rc = attach_compressed(ctx, a->table, a->order, L))) return rc;
   if ((rc = sct_launch_lane(ctx, L))) return rc;
   if (d_best) {
     ctx->launches++;

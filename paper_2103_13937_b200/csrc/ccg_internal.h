@@ -146,6 +146,9 @@ struct SctLaneLaunch {
   int64_t* lookups;       // mode 1: table lookups of the incremental rescoring, per worker
   uint32_t flags;
   unsigned long long* tickets;
+  const uint8_t* cidx;    // order 3, optional: per-entry index into <= 256 distinct values
+  const void* cvals;      // the distinct values (double for mode 0, int32 for mode 1)
+  int32_t n_cvals;
 };
 
 #ifdef __CUDACC__

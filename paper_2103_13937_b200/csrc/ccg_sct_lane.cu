@@ -63,6 +63,13 @@ __host__ __device__ constexpr size_t lane_fixed_bytes() {
   return (size_t)ring_of(MODE) * 128 + kQueueBytes + 2 * KMAX * 32 + KMAX * 64 +
          (MODE == 1 ? KMAX * 128 : 256);
 }
+template <int MODE, int ORDER, bool TSMEM, bool CIDX>
+__host__ __device__ constexpr size_t lane_tab_bytes() {
+  using Tab = typename std::conditional<MODE == 0, double, int32_t>::type;
+  return CIDX ? round16(256 * sizeof(Tab)) + round16((size_t)pow26(ORDER))
+              : TSMEM ? round16((size_t)pow26(ORDER) * sizeof(Tab)) : 0;
+}
+
 template <int MODE, int KMAX>
 __host__ __device__ size_t lane_warp_bytes(int max_len) {
   return lane_fixed_bytes<MODE, KMAX>() + round16((size_t)max_len + 16);
@@ -178,6 +185,17 @@ __device__ int build_plan(uint32_t plan, int n_terms) {
   return nops;
 }
 
+// A log table in shared or global memory: direct entries, or (CIDX) a byte index per entry
+// into at most 256 distinct values -- an n-gram log table built from counts has few distinct
+// entries (65 for the corpus trigram table), so the exact float64 / int32 values of a
+// 17,576-entry trigram table fit in 17.6 KB of shared memory instead of 140 / 70 KB.
+template <typename V, bool CIDX>
+struct TabRef {
+  const V* v;
+  const uint8_t* ix;
+  __device__ __forceinline__ V operator[](int i) const { return CIDX ? v[ix[i]] : v[i]; }
+};
+
 // The decryption walk of one lane: the letters of plain[0], plain[1], ... in order
 // (plain[t] = cipher[colstart[t % k] + t / k]).  Plain shared-memory pointers (no volatile
 // asm) so the compiler can issue the loads of eight consecutive positions back to back:
@@ -202,7 +220,7 @@ template <int ORDER, typename Tab>
 struct ParityTerms {
   Walk wk;
   int h[3];  // the previous ORDER-1 letters, oldest first
-  const Tab* tab;
+  Tab tab;
   __device__ __forceinline__ void prime() {
 #pragma unroll
     for (int i = 0; i < ORDER - 1; ++i) {
@@ -305,9 +323,9 @@ __device__ double parity_score(ParityTerms<ORDER, Tab>& T, const int32_t* plan, 
 
 // FAST mode: integer sum of the windows whose first letter lies in grid column w
 // (positions t = w + r*k, t <= n - ORDER), read column-wise from the ciphertext.
-template <int ORDER>
+template <int ORDER, typename Tab>
 __device__ __forceinline__ int32_t window_sum(int w, int k, int rows, const uint8_t* txt,
-                                              const uint16_t* cs, const int32_t* tab) {
+                                              const uint16_t* cs, Tab tab) {
   const uint8_t* b[ORDER];
 #pragma unroll
   for (int i = 0; i < ORDER; ++i) {
@@ -336,7 +354,7 @@ __device__ __forceinline__ int32_t window_sum(int w, int k, int rows, const uint
   return acc;
 }
 
-template <int MODE, int ORDER, int KMAX, bool TSMEM>
+template <int MODE, int ORDER, int KMAX, bool TSMEM, bool CIDX>
 __global__ void __launch_bounds__(kSctLaneWarps * 32, MODE == 1 ? 3 : 1)
     sct_lane_kernel(const SctLaneLaunch p) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -344,13 +362,21 @@ __global__ void __launch_bounds__(kSctLaneWarps * 32, MODE == 1 ? 3 : 1)
   using Tab = typename std::conditional<MODE == 0, double, int32_t>::type;
   constexpr int T = pow26(ORDER);
   const Tab* gtab = MODE == 0 ? (const Tab*)p.logs : (const Tab*)p.qtable;
-  const size_t tab_bytes = TSMEM ? round16((size_t)T * sizeof(Tab)) : 0;
-  const Tab* tab = gtab;
-  if (TSMEM) {
+  const size_t tab_bytes = lane_tab_bytes<MODE, ORDER, TSMEM, CIDX>();
+  TabRef<Tab, CIDX> tab{gtab, nullptr};
+  if (CIDX) {  // distinct values, then the byte index
+    Tab* sv = reinterpret_cast<Tab*>(smem);
+    uint8_t* si = smem + round16(256 * sizeof(Tab));
+    for (int i = threadIdx.x; i < p.n_cvals; i += blockDim.x) sv[i] = reinterpret_cast<const Tab*>(p.cvals)[i];
+    for (int i = threadIdx.x; i < T; i += blockDim.x) si[i] = p.cidx[i];
+    __syncthreads();
+    tab.v = sv;
+    tab.ix = si;
+  } else if (TSMEM) {
     Tab* st = reinterpret_cast<Tab*>(smem);
     for (int i = threadIdx.x; i < T; i += blockDim.x) st[i] = gtab[i];
     __syncthreads();
-    tab = st;
+    tab.v = st;
   }
   unsigned char* wb = smem + tab_bytes + (size_t)warp * lane_warp_bytes<MODE, KMAX>(p.max_len);
   const uint32_t ring = sm::addr(wb);
@@ -402,13 +428,13 @@ __global__ void __launch_bounds__(kSctLaneWarps * 32, MODE == 1 ? 3 : 1)
       const int no = n - ORDER;
       const int rows_q = no >= 0 ? no / k : 0, rows_s = no >= 0 ? no - rows_q * k : -1;
       auto rows_of = [&](int ww) { return no < 0 ? 0 : rows_q + (ww <= rows_s ? 1 : 0); };
-      ParityTerms<ORDER, Tab> pt;
+      ParityTerms<ORDER, TabRef<Tab, CIDX>> pt;
       pt.wk.txt = txt;
       pt.wk.cs = csp;
       pt.wk.k = k;
       pt.tab = tab;
       auto wsum = [&](int ww) {
-        return window_sum<ORDER>(ww, k, rows_of(ww), txt, csp, (const int32_t*)tab);
+        return window_sum<ORDER>(ww, k, rows_of(ww), txt, csp, tab);
       };
       int64_t lookups = 0;
 
@@ -431,7 +457,7 @@ __global__ void __launch_bounds__(kSctLaneWarps * 32, MODE == 1 ? 3 : 1)
           s += seglen(c);
         }
         if (MODE == 0) {
-          fscore = parity_score<ORDER, Tab>(pt, plan, nops);
+          fscore = parity_score(pt, plan, nops);
         } else {
           for (int ww = 0; ww < k; ++ww) {
             const int32_t g = wsum(ww);
@@ -573,7 +599,7 @@ __global__ void __launch_bounds__(kSctLaneWarps * 32, MODE == 1 ? 3 : 1)
         int32_t delta = 0;
         uint64_t wd = 0;
         if (MODE == 0) {
-          fcand = parity_score<ORDER, Tab>(pt, plan, nops);
+          fcand = parity_score(pt, plan, nops);
           accept = fcand > fscore;  // sct.py:168
         } else {
           // windows touching a moved column: w = c - i (mod k), i < ORDER
@@ -640,12 +666,11 @@ cudaError_t lane_smem_attr(K kern, size_t bytes) {
   return cudaSuccess;
 }
 
-template <int MODE, int ORDER, int KMAX, bool TSMEM>
+template <int MODE, int ORDER, int KMAX, bool TSMEM, bool CIDX = false>
 cudaError_t lane_launch(cudaStream_t s, const SctLaneLaunch& p, int sm_count) {
-  auto kern = sct_lane_kernel<MODE, ORDER, KMAX, TSMEM>;
-  using Tab = typename std::conditional<MODE == 0, double, int32_t>::type;
-  const size_t tab_bytes = TSMEM ? round16((size_t)pow26(ORDER) * sizeof(Tab)) : 0;
-  const size_t bytes = tab_bytes + kSctLaneWarps * lane_warp_bytes<MODE, KMAX>(p.max_len);
+  auto kern = sct_lane_kernel<MODE, ORDER, KMAX, TSMEM, CIDX>;
+  const size_t bytes =
+      lane_tab_bytes<MODE, ORDER, TSMEM, CIDX>() + kSctLaneWarps * lane_warp_bytes<MODE, KMAX>(p.max_len);
   cudaError_t e = lane_smem_attr(kern, bytes);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -660,13 +685,16 @@ cudaError_t lane_launch(cudaStream_t s, const SctLaneLaunch& p, int sm_count) {
   return cudaGetLastError();
 }
 
-// shared-memory tables: bigram always; trigram when the table plus the warps' arrays fit
+// Where the table lives: bigram in shared memory; trigram as a byte index + distinct values
+// in shared memory when the host found at most 256 distinct entries (p.cidx), else in shared
+// memory when it fits beside the warps' arrays, else read through L1/L2; quadgram via L2.
 template <int MODE, int ORDER, int KMAX>
 cudaError_t lane_table(cudaStream_t s, const SctLaneLaunch& p, int sm_count) {
   if (ORDER == 4) return lane_launch<MODE, 4, KMAX, false>(s, p, sm_count);
-  using Tab = typename std::conditional<MODE == 0, double, int32_t>::type;
-  const size_t tab_bytes = round16((size_t)pow26(ORDER) * sizeof(Tab));
-  const size_t bytes = tab_bytes + kSctLaneWarps * lane_warp_bytes<MODE, KMAX>(p.max_len);
+  if (ORDER == 3 && p.cidx && !(p.flags & CCG_FLAG_SCT_TABLE_L2))
+    return lane_launch<MODE, 3, KMAX, true, true>(s, p, sm_count);
+  const size_t bytes =
+      lane_tab_bytes<MODE, ORDER, true, false>() + kSctLaneWarps * lane_warp_bytes<MODE, KMAX>(p.max_len);
   if (ORDER == 2 || (bytes <= 200 * 1024 && !(p.flags & CCG_FLAG_SCT_TABLE_L2)))
     return lane_launch<MODE, ORDER, KMAX, true>(s, p, sm_count);
   return lane_launch<MODE, ORDER, KMAX, false>(s, p, sm_count);

@@ -236,3 +236,31 @@ def test_solve_sct_fast_public_api(golden):
     first = cc.solve_sct_fast(cipher, logs, cc.SctSolverConfig(key_length=10, workers=64,
                                                                global_seed=8000))[0]
     assert [int(round(v * 2.0**q.shift)) for v in first.per_worker_scores] == want.tolist()
+
+
+def test_compressed_trigram_tables(golden):
+    """A trigram log table with few distinct entries (the corpus table: log2 of small counts)
+    is held as a byte index + distinct values in shared memory; results are bit-identical to
+    the table read through L2 and to the oracle, in both the parity and the fast mode."""
+    corpus = "".join(chr(97 + int(x)) for x in golden.corpus())
+    l3 = cc.build_log_ngram_table(cc.build_ngram_table_from_corpus(corpus, 3))
+    assert np.unique(l3.logs).size <= 256
+    rng = np.random.default_rng(77)
+    ciphers = [rng.integers(0, 26, L) for L in (400, 251)]
+    cof = np.repeat(np.array([0, 1], np.int32), 32)
+    klens = np.repeat(np.array([13, 7], np.int32), 32)
+    keys = philox_keys([12], list(range(64)))
+    a = engine.sct_climb(ciphers, cof, keys, l3.logs, klens, 800, order=3, kernel="lane")
+    b = engine.sct_climb(ciphers, cof, keys, l3.logs, klens, 800, order=3, kernel="lane",
+                         table_l2=True)
+    assert a.scores.tolist() == b.scores.tolist() and np.array_equal(a.keys, b.keys)
+    for i in (0, 31, 32, 63):
+        k, s, _ = O.sct_worker(ciphers[cof[i]], l3.logs, int(klens[i]), 800, 12, i, order=3)
+        assert float(a.scores[i]) == s and np.array_equal(a.keys[i, :klens[i]].astype(np.int64), k)
+    q = cc.quantize_sct_table(l3, text_len=400)
+    fa = engine.sct_fast_climb(ciphers, cof, keys, q, klens, 800)
+    fb = engine.sct_fast_climb(ciphers, cof, keys, q, klens, 800, table_l2=True)
+    assert fa.scores.tolist() == fb.scores.tolist() and np.array_equal(fa.keys, fb.keys)
+    for i in (0, 63):
+        k, s, _ = O.sct_fast_worker(ciphers[cof[i]], q.table, 3, int(klens[i]), 800, 12, i)
+        assert int(fa.scores[i]) == s
