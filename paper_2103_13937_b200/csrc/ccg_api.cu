@@ -117,11 +117,42 @@ int check_ragged(const uint8_t* texts, const int64_t* offsets, int64_t n, const 
   }
   const int64_t total = n > 0 ? offsets[n] : 0;
   if (total > 0 && !texts) return fail(CCG_ERR_INVALID, "%s: null texts", what);
-  for (int64_t i = 0; i < total; ++i)
-    if (texts[i] >= kAlpha)
-      return fail(CCG_ERR_INVALID, "%s: letter %d at position %lld outside 0..25", what,
-                  (int)texts[i], (long long)i);
+  // eight letters per step: a byte is >= 26 iff its top bit is set or (its low 7 bits + 102)
+  // reaches 128 (no carry can cross bytes: 127 + 102 < 256); the byte loop only locates it
+  bool bad = false;
+  int64_t i = 0;
+  for (; i + 8 <= total; i += 8) {
+    uint64_t x;
+    memcpy(&x, texts + i, 8);
+    const uint64_t y = x & 0x7f7f7f7f7f7f7f7fULL;
+    if (((y + 0x6666666666666666ULL) | x) & 0x8080808080808080ULL) {
+      bad = true;
+      break;
+    }
+  }
+  if (!bad)
+    for (; i < total; ++i) bad |= texts[i] >= kAlpha;
+  if (bad)
+    for (int64_t j = 0; j < total; ++j)
+      if (texts[j] >= kAlpha)
+        return fail(CCG_ERR_INVALID, "%s: letter %d at position %lld outside 0..25", what,
+                    (int)texts[j], (long long)j);
   if (max_len) *max_len = m;
+  return CCG_OK;
+}
+
+// min/max over the indices (vectorises), the per-index loop only to report the first bad one
+int check_cipher_of(const int32_t* cof, int64_t nw, int64_t n_ciphers) {
+  int32_t lo = 0, hi = 0;
+  if (nw > 0) lo = hi = cof[0];
+  for (int64_t i = 0; i < nw; ++i) {
+    lo = std::min(lo, cof[i]);
+    hi = std::max(hi, cof[i]);
+  }
+  if (nw > 0 && (lo < 0 || hi >= n_ciphers))
+    for (int64_t i = 0; i < nw; ++i)
+      if (cof[i] < 0 || cof[i] >= n_ciphers)
+        return fail(CCG_ERR_INVALID, "cipher_of[%lld] out of range", (long long)i);
   return CCG_OK;
 }
 
@@ -612,9 +643,7 @@ int ccg_mas_climb(ccg_ctx* ctx, const ccg_mas_climb_args* a) {
   if ((rc = check_table(a->table, &tmax))) return rc;
   const int64_t nw = a->n_workers;
   if (nw == 0) return CCG_OK;
-  for (int64_t i = 0; i < nw; ++i)
-    if (a->cipher_of[i] < 0 || a->cipher_of[i] >= a->n_ciphers)
-      return fail(CCG_ERR_INVALID, "cipher_of[%lld] out of range", (long long)i);
+  if ((rc = check_cipher_of(a->cipher_of, nw, a->n_ciphers))) return rc;
   ccg_mas_climb_args d = *a;
   void* p;
   if ((rc = upload(ctx, 0, a->ciphers, (size_t)a->offsets[a->n_ciphers], &p))) return rc;
