@@ -264,3 +264,26 @@ def test_compressed_trigram_tables(golden):
     for i in (0, 63):
         k, s, _ = O.sct_fast_worker(ciphers[cof[i]], q.table, 3, int(klens[i]), 800, 12, i)
         assert int(fa.scores[i]) == s
+
+
+@pytest.mark.parametrize("order", [2, 3, 4])
+def test_lane_kernels_tiny_texts(order):
+    """Texts shorter than (or as long as) the n-gram order -- an empty or single-window
+    pairwise sum -- in both modes, ragged in one launch."""
+    rng = np.random.default_rng(1200 + order)
+    logs = -rng.random(26**order) * 20 - 1
+    ciphers = [rng.integers(0, 26, L) for L in (2, 3, 4, 5, 9)]
+    cof = np.repeat(np.arange(5, dtype=np.int32), 8)
+    klens = np.array([2 if len(ciphers[c]) < 4 else int(rng.integers(2, len(ciphers[c]) + 1))
+                      for c in cof], np.int32)
+    keys = philox_keys([21], list(range(cof.size)))
+    res = engine.sct_climb(ciphers, cof, keys, logs, klens, 120, order=order, kernel="lane")
+    lt = cc.LogNgramTable(order, logs, -30.0) if order > 2 else cc.LogBigramTable(logs, -30.0)
+    q = cc.quantize_sct_table(lt, text_len=9)
+    fres = engine.sct_fast_climb(ciphers, cof, keys, q, klens, 120)
+    for i in range(cof.size):
+        c, k = ciphers[cof[i]], int(klens[i])
+        key, s, _ = O.sct_worker(c, logs, k, 120, 21, i, order=order)
+        assert float(res.scores[i]) == s and np.array_equal(res.keys[i, :k].astype(np.int64), key)
+        fkey, fs, _ = O.sct_fast_worker(c, q.table, order, k, 120, 21, i)
+        assert int(fres.scores[i]) == fs and np.array_equal(fres.keys[i, :k].astype(np.int64), fkey)
