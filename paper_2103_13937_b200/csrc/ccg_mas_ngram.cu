@@ -374,9 +374,14 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
       const uint32_t wd = win.round_letters(lane);
       const uint32_t c0 = wd & 0xffu, c1 = (wd >> 8) & 0xffu, c2 = (wd >> 16) & 0xffu;
       // (o <= 128, so all 32 pairs and their redraw partners lie in the 256-draw window)
+      // lane j + 1's first two letters: after a second redraw the pairs realign on even draws
+      // one lane further on (three segments, as in ccg_mas_dform.cu)
+      const uint32_t wn = __shfl_down_sync(kFull, wd, 1);
+      const uint32_t n0 = wn & 0xffu, n1 = (wn >> 8) & 0xffu;
       const uint32_t eqA = __ballot_sync(kFull, c0 == c1);
       const uint32_t r0 = eqA ? (uint32_t)(__ffs(eqA) - 1) : 32u;
       uint32_t R = 32u;    // pairs in this round
+      uint32_t r1 = 32u;   // the second redraw pair, if handled
       bool seq = false;    // the round stopped at a pair that needs the sequential path
       if (r0 < 32u) {
         const uint32_t c2r = __shfl_sync(kFull, c2, (int)r0), c0r = __shfl_sync(kFull, c0, (int)r0);
@@ -384,10 +389,18 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
           R = r0;
           seq = true;
         } else {
-          // a second redraw ends the round; the next round starts at that pair, which it
-          // handles as its first-segment redraw (no sequential try needed)
           const uint32_t eqB = __ballot_sync(kFull, c1 == c2) & ~((2u << r0) - 1u);
-          if (eqB) R = (uint32_t)(__ffs(eqB) - 1);
+          if (eqB) {
+            const uint32_t rb = (uint32_t)(__ffs(eqB) - 1);
+            const uint32_t a1 = __shfl_sync(kFull, c1, (int)rb), b1 = __shfl_sync(kFull, n1, (int)rb);
+            if (rb == 31u || b1 == a1) {
+              R = rb;  // the next round handles it as its first-segment redraw
+            } else {
+              r1 = rb;
+              const uint32_t eqC = __ballot_sync(kFull, n0 == n1) & ~((2u << r1) - 1u);
+              R = eqC ? min((uint32_t)(__ffs(eqC) - 1), 31u) : 31u;
+            }
+          }
         }
       }
       if (R > climbings - t) {
@@ -395,7 +408,8 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
         seq = false;
       }
       const uint32_t j = (uint32_t)lane;
-      const uint32_t pa = j <= r0 ? c0 : c1, pb = j < r0 ? c1 : c2;
+      const uint32_t pa = j <= r0 ? c0 : (j <= r1 ? c1 : n0);
+      const uint32_t pb = j < r0 ? c1 : (j < r1 ? c2 : n1);
       const int key = (int)(min(pa, pb) * kAlpha + max(pa, pb));
       const bool in = j < R;
       const bool hit = in && dtag[key] == epoch;
@@ -408,7 +422,7 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
         const int ak = __shfl_sync(kFull, (int)pa, (int)k), bk = __shfl_sync(kFull, (int)pb, (int)k);
         const int dk = __shfl_sync(kFull, d, (int)k);
         t += k;
-        win.o += 2u * (k + 1u) + (k + 1u > r0 ? 1u : 0u);
+        win.o += 2u * (k + 1u) + (k + 1u > r0 ? 1u : 0u) + (k + 1u > r1 ? 1u : 0u);
         accept(ak, bk, dk);
         last = (int)t;
         since = 0;
@@ -418,7 +432,7 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
       }
       t += f;
       since += f;
-      win.o += 2u * f + (f > r0 ? 1u : 0u);
+      win.o += 2u * f + (f > r0 ? 1u : 0u) + (f > r1 ? 1u : 0u);
       if (f < R) {
         // lane g < kMissBatch takes the g-th miss of the round
         uint32_t m = miss, mg = 32u;
