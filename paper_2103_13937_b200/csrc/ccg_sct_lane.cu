@@ -46,8 +46,20 @@ constexpr unsigned kFull = 0xffffffffu;
 // draws buffered per lane (power of two) and proposal-parser steps per lane per round
 // (< ring - 3).  The fast mode trades ring depth for a third block per SM (its registers
 // fit 80); the parity mode's pairwise stack needs more registers and keeps two blocks.
-constexpr int ring_of(int mode) { return mode == 1 ? 16 : 32; }
-constexpr int parse_steps_of(int mode) { return mode == 1 ? 12 : 16; }
+#ifndef CCG_LANE_RING0
+#define CCG_LANE_RING0 32
+#endif
+#ifndef CCG_LANE_PARSE0
+#define CCG_LANE_PARSE0 16
+#endif
+#ifndef CCG_LANE_MINB0
+#define CCG_LANE_MINB0 1
+#endif
+#ifndef CCG_LANE_ILP
+#define CCG_LANE_ILP 8
+#endif
+constexpr int ring_of(int mode) { return mode == 1 ? 16 : CCG_LANE_RING0; }
+constexpr int parse_steps_of(int mode) { return mode == 1 ? 12 : CCG_LANE_PARSE0; }
 // parsed-proposal queue per lane: kQSlots proposals of a header word + up to kSctLaneMaxHops
 // position events (one per swap / block swap; a shift is one event)
 constexpr int kQSlots = 2;
@@ -229,12 +241,12 @@ struct ParityTerms {
       h[i] = wk.at(cc, rr);
     }
   }
-  // the letters of the next G positions, loaded before any is used.  For G = 8 and k >= 8
+  // the letters of the next G positions, loaded before any is used.  For G >= 4 and k >= G
   // the block spans at most one row boundary, so the column starts come from two base
   // pointers with immediate offsets instead of a per-position walk.
   template <int G>
   __device__ __forceinline__ void letters(int (&L)[ORDER - 1 + G]) {
-    if (G == 8 && wk.k >= 8) {
+    if (G >= 4 && wk.k >= G) {
       const int k = wk.k, c = wk.c, r = wk.r;
       const int split = k - c;  // positions j < split stay in row r
       const uint16_t* cb = wk.cs + 32 * c;
@@ -244,10 +256,10 @@ struct ParityTerms {
         const bool same = j < split;
         L[ORDER - 1 + j] = wk.txt[(same ? cb[32 * j] : cb2[32 * j]) + (same ? r : r + 1)];
       }
-      if (split > 8) {
-        wk.c = c + 8;
+      if (split > G) {
+        wk.c = c + G;
       } else {
-        wk.c = 8 - split;
+        wk.c = G - split;
         wk.r = r + 1;
       }
       return;
@@ -305,13 +317,30 @@ __device__ double parity_score(ParityTerms<ORDER, Tab>& T, const int32_t* plan, 
       res = 0.0;
       for (int j = 0; j < op; ++j) res += T.term();
     } else {
-      double r[8], v[8];
-      T.template terms<8>(r);
+      double r[8];
       const int blocks = op / 8;
-      for (int b = 1; b < blocks; ++b) {
-        T.template terms<8>(v);
+      if (CCG_LANE_ILP == 8) {
+        double v[8];
+        T.template terms<8>(r);
+        for (int b = 1; b < blocks; ++b) {
+          T.template terms<8>(v);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] += v[j];
+          for (int j = 0; j < 8; ++j) r[j] += v[j];
+        }
+      } else {  // four terms in flight (fewer live registers)
+        double v[4];
+        T.template terms<4>(v);
+        r[0] = v[0]; r[1] = v[1]; r[2] = v[2]; r[3] = v[3];
+        T.template terms<4>(v);
+        r[4] = v[0]; r[5] = v[1]; r[6] = v[2]; r[7] = v[3];
+        for (int b = 1; b < blocks; ++b) {
+          T.template terms<4>(v);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) r[j] += v[j];
+          T.template terms<4>(v);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) r[4 + j] += v[j];
+        }
       }
       res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
       for (int j = 8 * blocks; j < op; ++j) res += T.term();
@@ -355,7 +384,7 @@ __device__ __forceinline__ int32_t window_sum(int w, int k, int rows, const uint
 }
 
 template <int MODE, int ORDER, int KMAX, bool TSMEM, bool CIDX>
-__global__ void __launch_bounds__(kSctLaneWarps * 32, MODE == 1 ? 3 : 1)
+__global__ void __launch_bounds__(kSctLaneWarps * 32, MODE == 1 ? 3 : CCG_LANE_MINB0)
     sct_lane_kernel(const SctLaneLaunch p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
