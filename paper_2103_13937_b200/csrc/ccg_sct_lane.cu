@@ -24,15 +24,23 @@
 // windows of the moved columns.  The 32 workers of a warp share one ciphertext (workers of a
 // chunk with other ciphertexts run in further passes), staged once in shared memory.
 //
+// Proposals (sct.py:69-135) never read the key, so each lane parses its stream ahead, one
+// draw per step in every lane, into a small queue of position events (swap / block swap /
+// shift); a round = a fixed number of parse steps, then one evaluation per lane.  Long
+// rejection loops (apply_block_swaps) cost the lane that has them extra steps instead of
+// stalling the warp.
+//
 // Shared memory per warp, lane-interleaved so a lane's own arrays sit in its own banks:
-//   draw ring  u32[32 slots][32 lanes]: top 32 bits of each Philox word (rng.py:68-75); the
-//              ring is topped up warp-collectively once per try, so the Philox blocks of all
-//              lanes are generated together instead of diverging at every draw
+//   draw ring  u32[ring][32 lanes]: top 32 bits of each Philox word (rng.py:68-75), topped
+//              up warp-collectively once per round, so the lanes' Philox blocks are
+//              generated together instead of diverging at every draw
+//   queue      parsed proposals: a header word + up to kSctLaneMaxHops events each
 //   key, cand  u8[KMAX][32];  colstart u16[KMAX][32];  window sums i32[KMAX][32] (FAST)
 //   plan       the numpy pairwise recursion of this pass's text length (PARITY)
 //   text       the pass's ciphertext
-// The log table (676 f64 / 17,576 f64 or i32) is staged per block; quadgram tables are read
-// through L2.
+// The log table is staged per block: bigram directly (676 f64 / i32); trigram as a byte index
+// into its distinct values when it has at most 256 (exact, 17.6 KB -- the host finds them),
+// else directly when it fits, else through L1/L2; quadgram tables are read through L2.
 #include <type_traits>
 
 #include "ccg_internal.h"
@@ -136,9 +144,9 @@ struct LaneRing {
   // rng.py:77-79 int(u * bound), 1 <= bound < 2^11: A = (x >> 32) * bound gives it exactly
   // unless A's low word is within `bound` of wrapping (ccg_rng.cuh int_below_tiny)
   __device__ __forceinline__ int below(uint32_t bound) {
-    // A lane whose ring ran dry mid-try (operators with rejection loops can draw far more
-    // than the ring holds) refills together with every lane of its branch that has room:
-    // one Philox pass of the branch then serves all of them, instead of one pass per lane.
+    // Used for the start key's Fisher-Yates draws (up to 63, more than the ring holds): a
+    // lane whose ring ran dry refills together with every lane of its branch that has room,
+    // so one Philox pass serves all of them.
     if (__any_sync(__activemask(), prod == cons) && prod - cons <= (uint64_t)(kRing - 4)) gen();
     const uint32_t hi = sm::ld32(slot0 + 128u * (uint32_t)(cons & (kRing - 1)));
     const uint64_t A = (uint64_t)hi * bound;
@@ -153,12 +161,6 @@ struct LaneRing {
     ++cons;
     if ((uint32_t)A < 0u - bound) return (int)(A >> 32);
     return lane_exact_below(k0, k1, cons - 1, bound);
-  }
-  // rng.py:81-89
-  __device__ __forceinline__ void pair(uint32_t bound, int& a, int& b) {
-    a = below(bound);
-    b = below(bound);
-    while (b == a) b = below(bound);
   }
 };
 
