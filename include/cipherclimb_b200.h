@@ -91,6 +91,9 @@ enum {
 #define CCG_FLAG_SCT_KERNEL_WARP 0x200u
 #define CCG_FLAG_SCT_TABLE_L2 0x400u
 #define CCG_FLAG_SCT_KERNEL_LANE 0x800u
+/* SCT latency mode: the speculative kernel whose warps replay their predecessors' draws
+ * every round, instead of the chain-parsed kernel (identical results; for tests). */
+#define CCG_FLAG_SCT_SPEC_REPLAY 0x1000u
 
 typedef struct ccg_ctx ccg_ctx;
 

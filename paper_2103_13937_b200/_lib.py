@@ -24,6 +24,7 @@ FLAG_SCT_NO_SPEC = 0x100  # SCT: never use the speculative CTA-per-worker kernel
 FLAG_SCT_KERNEL_WARP = 0x200  # SCT: one warp per worker instead of one lane per worker
 FLAG_SCT_TABLE_L2 = 0x400  # SCT lane kernel: trigram table read through L2, not shared memory
 FLAG_SCT_KERNEL_LANE = 0x800  # SCT: one worker per lane
+FLAG_SCT_SPEC_REPLAY = 0x1000  # SCT latency mode: per-round draw replay instead of the parsed chain
 SCT_KERNEL_FLAGS = {"auto": 0, "lane": FLAG_SCT_KERNEL_LANE, "warp": FLAG_SCT_KERNEL_WARP}
 KERNEL_FLAGS = {"auto": 0, "dform": 0x10, "tform": 0x20, "packed": 0x30, "dtable": 0x40}
 

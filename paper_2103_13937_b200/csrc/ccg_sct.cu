@@ -26,6 +26,8 @@
 //    bit-identical to numpy's float64 sum, so accept decisions match the reference.
 //  * Tables: the 676 float64 log2 probabilities and each warp's ciphertext are staged in
 //    shared memory; colstart is a per-warp 64-entry u16 array (conflict-free).
+#include <cstdio>
+
 #include "ccg_internal.h"
 #include "ccg_rng.cuh"
 
@@ -630,6 +632,426 @@ __global__ void __launch_bounds__(P * 32, P >= 32 ? 1 : 32 / P)
   }
 }
 
+// ---- Latency mode, chain-parsed (sct_climb_chain_kernel) ----
+// The speculative kernel above makes warp j replay the draws of j proposals before it can
+// build its own, every round: the round lasts as long as warp P-1's serial replay.  But the
+// proposal sequence is a pure function of the stream (sct.py:69-135 never read the key, and
+// an accepted proposal is followed by exactly the proposal that follows it in the stream),
+// so it can be parsed once, ahead of the climb, and in parallel:
+//   1. the CTA generates a chunk of kChainDraws consecutive draws into shared memory;
+//   2. every thread parses the proposal that WOULD start at each of its draw offsets and
+//      records where it ends (one table of end offsets for the whole chunk);
+//   3. one thread follows end[] from the chunk's entry offset: the chain of true proposal
+//      starts (one shared load per proposal);
+//   4. the chain's proposals are parsed again, one per thread, into 16-byte descriptors
+//      (operator + up to kSctLaneMaxHops position events).
+// A round is then: warp j applies descriptor t+j to the current key and scores it; the first
+// improvement is accepted (sct.py:168) and the next round starts at the proposal after it.
+constexpr int kChainDraws = 4096;               // draws per parsed chunk
+constexpr int kChainMaxProps = kChainDraws / 4;  // every proposal reads at least 4 draws
+constexpr uint16_t kChainOvf = 0xffffu;          // the proposal runs past the chunk
+constexpr int kChainJumps = 5;
+constexpr size_t kMaxSmemPerBlock = 227 * 1024;  // sm_100 opt-in dynamic shared memory per block                   // jump tables of 1, 2, 4, 8, 16 proposals
+
+struct ChainSmem {
+  uint32_t hi[kChainDraws];            // top 32 bits of each draw of the chunk (rng.py:68-75)
+  uint16_t jump[kChainJumps][kChainDraws];  // jump[b][i]: offset 2^b proposals after i (>= kChainDraws: none)
+  uint16_t start[kChainMaxProps];      // the chain: start offsets of consecutive proposals
+  uint4 desc[kChainDraws];             // the proposal at each offset: x = op | events << 4,
+                                       // y, z, w = events (a | b << 8 | len << 16)
+  double score[2][32];                 // round exchange, alternated by round
+  uint8_t key[kSctMaxKey];
+  int n, next;                         // proposals in the chain; offset of the one after them
+  int ticket;                          // next offset to parse (chain_parse_lockstep)
+  uint32_t ptab[20];                   // parse automaton table (chain_parse_table)
+};
+
+// int(u*bound) of stream draw `pos` from its full 53-bit mantissa (the 32-bit test failed)
+__device__ __noinline__ int chain_exact_below(uint64_t k0, uint64_t k1, uint64_t pos, uint32_t bound) {
+  uint64_t v[4];
+  philox4x64_10(k0, k1, (pos >> 2) + 1, v[0], v[1], v[2], v[3]);
+  return (int)int_below_small(v[pos & 3], bound);
+}
+__device__ __noinline__ uint32_t chain_direct_hi(uint64_t k0, uint64_t k1, uint64_t pos) {
+  uint64_t v[4];
+  philox4x64_10(k0, k1, (pos >> 2) + 1, v[0], v[1], v[2], v[3]);
+  return (uint32_t)(v[pos & 3] >> 32);
+}
+
+// The proposal starting at draw offset i of the chunk whose draw 0 is stream index `base`
+// (sct.py:69-135; the same draws as skip_proposal / op_*): returns its end offset, or -1 when
+// it needs a draw at or past `lim`.  hi == nullptr reads the stream directly (no limit).
+__device__ __noinline__ int chain_parse(const uint32_t* hi, int lim, int i, uint64_t base,
+                                        uint64_t k0, uint64_t k1, int k, int p1, int p2, int h1,
+                                        int h2, uint4* out) {
+  auto draw = [&](uint32_t bound, int& v) -> bool {
+    uint32_t h;
+    if (hi) {
+      if (i >= lim) return false;
+      h = hi[i];
+    } else {
+      h = chain_direct_hi(k0, k1, base + (uint64_t)i);
+    }
+    const uint64_t A = (uint64_t)h * bound;
+    v = (uint32_t)A < 0u - bound ? (int)(A >> 32) : chain_exact_below(k0, k1, base + (uint64_t)i, bound);
+    ++i;
+    return true;
+  };
+  uint32_t e0 = 0u, e1 = 0u, e2 = 0u;  // the events (registers, not a local array)
+  int v, op, nev = 0;
+  auto put = [&](uint32_t x) {
+    if (nev == 0) e0 = x; else if (nev == 1) e1 = x; else e2 = x;
+    ++nev;
+  };
+  if (!draw(100u, v)) return -1;  // sct.py:69-79 select_operator
+  if (v < p1) {                   // sct.py:82-89 apply_element_swaps
+    op = 1;
+    if (!draw((uint32_t)h1, v)) return -1;
+    for (int h = 1 + v; h > 0; --h) {
+      int a;
+      if (!draw((uint32_t)k, a)) return -1;
+      do {
+        if (!draw((uint32_t)k, v)) return -1;
+      } while (v == a);
+      put((uint32_t)a | ((uint32_t)v << 8));
+    }
+  } else if (v < p2) {  // sct.py:92-112 apply_block_swaps
+    op = 2;
+    if (!draw((uint32_t)h2, v)) return -1;
+    for (int h = 1 + v; h > 0; --h) {
+      int len, a;
+      if (!draw((uint32_t)(k / 2), len)) return -1;
+      ++len;
+      const uint32_t m = (uint32_t)(k - len + 1);
+      for (;;) {  // the whole pair is redrawn while |p - q| < len
+        if (!draw(m, a)) return -1;
+        do {
+          if (!draw(m, v)) return -1;
+        } while (v == a);
+        if (abs(a - v) >= len) break;
+      }
+      put((uint32_t)min(a, v) | ((uint32_t)max(a, v) << 8) | ((uint32_t)len << 16));
+    }
+  } else {  // sct.py:115-135 apply_block_shift
+    op = 3;
+    int len, a;
+    if (!draw((uint32_t)(k - 1), len)) return -1;
+    ++len;
+    const uint32_t m = (uint32_t)(k - len + 1);
+    if (!draw(m, a)) return -1;
+    do {
+      if (!draw(m, v)) return -1;
+    } while (v == a);
+    put((uint32_t)a | ((uint32_t)v << 8) | ((uint32_t)len << 16));
+  }
+  if (out) *out = make_uint4((uint32_t)op | ((uint32_t)nev << 4), e0, e1, e2);
+  return i;
+}
+
+// The same parse as a one-draw-per-step automaton, table-driven so that the lanes of a warp
+// parse different proposals in lockstep without branching on their states: a proposal with a
+// long rejection loop costs its lane more steps instead of serialising the warp.
+// State s = 4 * phase + op: phase 0 = operator draw (select_operator), 1 = hop count, 2 = block
+// length, 3 = first position of a pair, 4 = second position (redrawn while equal; for block
+// swaps the whole pair is redrawn while |p - q| < len); op 1 = element swaps (0 5 (13 17)+),
+// 2 = block swaps (0 6 (10 14 18)+), 3 = block shift (0 11 15 19).  C.ptab[s] = the draw's
+// bound (0xffff: k - len + 1, the current block's position count) | the next state << 16.
+__device__ __forceinline__ void chain_parse_table(uint32_t* t, int k, int h1, int h2) {
+  for (int i = 0; i < 20; ++i) t[i] = 0u;
+  t[5] = (uint32_t)h1 | (13u << 16);
+  t[6] = (uint32_t)h2 | (10u << 16);
+  t[10] = (uint32_t)(k / 2) | (14u << 16);
+  t[11] = (uint32_t)(k - 1) | (15u << 16);
+  t[13] = (uint32_t)k | (17u << 16);
+  t[14] = 0xffffu | (18u << 16);
+  t[15] = 0xffffu | (19u << 16);
+  t[17] = (uint32_t)k | (13u << 16);
+  t[18] = 0xffffu | (10u << 16);
+  t[19] = 0xffffu;
+  t[0] = 100u;
+}
+
+// Parse, in lockstep, the proposal that would start at every offset of the chunk (draw values
+// C.hi, draw 0 = stream index base): C.jump[0][i] = its end offset (kChainOvf when it runs
+// past the chunk) and C.desc[i] = the proposal.  Thread t starts with offset t; a lane that
+// finishes takes the next offset from C.ticket (= the thread count at entry), so lanes with
+// long proposals do not leave the rest of their warp idle.  Every lane runs every step
+// (inactive lanes with their state frozen), so the warp stays converged: only the rare exact
+// conversion and the stores are predicated branches.
+__device__ __forceinline__ void chain_parse_lockstep(ChainSmem& C, uint64_t base, uint64_t k0,
+                                                     uint64_t k1, int k, int p1, int p2) {
+  const int lane = threadIdx.x & 31;
+  int j = threadIdx.x, cur = j;
+  int s = 0, hops = 1, plen = 1, pm = 2, pa = 0, nev = 0;
+  uint32_t e0 = 0u, e1 = 0u, e2 = 0u;
+  for (;;) {
+    const bool active = j < kChainDraws;
+    if (!__any_sync(kFull, active)) break;
+    const bool ovf = cur >= kChainDraws;
+    const uint32_t te = C.ptab[s];
+    const uint32_t bt = te & 0xffffu;
+    const uint32_t bound = bt == 0xffffu ? (uint32_t)pm : bt;
+    const uint64_t A = (uint64_t)C.hi[active && !ovf ? cur : 0] * bound;
+    int v = (int)(A >> 32);
+    const bool slow = active && !ovf && (uint32_t)A >= 0u - bound;
+    if (__any_sync(kFull, slow)) {
+      if (slow) v = chain_exact_below(k0, k1, base + (uint64_t)cur, bound);
+      __syncwarp();
+    }
+    const int ph = s >> 2;
+    const bool same = v == pa;
+    const bool pb = ph == 4 && !same;
+    const bool rej = pb && s == 18 && abs(pa - v) < plen;
+    const bool pair_done = pb && !rej;
+    {
+      const uint32_t lo = (uint32_t)min(pa, v), hi = (uint32_t)max(pa, v);
+      const uint32_t x = s == 18 ? lo | (hi << 8) | ((uint32_t)plen << 16)
+                                 : (uint32_t)pa | ((uint32_t)v << 8) | (s == 19 ? (uint32_t)plen << 16 : 0u);
+      const bool put = active && pair_done;
+      e0 = put && nev == 0 ? x : e0;
+      e1 = put && nev == 1 ? x : e1;
+      e2 = put && nev == 2 ? x : e2;
+      nev += put ? 1 : 0;
+    }
+    const int nop = v < p1 ? 1 : v < p2 ? 2 : 3;
+    int ns = (int)(te >> 16);
+    ns = s == 0 ? (nop == 3 ? 11 : 4 + nop) : ns;
+    ns = ph == 4 && same ? s : ns;
+    ns = rej ? 14 : ns;
+    const int op = s & 3;
+    if (active) {  // (if-converted: plain register selects)
+      hops = s == 0 ? 1 : ph == 1 ? 1 + v : hops - (pair_done ? 1 : 0);
+      plen = ph == 2 ? 1 + v : plen;
+      pm = ph == 2 ? k - v : pm;  // k - len + 1 positions
+      pa = ph == 3 ? v : pa;
+      s = ns;
+      ++cur;
+    }
+    const bool fin = active && (ovf || (pair_done && hops == 0));
+    if (fin) {
+      C.jump[0][j] = ovf ? kChainOvf : (uint16_t)cur;
+      if (!ovf) C.desc[j] = make_uint4((uint32_t)op | ((uint32_t)nev << 4), e0, e1, e2);
+    }
+    const unsigned fm = __ballot_sync(kFull, fin);
+    if (fm) {  // warp-aggregated ticket
+      const int leader = __ffs(fm) - 1;
+      int t0 = 0;
+      if (lane == leader) t0 = atomicAdd(&C.ticket, __popc(fm));
+      t0 = __shfl_sync(kFull, t0, leader);
+      if (fin) {
+        j = t0 + __popc(fm & ((1u << lane) - 1u));
+        cur = j;
+        s = 0;
+        nev = 0;
+      }
+    }
+  }
+}
+
+// The chain from entry offset e, by one warp: lane l composes the jump tables along the
+// binary digits of l to find the node l proposals ahead, so 32 nodes cost five dependent
+// shared loads.  Writes C.start[0 .. n), C.n (0: the first proposal overflows the chunk) and
+// C.next = the offset after the last node.
+__device__ __forceinline__ void chain_follow(ChainSmem& C, int e, int64_t need, int lane) {
+  int x = e, n = 0, next = e;
+  for (;;) {
+    int y = x;
+#pragma unroll
+    for (int b = 0; b < kChainJumps; ++b)
+      if ((lane >> b) & 1) y = y < kChainDraws ? (int)C.jump[b][y] : y;
+    // node y is in the chain iff its proposal ends inside the chunk; nodes past the first
+    // failure fail too, so the valid lanes are a prefix
+    const bool ok = y < kChainDraws && C.jump[0][y] != kChainOvf;
+    int cnt = __popc(__ballot_sync(kFull, ok));
+    if ((int64_t)cnt > need - n) cnt = (int)(need - n);
+    if (lane < cnt) C.start[n + lane] = (uint16_t)y;
+    n += cnt;
+    const int last = __shfl_sync(kFull, y, cnt > 0 ? cnt - 1 : 0);
+    if (cnt > 0) next = C.jump[0][last];
+    if (cnt < 32 || n >= need) break;
+    x = next;
+  }
+  if (lane == 0) {
+    C.n = n;
+    C.next = next;
+  }
+}
+
+// cand = the proposal `d` applied to the lane-distributed key (op_element_swaps /
+// op_block_swaps / op_block_shift with the parsed positions)
+__device__ __forceinline__ void chain_apply(Key& c, const uint4 d, int k, int lane) {
+  const int op = (int)(d.x & 15u), ne = (int)(d.x >> 4);
+  const bool wide = k > 32;
+#pragma unroll 1
+  for (int e = 0; e < ne; ++e) {
+    const uint32_t ev = e == 0 ? d.y : e == 1 ? d.z : d.w;
+    const int x = (int)(ev & 255u), y = (int)((ev >> 8) & 255u), len = (int)(ev >> 16);
+    if (op == 1) {
+      c.swap_pos(x, y, lane);
+    } else if (op == 2) {  // x < y
+      auto src = [&](int l) {
+        if (l >= x && l < x + len) return l - x + y;
+        if (l >= y && l < y + len) return l - y + x;
+        return l;
+      };
+      c = c.gather(src(lane), src(lane + 32), wide);
+    } else {
+      const int lo = min(x, y), hi = max(x, y) + len, w = hi - lo;
+      const int sh = y > x ? len : w - len;
+      auto src = [&](int l) {
+        if (l >= lo && l < hi) {
+          int i = l - lo + sh;
+          if (i >= w) i -= w;
+          return lo + i;
+        }
+        return l;
+      };
+      c = c.gather(src(lane), src(lane + 32), wide);
+    }
+  }
+}
+
+template <int SLOTS, int ORDER, int P>
+__global__ void __launch_bounds__(P * 32, P >= 32 ? 1 : 32 / P)
+    sct_climb_chain_kernel(const SctLaunch p, const __grid_constant__ SumPlan plan) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int NT = P * 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const WarpSmem ws(smem, warp, p.n);
+  const double* logs = stage_logs<ORDER>(reinterpret_cast<double*>(smem), p.logs);
+  ChainSmem& C = *reinterpret_cast<ChainSmem*>(smem + kLogsBytes + P * sct_warp_bytes(p.n));
+
+  Evaluator<SLOTS, ORDER> ev;
+  ev.init(plan, p.k, p.n, lane);
+  const int kmax = p.k;
+  const int64_t climbings = p.climbings;
+
+  for (int64_t w = blockIdx.x; w < p.n_workers; w += gridDim.x) {
+    const int32_t cid = p.cipher_of[w];
+    const int k = p.key_lengths ? p.key_lengths[w] : kmax;
+    if (p.key_lengths) ev.set_k(k, lane);
+    stage_text(ws.txt, p.ciphers + p.offsets[cid], p.n, lane);
+    const uint64_t k0 = p.keys[2 * w], k1 = p.keys[2 * w + 1];
+    Draws d;
+    d.key = p.keys + 2 * w;
+    d.win = ws.win;
+    d.start(p.skips ? p.skips[w] : 0, lane);
+    Key key;
+    key.v0 = lane;
+    key.v1 = lane + 32;
+    for (int i = k - 1; i > 0; --i) {  // rng.py:91-97
+      const int j = d.below((uint32_t)(i + 1), lane);
+      key.swap_pos(i, j, lane);
+    }
+    uint64_t entry = d.position();  // the first proposal's first draw
+    double score = ev.score(key, ws.txt, ws.colstart, ws.plain, logs, lane);
+    int64_t last = -1, t = 0;
+    uint32_t rnd = 0;
+#ifdef CCG_CHAIN_PROFILE
+    long long pr_gen = 0, pr_end = 0, pr_chase = 0, pr_round = 0, pr_t0;
+    int pr_rounds = 0, pr_chunks = 0;
+#define PR_MARK(v) do { __syncthreads(); const long long _c = clock64(); v += _c - pr_t0; pr_t0 = _c; } while (0)
+#else
+#define PR_MARK(v) __syncthreads()
+#endif
+    while (t < climbings) {
+      // ---- parse the proposals of the next chunk of draws ----
+      const uint64_t base = entry & ~3ULL;
+      const int e = (int)(entry - base);
+      __syncthreads();  // the previous chunk's descriptors are consumed
+#ifdef CCG_CHAIN_PROFILE
+      pr_t0 = clock64();
+      ++pr_chunks;
+#endif
+      if (tid == 0) {
+        C.ticket = NT;
+        chain_parse_table(C.ptab, k, p.op1_hop, p.op2_hop);
+      }
+      for (int j = tid; j < kChainDraws / 4; j += NT) {
+        uint64_t v0, v1, v2, v3;
+        philox4x64_10(k0, k1, (base >> 2) + 1 + (uint64_t)j, v0, v1, v2, v3);
+        *reinterpret_cast<uint4*>(C.hi + 4 * j) =
+            make_uint4((uint32_t)(v0 >> 32), (uint32_t)(v1 >> 32), (uint32_t)(v2 >> 32), (uint32_t)(v3 >> 32));
+      }
+      PR_MARK(pr_gen);
+      chain_parse_lockstep(C, base, k0, k1, k, p.p1, p.p2);
+      PR_MARK(pr_end);
+      // jump tables: 2^b proposals ahead (entries >= kChainDraws are terminal)
+#pragma unroll 1
+      for (int b = 1; b < kChainJumps; ++b) {
+        for (int i = tid; i < kChainDraws; i += NT) {
+          const int x = C.jump[b - 1][i];
+          C.jump[b][i] = x < kChainDraws ? C.jump[b - 1][x] : (uint16_t)x;
+        }
+        __syncthreads();
+      }
+      if (warp == 0) {
+        chain_follow(C, e, climbings - t, lane);
+        if (lane == 0 && C.n == 0) {  // a proposal longer than the chunk: parse it from the stream
+          C.start[0] = (uint16_t)e;
+          C.next = chain_parse(nullptr, 0, e, base, k0, k1, k, p.p1, p.p2, p.op1_hop, p.op2_hop,
+                               &C.desc[e]);
+          C.n = 1;
+        }
+      }
+      PR_MARK(pr_chase);
+      const int n = C.n;
+      entry = base + (uint64_t)C.next;
+      // ---- speculative rounds over the chain ----
+      for (int tl = 0; tl < n;) {
+        const int avail = n - tl < P ? n - tl : P;
+        Key cand = key;
+        double cs = 0.0;
+        if (warp < avail) {
+          chain_apply(cand, C.desc[C.start[tl + warp]], k, lane);
+          cs = ev.score(cand, ws.txt, ws.colstart, ws.plain, logs, lane);
+        }
+        double* ex = C.score[rnd++ & 1u];
+        if (lane == 0) ex[warp] = cs;
+        __syncthreads();
+        // the first improvement (sct.py:168): lane j tests proposal t+j, one ballot
+        const unsigned better = __ballot_sync(kFull, lane < avail && ex[lane] > score);
+        const int acc = better ? __ffs(better) - 1 : -1;
+        const int used = acc >= 0 ? acc : avail - 1;
+        if (acc >= 0) {  // block-uniform: every warp read the same scores
+          if (warp == acc) {
+            if (lane < k) C.key[lane] = (uint8_t)cand.v0;
+            if (lane + 32 < k) C.key[lane + 32] = (uint8_t)cand.v1;
+          }
+          const double next_score = ex[acc];
+          __syncthreads();
+          key.v0 = lane < k ? C.key[lane] : lane;
+          key.v1 = lane + 32 < k ? C.key[lane + 32] : lane + 32;
+          score = next_score;
+          last = t + acc;
+        }
+        tl += used + 1;
+        t += used + 1;
+#ifdef CCG_CHAIN_PROFILE
+        ++pr_rounds;
+#endif
+      }
+      PR_MARK(pr_round);
+    }
+#ifdef CCG_CHAIN_PROFILE
+    if (tid == 0 && w < 2)
+      printf("chain profile w=%lld: chunks %d rounds %d tries %lld | cycles gen %lld end %lld chase %lld rounds %lld\n",
+             (long long)w, pr_chunks, pr_rounds, (long long)t, pr_gen, pr_end, pr_chase, pr_round);
+#endif
+    if (warp == 0) {
+      if (lane < k) p.keys_out[w * kmax + lane] = (uint8_t)key.v0;
+      if (lane + 32 < k) p.keys_out[w * kmax + lane + 32] = (uint8_t)key.v1;
+      if (lane == 0) {
+        p.scores[w] = score;
+        if (p.draws_used) p.draws_used[w] = entry;
+        if (p.last_accept) p.last_accept[w] = last;
+        if (p.tries_done) p.tries_done[w] = t;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Score given (cipher, key) pairs with the same evaluator (sct.py:158-160).
 template <int SLOTS, int ORDER>
 __global__ void __launch_bounds__(kSctWarps * 32)
@@ -809,6 +1231,38 @@ cudaError_t climb_spec_slots(cudaStream_t s, const SctLaunch& p, const SumPlan& 
   return spec_launch<SLOTS, ORDER, 2>(s, p, plan, sm_count, launched);
 }
 
+template <int SLOTS, int ORDER, int P>
+cudaError_t chain_launch(cudaStream_t s, const SctLaunch& p, const SumPlan& plan, int sm_count,
+                         bool* launched) {
+  *launched = false;
+  auto kern = sct_climb_chain_kernel<SLOTS, ORDER, P>;
+  const size_t bytes = kLogsBytes + P * sct_warp_bytes(p.n) + sizeof(ChainSmem);
+  if (bytes > kMaxSmemPerBlock) return cudaSuccess;  // long texts: fewer warps per worker
+  cudaError_t e = prep_smem(kern, bytes);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P * 32, bytes);
+  if (e != cudaSuccess) return e;
+  if ((int64_t)per_sm * sm_count < p.n_workers) return cudaSuccess;  // more than one wave
+  kern<<<(unsigned)p.n_workers, P * 32, bytes, s>>>(p, plan);
+  *launched = true;
+  return cudaGetLastError();
+}
+
+// Chain-parsed latency mode: the deepest speculation (32, 16, 8 or 4 warps per worker) whose
+// CTAs all fit at once.  *launched = false: none fits.
+template <int SLOTS, int ORDER>
+cudaError_t climb_chain_slots(cudaStream_t s, const SctLaunch& p, const SumPlan& plan, int sm_count,
+                              bool* launched) {
+  cudaError_t e = chain_launch<SLOTS, ORDER, 32>(s, p, plan, sm_count, launched);
+  if (e != cudaSuccess || *launched) return e;
+  e = chain_launch<SLOTS, ORDER, 16>(s, p, plan, sm_count, launched);
+  if (e != cudaSuccess || *launched) return e;
+  e = chain_launch<SLOTS, ORDER, 8>(s, p, plan, sm_count, launched);
+  if (e != cudaSuccess || *launched) return e;
+  return chain_launch<SLOTS, ORDER, 4>(s, p, plan, sm_count, launched);
+}
+
 template <int SLOTS, int ORDER>
 cudaError_t score_slots(cudaStream_t s, const uint8_t* ciphers, const int64_t* offsets,
                         const int32_t* cipher_of, const uint8_t* keys, int32_t k, int64_t n_keys,
@@ -866,7 +1320,18 @@ static cudaError_t climb_order(cudaStream_t s, const SctLaunch& p, const SumPlan
   // latency mode: few enough workers that each can get a CTA of speculating warps
   if (p.n_workers <= 16 * (int64_t)sm_count && !(p.flags & CCG_FLAG_SCT_NO_SPEC)) {
     bool launched = false;
-    cudaError_t e;
+    cudaError_t e = cudaSuccess;
+    // the chain-parsed kernel's descriptors hold up to kSctLaneMaxHops events per proposal
+    if (!(p.flags & CCG_FLAG_SCT_SPEC_REPLAY) && p.op1_hop <= kSctLaneMaxHops &&
+        p.op2_hop <= kSctLaneMaxHops) {
+      switch (slots_for(plan)) {
+        case 1: e = climb_chain_slots<1, ORDER>(s, p, plan, sm_count, &launched); break;
+        case 2: e = climb_chain_slots<2, ORDER>(s, p, plan, sm_count, &launched); break;
+        case 4: e = climb_chain_slots<4, ORDER>(s, p, plan, sm_count, &launched); break;
+        default: e = climb_chain_slots<8, ORDER>(s, p, plan, sm_count, &launched); break;
+      }
+      if (e != cudaSuccess || launched) return e;
+    }
     switch (slots_for(plan)) {
       case 1: e = climb_spec_slots<1, ORDER>(s, p, plan, sm_count, &launched); break;
       case 2: e = climb_spec_slots<2, ORDER>(s, p, plan, sm_count, &launched); break;

@@ -204,7 +204,9 @@ def sct_climb(ciphers, cipher_of, keys, logs, key_length, climbings, *, p1=33, p
     uint8[n, max key length], row i valid in its first key_length[i] entries.  Ciphertexts
     may have any mix of lengths.  Kernels (identical results): with at most a few workers per
     SM and one common text length, each worker gets a CTA of warps that evaluate consecutive
-    proposals speculatively (speculate=False turns this off); otherwise one worker per lane
+    proposals speculatively from its proposal chain parsed ahead (speculate="replay": the
+    kernel whose warps replay their predecessors' draws instead; speculate=False turns
+    speculation off); otherwise one worker per lane
     (kernel="lane"); kernel="warp" forces the one-warp-per-worker kernel (one text length)."""
     flat, off = _lib.ragged(ciphers)
     cof = np.ascontiguousarray(cipher_of, dtype=np.int32).reshape(-1)
@@ -252,7 +254,9 @@ def sct_climb(ciphers, cipher_of, keys, logs, key_length, climbings, *, p1=33, p
         a.tries_done = _lib.ptr(out.tries_done)
         a.group_size, a.group_best = int(group_size), _lib.ptr(out.group_best)
         a.order = int(order)
-        a.flags = ((0 if speculate else _lib.FLAG_SCT_NO_SPEC) | _lib.SCT_KERNEL_FLAGS[kernel]
+        a.flags = ((0 if speculate else _lib.FLAG_SCT_NO_SPEC)
+                   | (_lib.FLAG_SCT_SPEC_REPLAY if speculate == "replay" else 0)
+                   | _lib.SCT_KERNEL_FLAGS[kernel]
                    | (_lib.FLAG_SCT_TABLE_L2 if table_l2 else 0))
         kl = None if klens is None else np.ascontiguousarray(klens[lo:hi])
         a.key_lengths = _lib.ptr(kl)

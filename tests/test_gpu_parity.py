@@ -250,9 +250,10 @@ def test_mas_results_independent_of_device_split():
 
 @pytest.mark.parametrize("order,kmax", [(2, 40), (3, 40), (2, 32), (3, 17)])
 def test_sct_speculative_kernel_matches_warp_kernel(order, kmax):
-    """Few workers run on the speculative CTA-per-worker kernel (ccg_sct.cu
-    sct_climb_spec_kernel): every output equals the one-warp-per-worker kernel's, for ragged
-    key lengths and budgets that are not multiples of the speculation depth."""
+    """Few workers run on the speculative CTA-per-worker kernels (ccg_sct.cu
+    sct_climb_chain_kernel, and sct_climb_spec_kernel with speculate="replay"): every output
+    equals the one-warp-per-worker kernel's, for ragged key lengths and budgets that are not
+    multiples of the speculation depth."""
     rng = np.random.default_rng(90 + order)
     n_len = 333
     cs = [rng.integers(0, 26, n_len) for _ in range(3)]
@@ -265,13 +266,37 @@ def test_sct_speculative_kernel_matches_warp_kernel(order, kmax):
     for climb in (0, 1, 2, 3, 5, 417):
         kw = dict(order=order, draws_used=True, last_accept=True, tries_done=True)
         a = engine.sct_climb(cs, cof, keys, logs, klens, climb, **kw)
+        r = engine.sct_climb(cs, cof, keys, logs, klens, climb, speculate="replay", **kw)
         b = engine.sct_climb(cs, cof, keys, logs, klens, climb, speculate=False, **kw)
-        assert a.scores.tolist() == b.scores.tolist(), climb
-        for i in range(m):
-            assert np.array_equal(a.keys[i, :klens[i]], b.keys[i, :klens[i]]), (climb, i)
-        assert np.array_equal(a.draws_used, b.draws_used), climb
-        assert np.array_equal(a.last_accept, b.last_accept), climb
-        assert np.array_equal(a.tries_done, b.tries_done), climb
+        for x in (a, r):
+            assert x.scores.tolist() == b.scores.tolist(), climb
+            for i in range(m):
+                assert np.array_equal(x.keys[i, :klens[i]], b.keys[i, :klens[i]]), (climb, i)
+            assert np.array_equal(x.draws_used, b.draws_used), climb
+            assert np.array_equal(x.last_accept, b.last_accept), climb
+            assert np.array_equal(x.tries_done, b.tries_done), climb
+
+
+@pytest.mark.parametrize("k,hops", [(2, (1, 1)), (3, (3, 1)), (7, (2, 3)), (12, (3, 3)), (64, (3, 2))])
+def test_sct_chain_kernel_long_climbs(k, hops):
+    """The chain-parsed latency kernel across many parse chunks (4,096 draws each) and odd
+    operator mixes: identical to the one-warp kernel for every output."""
+    rng = np.random.default_rng(500 + k)
+    n_len = 200 if k < 64 else 300
+    cs = [rng.integers(0, 26, n_len) for _ in range(2)]
+    logs = -rng.random(676) * 20 - 1
+    m = 6
+    cof = (np.arange(m) % 2).astype(np.int32)
+    keys = philox_keys([77], list(range(m)))
+    kw = dict(draws_used=True, last_accept=True, tries_done=True, op1_hop=hops[0],
+              op2_hop=hops[1], p1=20, p2=55)
+    a = engine.sct_climb(cs, cof, keys, logs, k, 5000, **kw)
+    b = engine.sct_climb(cs, cof, keys, logs, k, 5000, speculate=False, **kw)
+    assert a.scores.tolist() == b.scores.tolist()
+    assert np.array_equal(a.keys, b.keys)
+    assert np.array_equal(a.draws_used, b.draws_used)
+    assert np.array_equal(a.last_accept, b.last_accept)
+    assert np.array_equal(a.tries_done, b.tries_done)
 
 
 def test_restarts_stop_and_prefix(golden):
