@@ -315,20 +315,20 @@ struct Evaluator {
       }
       res[s] = acc;
     }
+    // leaf sums to lanes: lane L gets leaf L (slot L / 4, 8-lane group L % 4)
+    double lv = 0.0;
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+      const double v = __shfl_sync(kFull, res[s], 8 * (lane & 3));
+      if ((lane >> 2) == s) lv = v;
+    }
     // replay the recursion's merges (post-order): leaf[dst] = leaf[dst] + leaf[src]
     const SumPlan& P = *plan;
     for (int m = 0; m < P.n_merges; ++m) {
-      const int d = P.merge_dst[m], sidx = P.merge_src[m];
-      double sv = 0.0;
-#pragma unroll
-      for (int s = 0; s < SLOTS; ++s)
-        if (s == (sidx >> 2)) sv = res[s];
-      sv = __shfl_sync(kFull, sv, 8 * (sidx & 3));
-#pragma unroll
-      for (int s = 0; s < SLOTS; ++s)
-        if (s == (d >> 2) && (lane >> 3) == (d & 3)) res[s] = res[s] + sv;
+      const double sv = __shfl_sync(kFull, lv, P.merge_src[m]);
+      if (lane == P.merge_dst[m]) lv = lv + sv;
     }
-    const double out = __shfl_sync(kFull, res[0], 0);
+    const double out = __shfl_sync(kFull, lv, 0);
     __syncwarp();  // plain / colstart are rewritten by the next candidate
     return out;
   }
