@@ -651,6 +651,7 @@ constexpr int kChainDraws = 4096;               // draws per parsed chunk
 constexpr int kChainMaxProps = kChainDraws / 4;  // every proposal reads at least 4 draws
 constexpr uint16_t kChainOvf = 0xffffu;          // the proposal runs past the chunk
 constexpr int kChainJumps = 5;
+constexpr int kChainBudget = 24;                 // draws per proposal in the first parse pass
 constexpr size_t kMaxSmemPerBlock = 227 * 1024;  // sm_100 opt-in dynamic shared memory per block                   // jump tables of 1, 2, 4, 8, 16 proposals
 
 struct ChainSmem {
@@ -662,7 +663,8 @@ struct ChainSmem {
   double score[2][32];                 // round exchange, alternated by round
   uint8_t key[kSctMaxKey];
   int n, next;                         // proposals in the chain; offset of the one after them
-  int ticket;                          // next offset to parse (chain_parse_lockstep)
+  uint16_t queue[kChainDraws];         // offsets whose proposal outran the first pass's budget
+  int ticket, n_queued;                // next item to parse; queue length (chain_parse_lockstep)
   uint32_t ptab[20];                   // parse automaton table (chain_parse_table)
 };
 
@@ -778,14 +780,25 @@ __device__ __forceinline__ void chain_parse_table(uint32_t* t, int k, int h1, in
 // long proposals do not leave the rest of their warp idle.  Every lane runs every step
 // (inactive lanes with their state frozen), so the warp stays converged: only the rare exact
 // conversion and the stores are predicated branches.
+//
+// Proposal lengths are heavy-tailed (block swaps redraw whole pairs while |p - q| < len: ~2 %
+// of k = 10 proposals read more than 64 draws, a few several hundred), and a warp runs until
+// its slowest lane is done.  So the first pass gives each proposal kChainBudget draws and
+// queues the offsets that need more; the second pass (PASS2) parses the queued offsets in
+// full, from their start.
+template <bool PASS2>
 __device__ __forceinline__ void chain_parse_lockstep(ChainSmem& C, uint64_t base, uint64_t k0,
                                                      uint64_t k1, int k, int p1, int p2) {
   const int lane = threadIdx.x & 31;
-  int j = threadIdx.x, cur = j;
+  const int lim = PASS2 ? C.n_queued : kChainDraws;
+  int j = threadIdx.x;
+  auto offset_of = [&](int item) { return PASS2 ? (int)C.queue[item] : item; };
+  int o = j < lim ? offset_of(j) : 0;  // the offset being parsed
+  int cur = o;
   int s = 0, hops = 1, plen = 1, pm = 2, pa = 0, nev = 0;
   uint32_t e0 = 0u, e1 = 0u, e2 = 0u;
   for (;;) {
-    const bool active = j < kChainDraws;
+    const bool active = j < lim;
     if (!__any_sync(kFull, active)) break;
     const bool ovf = cur >= kChainDraws;
     const uint32_t te = C.ptab[s];
@@ -827,11 +840,23 @@ __device__ __forceinline__ void chain_parse_lockstep(ChainSmem& C, uint64_t base
       s = ns;
       ++cur;
     }
-    const bool fin = active && (ovf || (pair_done && hops == 0));
-    if (fin) {
-      C.jump[0][j] = ovf ? kChainOvf : (uint16_t)cur;
-      if (!ovf) C.desc[j] = make_uint4((uint32_t)op | ((uint32_t)nev << 4), e0, e1, e2);
+    const bool done = active && (ovf || (pair_done && hops == 0));
+    const bool defer = !PASS2 && active && !done && cur - o >= kChainBudget;  // to the second pass
+    if (done) {
+      C.jump[0][o] = ovf ? kChainOvf : (uint16_t)cur;
+      if (!ovf) C.desc[o] = make_uint4((uint32_t)op | ((uint32_t)nev << 4), e0, e1, e2);
     }
+    if (!PASS2) {  // warp-aggregated push of the deferred offsets
+      const unsigned dm = __ballot_sync(kFull, defer);
+      if (dm) {
+        const int leader = __ffs(dm) - 1;
+        int q0 = 0;
+        if (lane == leader) q0 = atomicAdd(&C.n_queued, __popc(dm));
+        q0 = __shfl_sync(kFull, q0, leader);
+        if (defer) C.queue[q0 + __popc(dm & ((1u << lane) - 1u))] = (uint16_t)o;
+      }
+    }
+    const bool fin = done || defer;
     const unsigned fm = __ballot_sync(kFull, fin);
     if (fm) {  // warp-aggregated ticket
       const int leader = __ffs(fm) - 1;
@@ -840,7 +865,8 @@ __device__ __forceinline__ void chain_parse_lockstep(ChainSmem& C, uint64_t base
       t0 = __shfl_sync(kFull, t0, leader);
       if (fin) {
         j = t0 + __popc(fm & ((1u << lane) - 1u));
-        cur = j;
+        o = j < lim ? offset_of(j) : 0;
+        cur = o;
         s = 0;
         nev = 0;
       }
@@ -948,7 +974,7 @@ __global__ void __launch_bounds__(P * 32, P >= 32 ? 1 : 32 / P)
     int64_t last = -1, t = 0;
     uint32_t rnd = 0;
 #ifdef CCG_CHAIN_PROFILE
-    long long pr_gen = 0, pr_end = 0, pr_chase = 0, pr_round = 0, pr_t0;
+    long long pr_gen = 0, pr_end = 0, pr_end2 = 0, pr_chase = 0, pr_round = 0, pr_t0;
     int pr_rounds = 0, pr_chunks = 0;
 #define PR_MARK(v) do { __syncthreads(); const long long _c = clock64(); v += _c - pr_t0; pr_t0 = _c; } while (0)
 #else
@@ -965,6 +991,7 @@ __global__ void __launch_bounds__(P * 32, P >= 32 ? 1 : 32 / P)
 #endif
       if (tid == 0) {
         C.ticket = NT;
+        C.n_queued = 0;
         chain_parse_table(C.ptab, k, p.op1_hop, p.op2_hop);
       }
       for (int j = tid; j < kChainDraws / 4; j += NT) {
@@ -974,8 +1001,12 @@ __global__ void __launch_bounds__(P * 32, P >= 32 ? 1 : 32 / P)
             make_uint4((uint32_t)(v0 >> 32), (uint32_t)(v1 >> 32), (uint32_t)(v2 >> 32), (uint32_t)(v3 >> 32));
       }
       PR_MARK(pr_gen);
-      chain_parse_lockstep(C, base, k0, k1, k, p.p1, p.p2);
+      chain_parse_lockstep<false>(C, base, k0, k1, k, p.p1, p.p2);
       PR_MARK(pr_end);
+      if (tid == 0) C.ticket = NT;
+      __syncthreads();
+      chain_parse_lockstep<true>(C, base, k0, k1, k, p.p1, p.p2);
+      PR_MARK(pr_end2);
       // jump tables: 2^b proposals ahead (entries >= kChainDraws are terminal)
 #pragma unroll 1
       for (int b = 1; b < kChainJumps; ++b) {
@@ -1035,8 +1066,8 @@ __global__ void __launch_bounds__(P * 32, P >= 32 ? 1 : 32 / P)
     }
 #ifdef CCG_CHAIN_PROFILE
     if (tid == 0 && w < 2)
-      printf("chain profile w=%lld: chunks %d rounds %d tries %lld | cycles gen %lld end %lld chase %lld rounds %lld\n",
-             (long long)w, pr_chunks, pr_rounds, (long long)t, pr_gen, pr_end, pr_chase, pr_round);
+      printf("chain profile w=%lld: chunks %d rounds %d tries %lld | cycles gen %lld end %lld end2 %lld chase %lld rounds %lld (queued last chunk %d)\n",
+             (long long)w, pr_chunks, pr_rounds, (long long)t, pr_gen, pr_end, pr_end2, pr_chase, pr_round, C.n_queued);
 #endif
     if (warp == 0) {
       if (lane < k) p.keys_out[w * kmax + lane] = (uint8_t)key.v0;

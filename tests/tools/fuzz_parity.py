@@ -82,8 +82,10 @@ def fuzz_sct(rng, stats):
     p1, p2 = sorted(int(v) for v in rng.integers(0, 101, 2))
     hmax = 4 if kernel == "lane" else 10  # the lane kernels take up to 3 hops
     h1, h2 = int(rng.integers(1, hmax)), int(rng.integers(1, hmax))
-    climb = int(rng.choice([0, 1, 50, 400]))
-    spec = bool(rng.integers(0, 2))  # speculative CTA kernel or one warp per worker
+    climb = int(rng.choice([0, 1, 50, 400, 3000]))
+    # few workers: the chain-parsed speculative CTA kernel (hops <= 3), the replaying one, or
+    # one warp per worker
+    spec = [True, "replay", False][int(rng.integers(0, 3))]
     res = engine.sct_climb(cs, cof, philox_keys(seeds, streams), logs, klens, climb, p1=p1, p2=p2,
                            op1_hop=h1, op2_hop=h2, order=order, speculate=spec, kernel=kernel)
     for i in range(m):
@@ -94,6 +96,8 @@ def fuzz_sct(rng, stats):
             raise AssertionError(f"SCT mismatch: kernel={kernel} order={order} k={k} climb={climb}")
     stats["sct_workers"] += m
     stats["sct_lane_workers" if kernel == "lane" else "sct_warp_workers"] += m
+    if kernel == "warp" and spec is True and max(h1, h2) <= 3:
+        stats["sct_chain_workers"] += m
 
 
 def fuzz_sct_fast(rng, stats):
@@ -149,7 +153,7 @@ def main():
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     stats = {"rounds": 0, "mas_workers": 0, "mas_tries": 0, "ngram_workers": 0, "sct_workers": 0,
-             "sct_warp_workers": 0, "sct_lane_workers": 0, "sct_fast_workers": 0, "det_jobs": 0}
+             "sct_warp_workers": 0, "sct_lane_workers": 0, "sct_chain_workers": 0, "sct_fast_workers": 0, "det_jobs": 0}
     t0 = time.time()
     while time.time() - t0 < a.seconds:
         for f in (fuzz_mas, fuzz_ngram, fuzz_sct, fuzz_sct_fast, fuzz_det):
