@@ -26,13 +26,14 @@
 //    bit-identical to numpy's float64 sum, so accept decisions match the reference.
 //  * Tables: the 676 float64 log2 probabilities and each warp's ciphertext are staged in
 //    shared memory; colstart is a per-warp 64-entry u16 array (conflict-free).
-#include <cstdio>
+#include <cooperative_groups.h>
 
 #include "ccg_internal.h"
 #include "ccg_rng.cuh"
 
 namespace ccg {
 namespace {
+namespace cg = cooperative_groups;
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kSctWarps = 8;
@@ -937,6 +938,55 @@ __device__ __forceinline__ void chain_apply(Key& c, const uint4 d, int k, int la
   }
 }
 
+// One chunk of the proposal chain, by the whole CTA (nt threads): the draws from stream
+// index `entry` on, every offset's proposal (two lockstep passes), the jump tables and the
+// chain of at most `need` proposals from the entry.  Ends with a barrier; then C.n proposals
+// start at C.start[j] (descriptors C.desc[C.start[j]]) and the next chunk's entry is
+// (entry & ~3) + C.next.
+__device__ __forceinline__ void chain_parse_chunk(ChainSmem& C, uint64_t entry, int64_t need,
+                                                  uint64_t k0, uint64_t k1, int k, int p1, int p2,
+                                                  int h1, int h2, int nt) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t base = entry & ~3ULL;
+  const int e = (int)(entry - base);
+  if (tid == 0) {
+    C.ticket = nt;
+    C.n_queued = 0;
+    chain_parse_table(C.ptab, k, h1, h2);
+  }
+  for (int j = tid; j < kChainDraws / 4; j += nt) {
+    uint64_t v0, v1, v2, v3;
+    philox4x64_10(k0, k1, (base >> 2) + 1 + (uint64_t)j, v0, v1, v2, v3);
+    *reinterpret_cast<uint4*>(C.hi + 4 * j) =
+        make_uint4((uint32_t)(v0 >> 32), (uint32_t)(v1 >> 32), (uint32_t)(v2 >> 32), (uint32_t)(v3 >> 32));
+  }
+  __syncthreads();
+  chain_parse_lockstep<false>(C, base, k0, k1, k, p1, p2);
+  __syncthreads();
+  if (tid == 0) C.ticket = nt;
+  __syncthreads();
+  chain_parse_lockstep<true>(C, base, k0, k1, k, p1, p2);
+  __syncthreads();
+  // jump tables: 2^b proposals ahead (entries >= kChainDraws are terminal)
+#pragma unroll 1
+  for (int b = 1; b < kChainJumps; ++b) {
+    for (int i = tid; i < kChainDraws; i += nt) {
+      const int x = C.jump[b - 1][i];
+      C.jump[b][i] = x < kChainDraws ? C.jump[b - 1][x] : (uint16_t)x;
+    }
+    __syncthreads();
+  }
+  if (warp == 0) {
+    chain_follow(C, e, need, lane);
+    if (lane == 0 && C.n == 0) {  // a proposal longer than the chunk: parse it from the stream
+      C.start[0] = (uint16_t)e;
+      C.next = chain_parse(nullptr, 0, e, base, k0, k1, k, p1, p2, h1, h2, &C.desc[e]);
+      C.n = 1;
+    }
+  }
+  __syncthreads();
+}
+
 template <int SLOTS, int ORDER, int P>
 __global__ void __launch_bounds__(P * 32, P >= 32 ? 1 : 32 / P)
     sct_climb_chain_kernel(const SctLaunch p, const __grid_constant__ SumPlan plan) {
@@ -973,61 +1023,12 @@ __global__ void __launch_bounds__(P * 32, P >= 32 ? 1 : 32 / P)
     double score = ev.score(key, ws.txt, ws.colstart, ws.plain, logs, lane);
     int64_t last = -1, t = 0;
     uint32_t rnd = 0;
-#ifdef CCG_CHAIN_PROFILE
-    long long pr_gen = 0, pr_end = 0, pr_end2 = 0, pr_chase = 0, pr_round = 0, pr_t0;
-    int pr_rounds = 0, pr_chunks = 0;
-#define PR_MARK(v) do { __syncthreads(); const long long _c = clock64(); v += _c - pr_t0; pr_t0 = _c; } while (0)
-#else
-#define PR_MARK(v) __syncthreads()
-#endif
     while (t < climbings) {
       // ---- parse the proposals of the next chunk of draws ----
-      const uint64_t base = entry & ~3ULL;
-      const int e = (int)(entry - base);
       __syncthreads();  // the previous chunk's descriptors are consumed
-#ifdef CCG_CHAIN_PROFILE
-      pr_t0 = clock64();
-      ++pr_chunks;
-#endif
-      if (tid == 0) {
-        C.ticket = NT;
-        C.n_queued = 0;
-        chain_parse_table(C.ptab, k, p.op1_hop, p.op2_hop);
-      }
-      for (int j = tid; j < kChainDraws / 4; j += NT) {
-        uint64_t v0, v1, v2, v3;
-        philox4x64_10(k0, k1, (base >> 2) + 1 + (uint64_t)j, v0, v1, v2, v3);
-        *reinterpret_cast<uint4*>(C.hi + 4 * j) =
-            make_uint4((uint32_t)(v0 >> 32), (uint32_t)(v1 >> 32), (uint32_t)(v2 >> 32), (uint32_t)(v3 >> 32));
-      }
-      PR_MARK(pr_gen);
-      chain_parse_lockstep<false>(C, base, k0, k1, k, p.p1, p.p2);
-      PR_MARK(pr_end);
-      if (tid == 0) C.ticket = NT;
-      __syncthreads();
-      chain_parse_lockstep<true>(C, base, k0, k1, k, p.p1, p.p2);
-      PR_MARK(pr_end2);
-      // jump tables: 2^b proposals ahead (entries >= kChainDraws are terminal)
-#pragma unroll 1
-      for (int b = 1; b < kChainJumps; ++b) {
-        for (int i = tid; i < kChainDraws; i += NT) {
-          const int x = C.jump[b - 1][i];
-          C.jump[b][i] = x < kChainDraws ? C.jump[b - 1][x] : (uint16_t)x;
-        }
-        __syncthreads();
-      }
-      if (warp == 0) {
-        chain_follow(C, e, climbings - t, lane);
-        if (lane == 0 && C.n == 0) {  // a proposal longer than the chunk: parse it from the stream
-          C.start[0] = (uint16_t)e;
-          C.next = chain_parse(nullptr, 0, e, base, k0, k1, k, p.p1, p.p2, p.op1_hop, p.op2_hop,
-                               &C.desc[e]);
-          C.n = 1;
-        }
-      }
-      PR_MARK(pr_chase);
+      chain_parse_chunk(C, entry, climbings - t, k0, k1, k, p.p1, p.p2, p.op1_hop, p.op2_hop, NT);
       const int n = C.n;
-      entry = base + (uint64_t)C.next;
+      entry = (entry & ~3ULL) + (uint64_t)C.next;
       // ---- speculative rounds over the chain ----
       for (int tl = 0; tl < n;) {
         const int avail = n - tl < P ? n - tl : P;
@@ -1058,17 +1059,8 @@ __global__ void __launch_bounds__(P * 32, P >= 32 ? 1 : 32 / P)
         }
         tl += used + 1;
         t += used + 1;
-#ifdef CCG_CHAIN_PROFILE
-        ++pr_rounds;
-#endif
       }
-      PR_MARK(pr_round);
     }
-#ifdef CCG_CHAIN_PROFILE
-    if (tid == 0 && w < 2)
-      printf("chain profile w=%lld: chunks %d rounds %d tries %lld | cycles gen %lld end %lld end2 %lld chase %lld rounds %lld (queued last chunk %d)\n",
-             (long long)w, pr_chunks, pr_rounds, (long long)t, pr_gen, pr_end, pr_end2, pr_chase, pr_round, C.n_queued);
-#endif
     if (warp == 0) {
       if (lane < k) p.keys_out[w * kmax + lane] = (uint8_t)key.v0;
       if (lane + 32 < k) p.keys_out[w * kmax + lane + 32] = (uint8_t)key.v1;
@@ -1080,6 +1072,144 @@ __global__ void __launch_bounds__(P * 32, P >= 32 ? 1 : 32 / P)
       }
     }
     __syncthreads();
+  }
+}
+
+// ---- Latency mode on a pair of SMs (sct_climb_pair_kernel) ----
+// A restart is 64 workers, so in latency mode most of the GPU's 148 SMs idle.  Here each
+// worker gets a cluster of two CTAs: CTA 1 parses the worker's proposal chain chunk by chunk
+// (chain_parse_chunk, as above) and copies each chunk's descriptors into CTA 0's shared
+// memory (distributed shared memory); CTA 0 runs the speculative scoring rounds.  Double
+// buffering lets CTA 1 parse chunk c+1 while CTA 0 scores chunk c; one cluster barrier per
+// chunk hands the buffers over.
+struct PairBuf {  // in the scoring CTA
+  uint4 desc[2][kChainMaxProps];
+  int n[2];
+  double score[2][32];
+  uint8_t key[kSctMaxKey];
+};
+constexpr int kPairWarps = 32;
+
+__host__ __device__ inline size_t pair_buf_offset(int n) {
+  return kLogsBytes + kPairWarps * sct_warp_bytes(n);
+}
+__host__ __device__ inline size_t pair_smem_bytes(int n) {
+  const size_t scorer = pair_buf_offset(n) + sizeof(PairBuf);
+  return scorer > sizeof(ChainSmem) ? scorer : sizeof(ChainSmem);
+}
+
+template <int SLOTS, int ORDER>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairWarps * 32, 1)
+    sct_climb_pair_kernel(const SctLaunch p, const __grid_constant__ SumPlan plan) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int P = kPairWarps, NT = kPairWarps * 32;
+  cg::cluster_group cluster = cg::this_cluster();
+  const unsigned rank = cluster.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kmax = p.k;
+  const int64_t climbings = p.climbings;
+  const int64_t n_pairs = gridDim.x / 2;
+  PairBuf* buf_view = reinterpret_cast<PairBuf*>(smem + pair_buf_offset(p.n));
+
+  if (rank == 1) {
+    // ---- the parsing CTA ----
+    ChainSmem& C = *reinterpret_cast<ChainSmem*>(smem);
+    PairBuf* remote = cluster.map_shared_rank(buf_view, 0);
+    for (int64_t w = blockIdx.x / 2; w < p.n_workers; w += n_pairs) {
+      const int k = p.key_lengths ? p.key_lengths[w] : kmax;
+      const uint64_t k0 = p.keys[2 * w], k1 = p.keys[2 * w + 1];
+      // the first proposal follows permutation(k)'s k - 1 draws (rng.py:91-97)
+      uint64_t entry = (p.skips ? p.skips[w] : 0) + (uint64_t)(k - 1);
+      int64_t produced = 0;
+      int b = 0;
+      while (produced < climbings) {
+        chain_parse_chunk(C, entry, climbings - produced, k0, k1, k, p.p1, p.p2, p.op1_hop,
+                          p.op2_hop, NT);
+        const int n = C.n;
+        for (int j = tid; j < n; j += NT) remote->desc[b][j] = C.desc[C.start[j]];
+        if (tid == 0) remote->n[b] = n;
+        entry = (entry & ~3ULL) + (uint64_t)C.next;
+        produced += n;
+        cluster.sync();  // chunk ready; the scorers are done with the buffer written next
+        b ^= 1;
+      }
+      if (tid == 0 && p.draws_used) p.draws_used[w] = entry;
+      cluster.sync();  // end of the worker
+    }
+    return;
+  }
+
+  // ---- the scoring CTA ----
+  const WarpSmem ws(smem, warp, p.n);
+  const double* logs = stage_logs<ORDER>(reinterpret_cast<double*>(smem), p.logs);
+  PairBuf& B = *buf_view;
+  Evaluator<SLOTS, ORDER> ev;
+  ev.init(plan, p.k, p.n, lane);
+  for (int64_t w = blockIdx.x / 2; w < p.n_workers; w += n_pairs) {
+    const int32_t cid = p.cipher_of[w];
+    const int k = p.key_lengths ? p.key_lengths[w] : kmax;
+    if (p.key_lengths) ev.set_k(k, lane);
+    stage_text(ws.txt, p.ciphers + p.offsets[cid], p.n, lane);
+    Draws d;
+    d.key = p.keys + 2 * w;
+    d.win = ws.win;
+    d.start(p.skips ? p.skips[w] : 0, lane);
+    Key key;
+    key.v0 = lane;
+    key.v1 = lane + 32;
+    for (int i = k - 1; i > 0; --i) {  // rng.py:91-97
+      const int j = d.below((uint32_t)(i + 1), lane);
+      key.swap_pos(i, j, lane);
+    }
+    double score = ev.score(key, ws.txt, ws.colstart, ws.plain, logs, lane);
+    int64_t last = -1, t = 0;
+    uint32_t rnd = 0;
+    int b = 0;
+    while (t < climbings) {
+      cluster.sync();  // the parser's chunk is in buffer b
+      const int n = B.n[b];
+      for (int tl = 0; tl < n;) {
+        const int avail = n - tl < P ? n - tl : P;
+        Key cand = key;
+        double cs = 0.0;
+        if (warp < avail) {
+          chain_apply(cand, B.desc[b][tl + warp], k, lane);
+          cs = ev.score(cand, ws.txt, ws.colstart, ws.plain, logs, lane);
+        }
+        double* ex = B.score[rnd++ & 1u];
+        if (lane == 0) ex[warp] = cs;
+        __syncthreads();
+        // the first improvement (sct.py:168): lane j tests proposal t+j, one ballot
+        const unsigned better = __ballot_sync(kFull, lane < avail && ex[lane] > score);
+        const int acc = better ? __ffs(better) - 1 : -1;
+        const int used = acc >= 0 ? acc : avail - 1;
+        if (acc >= 0) {  // block-uniform: every warp read the same scores
+          if (warp == acc) {
+            if (lane < k) B.key[lane] = (uint8_t)cand.v0;
+            if (lane + 32 < k) B.key[lane + 32] = (uint8_t)cand.v1;
+          }
+          const double next_score = ex[acc];
+          __syncthreads();
+          key.v0 = lane < k ? B.key[lane] : lane;
+          key.v1 = lane + 32 < k ? B.key[lane + 32] : lane + 32;
+          score = next_score;
+          last = t + acc;
+        }
+        tl += used + 1;
+        t += used + 1;
+      }
+      b ^= 1;
+    }
+    if (warp == 0) {
+      if (lane < k) p.keys_out[w * kmax + lane] = (uint8_t)key.v0;
+      if (lane + 32 < k) p.keys_out[w * kmax + lane + 32] = (uint8_t)key.v1;
+      if (lane == 0) {
+        p.scores[w] = score;
+        if (p.last_accept) p.last_accept[w] = last;
+        if (p.tries_done) p.tries_done[w] = t;
+      }
+    }
+    cluster.sync();  // end of the worker
   }
 }
 
@@ -1280,6 +1410,29 @@ cudaError_t chain_launch(cudaStream_t s, const SctLaunch& p, const SumPlan& plan
   return cudaGetLastError();
 }
 
+template <int SLOTS, int ORDER>
+cudaError_t pair_launch(cudaStream_t s, const SctLaunch& p, const SumPlan& plan, int sm_count,
+                        bool* launched) {
+  *launched = false;
+  auto kern = sct_climb_pair_kernel<SLOTS, ORDER>;
+  const size_t bytes = pair_smem_bytes(p.n);
+  if (bytes > kMaxSmemPerBlock || 2 * p.n_workers > sm_count) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * p.n_workers));
+  cfg.blockDim = dim3(kPairWarps * 32);
+  cfg.dynamicSmemBytes = bytes;
+  cfg.stream = s;
+  int clusters = 0;
+  e = cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg);
+  if (e != cudaSuccess) return e;
+  if (clusters < p.n_workers) return cudaSuccess;  // not all workers at once
+  kern<<<cfg.gridDim, cfg.blockDim, bytes, s>>>(p, plan);
+  *launched = true;
+  return cudaGetLastError();
+}
+
 // Chain-parsed latency mode: the deepest speculation (32, 16, 8 or 4 warps per worker) whose
 // CTAs all fit at once.  *launched = false: none fits.
 template <int SLOTS, int ORDER>
@@ -1355,6 +1508,13 @@ static cudaError_t climb_order(cudaStream_t s, const SctLaunch& p, const SumPlan
     // the chain-parsed kernel's descriptors hold up to kSctLaneMaxHops events per proposal
     if (!(p.flags & CCG_FLAG_SCT_SPEC_REPLAY) && p.op1_hop <= kSctLaneMaxHops &&
         p.op2_hop <= kSctLaneMaxHops) {
+      switch (slots_for(plan)) {  // two SMs per worker when the GPU has them
+        case 1: e = pair_launch<1, ORDER>(s, p, plan, sm_count, &launched); break;
+        case 2: e = pair_launch<2, ORDER>(s, p, plan, sm_count, &launched); break;
+        case 4: e = pair_launch<4, ORDER>(s, p, plan, sm_count, &launched); break;
+        default: e = pair_launch<8, ORDER>(s, p, plan, sm_count, &launched); break;
+      }
+      if (e != cudaSuccess || launched) return e;
       switch (slots_for(plan)) {
         case 1: e = climb_chain_slots<1, ORDER>(s, p, plan, sm_count, &launched); break;
         case 2: e = climb_chain_slots<2, ORDER>(s, p, plan, sm_count, &launched); break;

@@ -248,17 +248,18 @@ def test_mas_results_independent_of_device_split():
     assert np.array_equal(one.group_best, two.group_best)
 
 
-@pytest.mark.parametrize("order,kmax", [(2, 40), (3, 40), (2, 32), (3, 17)])
-def test_sct_speculative_kernel_matches_warp_kernel(order, kmax):
-    """Few workers run on the speculative CTA-per-worker kernels (ccg_sct.cu
-    sct_climb_chain_kernel, and sct_climb_spec_kernel with speculate="replay"): every output
-    equals the one-warp-per-worker kernel's, for ragged key lengths and budgets that are not
-    multiples of the speculation depth."""
+@pytest.mark.parametrize("order,kmax,m", [(2, 40, 40), (3, 40, 40), (2, 32, 40), (3, 17, 40),
+                                           (2, 40, 100), (3, 17, 100)])
+def test_sct_speculative_kernel_matches_warp_kernel(order, kmax, m):
+    """Few workers run on the speculative latency kernels (ccg_sct.cu: up to 74 workers on the
+    two-SM sct_climb_pair_kernel, up to one per SM on sct_climb_chain_kernel, and
+    sct_climb_spec_kernel with speculate="replay"): every output equals the
+    one-warp-per-worker kernel's, for ragged key lengths and budgets that are not multiples
+    of the speculation depth."""
     rng = np.random.default_rng(90 + order)
     n_len = 333
     cs = [rng.integers(0, 26, n_len) for _ in range(3)]
     logs = -rng.random(26**order) * 20 - 1
-    m = 40
     cof = rng.integers(0, 3, m).astype(np.int32)
     klens = rng.integers(2, kmax + 1, m).astype(np.int32)
     klens[0] = kmax  # the batch maximum picks the warp kernel's narrow (<= 32) or wide variant
