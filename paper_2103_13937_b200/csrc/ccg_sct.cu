@@ -27,6 +27,7 @@
 //  * Tables: the 676 float64 log2 probabilities and each warp's ciphertext are staged in
 //    shared memory; colstart is a per-warp 64-entry u16 array (conflict-free).
 #include <cooperative_groups.h>
+#include <cstdio>
 
 #include "ccg_internal.h"
 #include "ccg_rng.cuh"
@@ -667,6 +668,9 @@ struct ChainSmem {
   uint16_t queue[kChainDraws];         // offsets whose proposal outran the first pass's budget
   int ticket, n_queued;                // next item to parse; queue length (chain_parse_lockstep)
   uint32_t ptab[20];                   // parse automaton table (chain_parse_table)
+#ifdef CCG_CHAIN_PROFILE
+  long long prof[5];                   // cycles per parse phase (CCG_CHAIN_PROFILE builds)
+#endif
 };
 
 // int(u*bound) of stream draw `pos` from its full 53-bit mantissa (the 32-bit test failed)
@@ -787,75 +791,96 @@ __device__ __forceinline__ void chain_parse_table(uint32_t* t, int k, int h1, in
 // its slowest lane is done.  So the first pass gives each proposal kChainBudget draws and
 // queues the offsets that need more; the second pass (PASS2) parses the queued offsets in
 // full, from their start.
-template <bool PASS2>
-__device__ __forceinline__ void chain_parse_lockstep(ChainSmem& C, uint64_t base, uint64_t k0,
-                                                     uint64_t k1, int k, int p1, int p2) {
-  const int lane = threadIdx.x & 31;
-  const int lim = PASS2 ? C.n_queued : kChainDraws;
-  int j = threadIdx.x;
-  auto offset_of = [&](int item) { return PASS2 ? (int)C.queue[item] : item; };
-  int o = j < lim ? offset_of(j) : 0;  // the offset being parsed
-  int cur = o;
-  int s = 0, hops = 1, plen = 1, pm = 2, pa = 0, nev = 0;
+// One automaton step of the proposal at offset o (state s, hops, plen, pm, pa, events): reads
+// draw cur; returns true when the proposal is complete or ran past the chunk (ovf).
+struct ChainStep {
+  int s = 0, hops = 1, plen = 1, pm = 2, pa = 0, nev = 0, op = 0;
   uint32_t e0 = 0u, e1 = 0u, e2 = 0u;
-  for (;;) {
-    const bool active = j < lim;
-    if (!__any_sync(kFull, active)) break;
-    const bool ovf = cur >= kChainDraws;
+  __device__ __forceinline__ void reset() {
+    s = 0;
+    nev = 0;
+  }
+  __device__ __forceinline__ bool step(const ChainSmem& C, int& cur, bool& ovf, uint64_t base,
+                                       uint64_t k0, uint64_t k1, int k, int p1, int p2) {
+    ovf = cur >= kChainDraws;
+    if (ovf) return true;
     const uint32_t te = C.ptab[s];
     const uint32_t bt = te & 0xffffu;
     const uint32_t bound = bt == 0xffffu ? (uint32_t)pm : bt;
-    const uint64_t A = (uint64_t)C.hi[active && !ovf ? cur : 0] * bound;
+    const uint64_t A = (uint64_t)C.hi[cur] * bound;
     int v = (int)(A >> 32);
-    const bool slow = active && !ovf && (uint32_t)A >= 0u - bound;
-    if (__any_sync(kFull, slow)) {
-      if (slow) v = chain_exact_below(k0, k1, base + (uint64_t)cur, bound);
-      __syncwarp();
-    }
+    if ((uint32_t)A >= 0u - bound) v = chain_exact_below(k0, k1, base + (uint64_t)cur, bound);
+    ++cur;
     const int ph = s >> 2;
     const bool same = v == pa;
     const bool pb = ph == 4 && !same;
     const bool rej = pb && s == 18 && abs(pa - v) < plen;
     const bool pair_done = pb && !rej;
-    {
-      const uint32_t lo = (uint32_t)min(pa, v), hi = (uint32_t)max(pa, v);
-      const uint32_t x = s == 18 ? lo | (hi << 8) | ((uint32_t)plen << 16)
-                                 : (uint32_t)pa | ((uint32_t)v << 8) | (s == 19 ? (uint32_t)plen << 16 : 0u);
-      const bool put = active && pair_done;
-      e0 = put && nev == 0 ? x : e0;
-      e1 = put && nev == 1 ? x : e1;
-      e2 = put && nev == 2 ? x : e2;
-      nev += put ? 1 : 0;
-    }
+    const uint32_t lo = (uint32_t)min(pa, v), hi = (uint32_t)max(pa, v);
+    const uint32_t x = s == 18 ? lo | (hi << 8) | ((uint32_t)plen << 16)
+                               : (uint32_t)pa | ((uint32_t)v << 8) | (s == 19 ? (uint32_t)plen << 16 : 0u);
+    e0 = pair_done && nev == 0 ? x : e0;
+    e1 = pair_done && nev == 1 ? x : e1;
+    e2 = pair_done && nev == 2 ? x : e2;
+    nev += pair_done ? 1 : 0;
     const int nop = v < p1 ? 1 : v < p2 ? 2 : 3;
     int ns = (int)(te >> 16);
     ns = s == 0 ? (nop == 3 ? 11 : 4 + nop) : ns;
     ns = ph == 4 && same ? s : ns;
     ns = rej ? 14 : ns;
-    const int op = s & 3;
-    if (active) {  // (if-converted: plain register selects)
-      hops = s == 0 ? 1 : ph == 1 ? 1 + v : hops - (pair_done ? 1 : 0);
-      plen = ph == 2 ? 1 + v : plen;
-      pm = ph == 2 ? k - v : pm;  // k - len + 1 positions
-      pa = ph == 3 ? v : pa;
-      s = ns;
-      ++cur;
-    }
-    const bool done = active && (ovf || (pair_done && hops == 0));
-    const bool defer = !PASS2 && active && !done && cur - o >= kChainBudget;  // to the second pass
-    if (done) {
-      C.jump[0][o] = ovf ? kChainOvf : (uint16_t)cur;
-      if (!ovf) C.desc[o] = make_uint4((uint32_t)op | ((uint32_t)nev << 4), e0, e1, e2);
-    }
-    if (!PASS2) {  // warp-aggregated push of the deferred offsets
-      const unsigned dm = __ballot_sync(kFull, defer);
-      if (dm) {
-        const int leader = __ffs(dm) - 1;
-        int q0 = 0;
-        if (lane == leader) q0 = atomicAdd(&C.n_queued, __popc(dm));
-        q0 = __shfl_sync(kFull, q0, leader);
-        if (defer) C.queue[q0 + __popc(dm & ((1u << lane) - 1u))] = (uint16_t)o;
+    op = s & 3;
+    hops = s == 0 ? 1 : ph == 1 ? 1 + v : hops - (pair_done ? 1 : 0);
+    plen = ph == 2 ? 1 + v : plen;
+    pm = ph == 2 ? k - v : pm;  // k - len + 1 positions
+    pa = ph == 3 ? v : pa;
+    s = ns;
+    return pair_done && hops == 0;
+  }
+  __device__ __forceinline__ void record(ChainSmem& C, int o, int cur, bool ovf) const {
+    C.jump[0][o] = ovf ? kChainOvf : (uint16_t)cur;
+    if (!ovf) C.desc[o] = make_uint4((uint32_t)op | ((uint32_t)nev << 4), e0, e1, e2);
+  }
+};
+
+template <bool PASS2>
+__device__ __forceinline__ void chain_parse_lockstep(ChainSmem& C, uint64_t base, uint64_t k0,
+                                                     uint64_t k1, int k, int p1, int p2) {
+  if (PASS2) {
+    // the few deferred offsets, one (or a few) per thread, each parsed to its end with no
+    // warp-collective step: a lone long proposal runs at one shared load per draw
+    const int nt = blockDim.x;
+    for (int j = threadIdx.x; j < C.n_queued; j += nt) {
+      const int o = C.queue[j];
+      int cur = o;
+      bool ovf = false;
+      ChainStep ps;
+      while (!ps.step(C, cur, ovf, base, k0, k1, k, p1, p2)) {
       }
+      ps.record(C, o, cur, ovf);
+    }
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int lim = kChainDraws;
+  int j = threadIdx.x;
+  int o = j;  // the offset being parsed
+  int cur = o;
+  ChainStep ps;
+  for (;;) {
+    const bool active = j < lim;
+    if (!__any_sync(kFull, active)) break;
+    bool done = false, ovf = false;
+    if (active) done = ps.step(C, cur, ovf, base, k0, k1, k, p1, p2);
+    const bool defer = active && !done && cur - o >= kChainBudget;  // to the second pass
+    if (done) ps.record(C, o, cur, ovf);
+    // warp-aggregated push of the deferred offsets
+    const unsigned dm = __ballot_sync(kFull, defer);
+    if (dm) {
+      const int leader = __ffs(dm) - 1;
+      int q0 = 0;
+      if (lane == leader) q0 = atomicAdd(&C.n_queued, __popc(dm));
+      q0 = __shfl_sync(kFull, q0, leader);
+      if (defer) C.queue[q0 + __popc(dm & ((1u << lane) - 1u))] = (uint16_t)o;
     }
     const bool fin = done || defer;
     const unsigned fm = __ballot_sync(kFull, fin);
@@ -866,10 +891,9 @@ __device__ __forceinline__ void chain_parse_lockstep(ChainSmem& C, uint64_t base
       t0 = __shfl_sync(kFull, t0, leader);
       if (fin) {
         j = t0 + __popc(fm & ((1u << lane) - 1u));
-        o = j < lim ? offset_of(j) : 0;
+        o = j;
         cur = o;
-        s = 0;
-        nev = 0;
+        ps.reset();
       }
     }
   }
@@ -949,6 +973,12 @@ __device__ __forceinline__ void chain_parse_chunk(ChainSmem& C, uint64_t entry, 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t base = entry & ~3ULL;
   const int e = (int)(entry - base);
+#ifdef CCG_CHAIN_PROFILE
+  long long c0 = clock64();
+#define CHAIN_T(i) do { __syncthreads(); const long long c1 = clock64(); if (tid == 0) C.prof[i] += c1 - c0; c0 = c1; } while (0)
+#else
+#define CHAIN_T(i) __syncthreads()
+#endif
   if (tid == 0) {
     C.ticket = nt;
     C.n_queued = 0;
@@ -960,13 +990,13 @@ __device__ __forceinline__ void chain_parse_chunk(ChainSmem& C, uint64_t entry, 
     *reinterpret_cast<uint4*>(C.hi + 4 * j) =
         make_uint4((uint32_t)(v0 >> 32), (uint32_t)(v1 >> 32), (uint32_t)(v2 >> 32), (uint32_t)(v3 >> 32));
   }
-  __syncthreads();
+  CHAIN_T(0);
   chain_parse_lockstep<false>(C, base, k0, k1, k, p1, p2);
-  __syncthreads();
+  CHAIN_T(1);
   if (tid == 0) C.ticket = nt;
   __syncthreads();
   chain_parse_lockstep<true>(C, base, k0, k1, k, p1, p2);
-  __syncthreads();
+  CHAIN_T(2);
   // jump tables: 2^b proposals ahead (entries >= kChainDraws are terminal)
 #pragma unroll 1
   for (int b = 1; b < kChainJumps; ++b) {
@@ -976,6 +1006,7 @@ __device__ __forceinline__ void chain_parse_chunk(ChainSmem& C, uint64_t entry, 
     }
     __syncthreads();
   }
+  CHAIN_T(3);
   if (warp == 0) {
     chain_follow(C, e, need, lane);
     if (lane == 0 && C.n == 0) {  // a proposal longer than the chunk: parse it from the stream
@@ -984,7 +1015,7 @@ __device__ __forceinline__ void chain_parse_chunk(ChainSmem& C, uint64_t entry, 
       C.n = 1;
     }
   }
-  __syncthreads();
+  CHAIN_T(4);
 }
 
 template <int SLOTS, int ORDER, int P>
@@ -1134,6 +1165,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairWarps * 32, 1)
         b ^= 1;
       }
       if (tid == 0 && p.draws_used) p.draws_used[w] = entry;
+#ifdef CCG_CHAIN_PROFILE
+      if (tid == 0 && w < 2) {
+        printf("parse profile w=%lld: gen %lld pass1 %lld pass2 %lld jumps %lld follow %lld\n", (long long)w,
+               C.prof[0], C.prof[1], C.prof[2], C.prof[3], C.prof[4]);
+        for (int i = 0; i < 5; ++i) C.prof[i] = 0;
+      }
+#endif
       cluster.sync();  // end of the worker
     }
     return;
