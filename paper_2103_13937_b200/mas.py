@@ -118,26 +118,31 @@ def solve_stochastic(cipher: MappedText, table: BigramTable, cfg: MasSolverConfi
     return _restart_batch(text, table, cfg, [restart])[0]
 
 
-def _batched_restarts(make_batch, restarts: int, workers: int, stop):
+def _batched_restarts(make_batch, restarts: int, workers: int, stop, grow: bool = True):
     """Evaluate restarts in launches of several restarts and fold them in order
     (search.py:61-86).  Results equal the sequential reference: restarts are independent of
     each other and of `stop`, which is applied restart by restart in order.
 
-    With a `stop` callback the launches grow 1, 2, 4, ... restarts: a solve usually stops
-    after its first restart, so the first launch is a single restart, and at most one launch
-    ever computes restarts past the stopping one (they are discarded, never reported).
-    Without `stop` every launch is about one full wave.  RestartSummary.elapsed is the wall
-    time of the launch that computed the restart (its restarts ran concurrently for that
-    long), the analogue of the reference's per-restart timing (search.py:75-78)."""
+    With a `stop` callback the first launch is a single restart (a solve usually stops after
+    it) and, with `grow`, the launches grow 1, 2, 4, ... restarts; at most one launch ever
+    computes restarts past the stopping one (they are discarded, never reported).  The SCT
+    solvers pass grow=False: their latency kernels give a restart of 64 workers a pair of SMs
+    each, so two restarts in one launch take about as long as two launches of one, and four
+    fall back to slower kernels.  Without `stop` every launch is about one full wave.
+    RestartSummary.elapsed is the wall time of the launch that computed the restart (its
+    restarts ran concurrently for that long), the analogue of the reference's per-restart
+    timing (search.py:75-78)."""
     target = 8192 * max(1, len(engine.devices()))  # workers per chunk: ~one full wave
     chunk = max(1, min(restarts, target // max(1, workers)))
+    first = 1 if grow else max(1, min(chunk, 64 // max(1, workers)))
 
     def gen():
         r = 0
-        size = 1 if stop is not None else chunk
+        size = first if stop is not None else chunk
         while r < restarts:
             rs = list(range(r, min(restarts, r + size)))
-            size = min(chunk, 2 * size)
+            if grow:
+                size = min(chunk, 2 * size)
             t0 = time.perf_counter()
             results = make_batch(rs)
             dt = time.perf_counter() - t0

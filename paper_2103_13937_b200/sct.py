@@ -155,7 +155,7 @@ def solve_sct(cipher: MappedText, logs: LogBigramTable, cfg: SctSolverConfig, jo
     if text.size < cfg.key_length:
         raise ValueError("ciphertext shorter than the key")
     return _batched_restarts(lambda rs: _restart_batch(text, logs, cfg, rs), cfg.restarts,
-                             cfg.workers, stop)
+                             cfg.workers, stop, grow=False)
 
 
 def solve_sct_batch(ciphers, logs, cfg: SctSolverConfig, restart: int = 0, seeds=None,
@@ -228,4 +228,4 @@ def solve_sct_fast(cipher: MappedText, logs: LogBigramTable, cfg: SctSolverConfi
                                    best_key=key))
         return out
 
-    return _batched_restarts(batch, cfg.restarts, W, stop)
+    return _batched_restarts(batch, cfg.restarts, W, stop, grow=False)

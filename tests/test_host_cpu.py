@@ -400,3 +400,12 @@ def test_restarts_with_stop_compute_nothing_past_the_stop():
     calls.clear()
     best, runs = _batched_restarts(make_batch, 50, 64, stop=None)
     assert len(runs) == 50 and len(calls) < 50 and best.restart_index == 3
+    # the SCT solvers' constant launches (grow=False): one 64-worker restart per launch,
+    # 64 workers' worth of smaller restarts
+    calls.clear()
+    best, runs = _batched_restarts(make_batch, 50, 64, stop=lambda res: res.best_score == 10,
+                                   grow=False)
+    assert calls == [[0], [1], [2], [3]] and len(runs) == 4 and best.restart_index == 3
+    calls.clear()
+    _batched_restarts(make_batch, 50, 16, stop=lambda res: res.best_score == 10, grow=False)
+    assert calls == [[0, 1, 2, 3]]
