@@ -78,9 +78,10 @@ enum {
 #define CCG_FLAG_KERNEL_TFORM 0x20u
 #define CCG_FLAG_KERNEL_PACKED 0x30u
 #define CCG_FLAG_KERNEL_DTABLE 0x40u /* D-form with the full delta table kept in smem */
-/* SCT: with at most one worker per SM the climb runs each worker on a CTA of warps that
- * evaluate consecutive proposals speculatively (identical results, lower latency); this
- * flag forces the one-warp-per-worker kernel instead. */
+/* SCT: with few workers (up to 16 per SM) the climb runs each worker on a CTA of warps that
+ * evaluate consecutive proposals speculatively -- up to 74 workers on two SMs each, one
+ * parsing the worker's proposal chain ahead (identical results, lower latency); this flag
+ * forces the one-warp-per-worker kernel instead. */
 #define CCG_FLAG_SCT_NO_SPEC 0x100u
 /* SCT kernel selection (identical results; for tests and benchmarks).  Automatic: few workers
  * of one text length -> the speculative CTA-per-worker kernel; mixed text lengths or large

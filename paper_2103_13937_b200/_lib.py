@@ -20,7 +20,7 @@ ALPHA = 26
 
 CCG_OK, CCG_ERR_INVALID, CCG_ERR_CUDA, CCG_ERR_NO_DEVICE, CCG_ERR_UNSUPPORTED = 0, -1, -2, -3, -4
 FLAG_EARLY_EXIT = 1
-FLAG_SCT_NO_SPEC = 0x100  # SCT: never use the speculative CTA-per-worker kernel
+FLAG_SCT_NO_SPEC = 0x100  # SCT: never use the speculative latency kernels
 FLAG_SCT_KERNEL_WARP = 0x200  # SCT: one warp per worker instead of one lane per worker
 FLAG_SCT_TABLE_L2 = 0x400  # SCT lane kernel: trigram table read through L2, not shared memory
 FLAG_SCT_KERNEL_LANE = 0x800  # SCT: one worker per lane
