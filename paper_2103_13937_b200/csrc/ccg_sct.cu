@@ -1141,6 +1141,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairWarps * 32, 1)
   const int64_t climbings = p.climbings;
   const int64_t n_pairs = gridDim.x / 2;
   PairBuf* buf_view = reinterpret_cast<PairBuf*>(smem + pair_buf_offset(p.n));
+  cluster.sync();  // both CTAs are running before either touches the other's shared memory
 
   if (rank == 1) {
     // ---- the parsing CTA ----

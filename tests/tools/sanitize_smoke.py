@@ -38,11 +38,19 @@ logs = -rng.random(676) * 20 - 1
 sc_c = [rng.integers(0, 26, 200) for _ in range(2)]
 sc_cof = np.array([0, 1, 1, 0], np.int32)
 sk = philox_keys([4] * 4, list(range(4)))
-for spec in (True, False):
+# latency kernels: two SMs per worker (4 workers), the replaying CTA kernel, one warp
+for spec in (True, "replay", False):
     r = engine.sct_climb(sc_c, sc_cof, sk, logs, 9, 60, speculate=spec)
     for i in range(4):
         _, s, _ = O.sct_worker(sc_c[sc_cof[i]], logs, 9, 60, 4, i)
         assert float(r.scores[i]) == s, (spec, i)
+# the one-CTA chain kernel (more workers than SM pairs), a climb spanning parse chunks
+ch_cof = (np.arange(80) % 2).astype(np.int32)
+ch_k = philox_keys([5] * 80, list(range(80)))
+r = engine.sct_climb(sc_c, ch_cof, ch_k, logs, 9, 700)
+for i in (0, 1, 79):
+    _, s, _ = O.sct_worker(sc_c[ch_cof[i]], logs, 9, 700, 5, i)
+    assert float(r.scores[i]) == s, ("chain", i)
 # per-lane SCT kernels: parity (orders 2-4, ragged lengths, a chunk spanning ciphertexts) and
 # the fast mode
 lane_c = [rng.integers(0, 26, int(L)) for L in (200, 57, 333)]
