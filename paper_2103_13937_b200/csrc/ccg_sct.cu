@@ -973,7 +973,7 @@ __device__ __forceinline__ void chain_parse_chunk(ChainSmem& C, uint64_t entry, 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t base = entry & ~3ULL;
   const int e = (int)(entry - base);
-#ifdef CCG_CHAIN_PROFILE
+#ifdef CCG_CHAIN_PROFILE  // per-phase cycle counts (make NVFLAGS="... -DCCG_CHAIN_PROFILE")
   long long c0 = clock64();
 #define CHAIN_T(i) do { __syncthreads(); const long long c1 = clock64(); if (tid == 0) C.prof[i] += c1 - c0; c0 = c1; } while (0)
 #else
@@ -1147,6 +1147,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairWarps * 32, 1)
     // ---- the parsing CTA ----
     ChainSmem& C = *reinterpret_cast<ChainSmem*>(smem);
     PairBuf* remote = cluster.map_shared_rank(buf_view, 0);
+#ifdef CCG_CHAIN_PROFILE
+    if (tid < 5) C.prof[tid] = 0;
+#endif
     for (int64_t w = blockIdx.x / 2; w < p.n_workers; w += n_pairs) {
       const int k = p.key_lengths ? p.key_lengths[w] : kmax;
       const uint64_t k0 = p.keys[2 * w], k1 = p.keys[2 * w + 1];
