@@ -654,6 +654,10 @@ constexpr int kChainMaxProps = kChainDraws / 4;  // every proposal reads at leas
 constexpr uint16_t kChainOvf = 0xffffu;          // the proposal runs past the chunk
 constexpr int kChainJumps = 5;
 constexpr int kChainBudget = 24;                 // draws per proposal in the first parse pass
+#ifndef CCG_CHAIN_STEPS
+#define CCG_CHAIN_STEPS 4
+#endif
+constexpr int kChainSteps = CCG_CHAIN_STEPS;     // first-pass automaton steps per bookkeeping round
 constexpr size_t kMaxSmemPerBlock = 227 * 1024;  // sm_100 opt-in dynamic shared memory per block                   // jump tables of 1, 2, 4, 8, 16 proposals
 
 struct ChainSmem {
@@ -870,7 +874,13 @@ __device__ __forceinline__ void chain_parse_lockstep(ChainSmem& C, uint64_t base
     const bool active = j < lim;
     if (!__any_sync(kFull, active)) break;
     bool done = false, ovf = false;
-    if (active) done = ps.step(C, cur, ovf, base, k0, k1, k, p1, p2);
+    // kChainSteps automaton steps per round of warp-collective bookkeeping
+    if (active) {
+      done = ps.step(C, cur, ovf, base, k0, k1, k, p1, p2);
+#pragma unroll
+      for (int r = 1; r < kChainSteps; ++r)
+        if (!done && cur - o < kChainBudget) done = ps.step(C, cur, ovf, base, k0, k1, k, p1, p2);
+    }
     const bool defer = active && !done && cur - o >= kChainBudget;  // to the second pass
     if (done) ps.record(C, o, cur, ovf);
     // warp-aggregated push of the deferred offsets
