@@ -95,6 +95,9 @@ enum {
 /* SCT latency mode: the speculative kernel whose warps replay their predecessors' draws
  * every round, instead of the chain-parsed kernel (identical results; for tests). */
 #define CCG_FLAG_SCT_SPEC_REPLAY 0x1000u
+/* SCT fast mode: walk every changed window's column instead of reading the regular-grid
+ * window-sum tables (identical results; for tests). */
+#define CCG_FLAG_SCT_NO_WINDOW_TABLES 0x2000u
 
 typedef struct ccg_ctx ccg_ctx;
 

@@ -25,6 +25,7 @@ FLAG_SCT_KERNEL_WARP = 0x200  # SCT: one warp per worker instead of one lane per
 FLAG_SCT_TABLE_L2 = 0x400  # SCT lane kernel: trigram table read through L2, not shared memory
 FLAG_SCT_KERNEL_LANE = 0x800  # SCT: one worker per lane
 FLAG_SCT_SPEC_REPLAY = 0x1000  # SCT latency mode: per-round draw replay instead of the parsed chain
+FLAG_SCT_NO_WINDOW_TABLES = 0x2000  # SCT fast mode: no regular-grid window-sum tables
 SCT_KERNEL_FLAGS = {"auto": 0, "lane": FLAG_SCT_KERNEL_LANE, "warp": FLAG_SCT_KERNEL_WARP}
 KERNEL_FLAGS = {"auto": 0, "dform": 0x10, "tform": 0x20, "packed": 0x30, "dtable": 0x40}
 

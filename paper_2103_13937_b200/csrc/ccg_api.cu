@@ -1361,6 +1361,52 @@ int ccg_sct_climb(ccg_ctx* ctx, const ccg_sct_climb_args* a) {
   return finish(ctx, cudaSuccess, "sct_climb");
 }
 
+// Fast mode, regular grids (ciphertext length a multiple of the worker's key length, k >= the
+// n-gram order): tabulate each (ciphertext, k)'s window sums by column ranks once
+// (sct_ftab_kernel), so the climb reads one entry per changed window instead of walking the
+// window's column.  The integer sums are the same; other workers keep the column walk.
+extern "C++" static int attach_window_tables(ccg_ctx* ctx, const ccg_sct_fast_args* a,
+                                             SctLaneLaunch& L) {
+  if (a->order > 3 || (a->flags & CCG_FLAG_SCT_NO_WINDOW_TABLES)) return CCG_OK;
+  const int64_t nw = a->n_workers;
+  std::map<std::pair<int32_t, int32_t>, int64_t> where;
+  std::vector<SctFPair> pairs;
+  std::vector<int64_t> foff((size_t)nw, -1);
+  int64_t total = 0;
+  for (int64_t i = 0; i < nw; ++i) {
+    const int32_t c = a->cipher_of[i];
+    const int32_t kw = a->key_lengths ? a->key_lengths[i] : a->key_length;
+    const int64_t n = a->offsets[c + 1] - a->offsets[c];
+    // (L = n / k >= 2: the kernel's rank = colstart * ceil(2^32 / L) >> 32 needs L > 1)
+    if (kw < a->order || n % kw != 0 || n / kw < 2 || n > 40960) continue;
+    int64_t entries = a->order;
+    for (int q = 0; q < a->order; ++q) entries *= kw;
+    if (entries > kSctFTabMaxEntries) continue;
+    auto it = where.find({c, kw});
+    if (it == where.end()) {
+      if (total + entries > (int64_t(1) << 27)) continue;  // 512 MB of tables at most
+      it = where.emplace(std::make_pair(c, kw), total).first;
+      pairs.push_back(SctFPair{c, kw, total});
+      total += entries;
+    }
+    foff[(size_t)i] = it->second;
+  }
+  if (pairs.empty()) return CCG_OK;
+  int rc;
+  void *pp, *pf, *po;
+  if ((rc = upload(ctx, 20, pairs.data(), pairs.size() * sizeof(SctFPair), &pp))) return rc;
+  if ((rc = ctx->buf(18, (size_t)total * 4, &pf))) return rc;
+  if ((rc = upload(ctx, 19, foff.data(), foff.size() * 8, &po))) return rc;
+  ctx->launches++;
+  cudaError_t e = launch_sct_ftab(ctx->stream, L.ciphers, L.offsets, (const SctFPair*)pp,
+                                  (int64_t)pairs.size(), L.qtable, a->order, L.max_len,
+                                  (int32_t*)pf);
+  if (e != cudaSuccess) return cuda_fail(e, "sct_ftab kernel");
+  L.ftab = (const int32_t*)pf;
+  L.f_off = (const int64_t*)po;
+  return CCG_OK;
+}
+
 int ccg_sct_fast_climb(ccg_ctx* ctx, const ccg_sct_fast_args* a) {
   int rc = enter(ctx);
   if (rc) return rc;
@@ -1437,6 +1483,7 @@ int ccg_sct_fast_climb(ccg_ctx* ctx, const ccg_sct_fast_args* a) {
   L.order = a->order;
   L.flags = a->flags;
   if ((rc = attach_compressed(ctx, a->table, a->order, L))) return rc;
+  if ((rc = attach_window_tables(ctx, a, L))) return rc;
   if ((rc = sct_launch_lane(ctx, L))) return rc;
   if (d_best) {
     ctx->launches++;

@@ -149,7 +149,20 @@ struct SctLaneLaunch {
   const uint8_t* cidx;    // order 3, optional: per-entry index into <= 256 distinct values
   const void* cvals;      // the distinct values (double for mode 0, int32 for mode 1)
   int32_t n_cvals;
+  // mode 1, optional: window-sum tables of regular grids (text length a multiple of k):
+  // worker i's table at ftab + f_off[i] (f_off[i] < 0: none), see sct_ftab_kernel
+  const int32_t* ftab;
+  const int64_t* f_off;
 };
+// One (ciphertext, key length) whose fast-mode window sums are tabulated (regular grid).
+struct SctFPair {
+  int32_t cipher, k;
+  int64_t off;
+};
+constexpr int64_t kSctFTabMaxEntries = int64_t(1) << 17;  // order * k^order per table
+cudaError_t launch_sct_ftab(cudaStream_t s, const uint8_t* ciphers, const int64_t* offsets,
+                            const SctFPair* pairs, int64_t n_pairs, const int32_t* qtable,
+                            int order, int max_len, int32_t* ftab);
 
 #ifdef __CUDACC__
 // Worker scheduling for the persistent climb kernels: a warp's first worker is static

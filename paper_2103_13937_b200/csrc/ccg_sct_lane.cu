@@ -464,7 +464,32 @@ __global__ void __launch_bounds__(kSctLaneWarps * 32, MODE == 1 ? 3 : CCG_LANE_M
       pt.wk.cs = csp;
       pt.wk.k = k;
       pt.tab = tab;
-      auto wsum = [&](int ww) {
+      // regular grid with a tabulated window sum (fast mode): segment c starts at rank(c) * L,
+      // so a window's sum is a function of its columns' ranks (sct_ftab_kernel)
+      const int32_t* F = nullptr;
+      uint32_t rank_mul = 0;
+      if (MODE == 1 && p.ftab && mine) {
+        const int64_t fo = p.f_off[w];
+        if (fo >= 0) {
+          F = p.ftab + fo;
+          rank_mul = (uint32_t)((0x100000000ULL + (uint64_t)base - 1) / (uint64_t)base);  // ceil(2^32 / L)
+        }
+      }
+      int kpow = 1;
+#pragma unroll
+      for (int i = 0; i < ORDER; ++i) kpow *= k;
+      auto wsum = [&](int ww) -> int32_t {
+        if (MODE == 1 && F) {
+          const int kind = ww > k - ORDER ? ww - (k - ORDER) : 0;
+          int e = 0;
+#pragma unroll
+          for (int i = 0; i < ORDER; ++i) {
+            int cc = ww + i;
+            if (cc >= k) cc -= k;
+            e = e * k + (int)__umulhi((uint32_t)csp[32 * cc], rank_mul);
+          }
+          return __ldg(F + (int64_t)kind * kpow + e);
+        }
         return window_sum<ORDER>(ww, k, rows_of(ww), txt, csp, tab);
       };
       int64_t lookups = 0;
@@ -645,7 +670,7 @@ __global__ void __launch_bounds__(kSctLaneWarps * 32, MODE == 1 ? 3 : CCG_LANE_M
           while (m) {
             const int ww = __ffsll((long long)m) - 1;
             m &= m - 1;
-            lookups += rows_of(ww);
+            lookups += F ? 1 : rows_of(ww);
             delta += wsum(ww) - gp[32 * ww];
           }
           accept = delta > 0;  // sct.py:168, on the quantised fitness
@@ -687,6 +712,45 @@ __global__ void __launch_bounds__(kSctLaneWarps * 32, MODE == 1 ? 3 : CCG_LANE_M
       }
       __syncwarp();
     }
+  }
+}
+
+// Fast mode on a regular grid (n = L * k): segment j of the ciphertext is cipher[jL, jL + L)
+// and plaintext column c reads segment rank(c), so the integer sum of the windows starting in
+// column w is F[kind][rank(w)][rank(w+1)]...[rank(w+ORDER-1)] with kind = the number of the
+// window's letters that wrap to the next row (w > k - ORDER) and L (kind 0) or L - 1 rows.
+// One CTA per (ciphertext, k): the text in shared memory, one table entry per thread.  A
+// candidate then costs one table read per changed window instead of a column walk.
+__global__ void __launch_bounds__(256) sct_ftab_kernel(const uint8_t* __restrict__ ciphers,
+                                                        const int64_t* __restrict__ offsets,
+                                                        const SctFPair* __restrict__ pairs,
+                                                        const int32_t* __restrict__ qt, int order,
+                                                        int32_t* __restrict__ F) {
+  extern __shared__ uint8_t ftxt[];
+  const SctFPair P = pairs[blockIdx.x];
+  const int64_t off = offsets[P.cipher];
+  const int n = (int)(offsets[P.cipher + 1] - off), k = P.k, L = n / k;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) ftxt[i] = ciphers[off + i];
+  __syncthreads();
+  int kpow = 1;
+  for (int i = 0; i < order; ++i) kpow *= k;
+  for (int e = threadIdx.x; e < order * kpow; e += blockDim.x) {
+    const int kind = e / kpow;
+    int rem = e - kind * kpow;
+    int start[4];
+    for (int i = order - 1; i >= 0; --i) {
+      const int r = rem % k;
+      rem /= k;
+      start[i] = r * L + (i >= order - kind ? 1 : 0);  // wrapped letters read the next row
+    }
+    const int rows = kind == 0 ? L : L - 1;
+    int32_t acc = 0;
+    for (int r = 0; r < rows; ++r) {
+      int idx = 0;
+      for (int i = 0; i < order; ++i) idx = idx * kAlpha + ftxt[start[i] + r];
+      acc += __ldg(qt + idx);
+    }
+    F[P.off + e] = acc;
   }
 }
 
@@ -760,6 +824,15 @@ size_t sct_lane_smem_bytes(int mode, int kmax, int64_t max_len) {
 cudaError_t launch_sct_lane(cudaStream_t s, const SctLaneLaunch& p, int sm_count) {
   if (p.n_workers <= 0) return cudaSuccess;
   return p.mode == 0 ? lane_order<0>(s, p, sm_count) : lane_order<1>(s, p, sm_count);
+}
+
+cudaError_t launch_sct_ftab(cudaStream_t s, const uint8_t* ciphers, const int64_t* offsets,
+                            const SctFPair* pairs, int64_t n_pairs, const int32_t* qtable,
+                            int order, int max_len, int32_t* ftab) {
+  if (n_pairs <= 0) return cudaSuccess;
+  sct_ftab_kernel<<<(unsigned)n_pairs, 256, (size_t)max_len, s>>>(ciphers, offsets, pairs, qtable,
+                                                                    order, ftab);
+  return cudaGetLastError();
 }
 
 }  // namespace ccg

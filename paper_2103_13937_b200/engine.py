@@ -279,13 +279,16 @@ def sct_climb(ciphers, cipher_of, keys, logs, key_length, climbings, *, p1=33, p
 def sct_fast_climb(ciphers, cipher_of, keys, table, key_length, climbings, *, p1=33, p2=66,
                    op1_hop=3, op2_hop=3, skips=None, group_size=0, draws_used=False,
                    last_accept=False, tries_done=False, lookups=True, table_l2=False,
-                   devices_=None) -> ClimbResult:
+                   window_tables=True, devices_=None) -> ClimbResult:
     """The opt-in fast SCT mode (ccg_sct_fast_climb): sct_worker (sct.py:148-170) with the
     fitness replaced by the integer sum of a quantised log table (ngrams.quantize_sct_table:
     `table` is a QuantizedSctTable or its int32[26**order] entries plus `order` attribute),
     scored incrementally over the windows of the columns a candidate moves.  Same draws,
     operators and strict acceptance as the reference; scores come back as int64 quantised
-    fitness.  `lookups` reports the table lookups each worker's incremental rescoring made."""
+    fitness.  `lookups` reports the table lookups each worker's incremental rescoring made.
+    On regular grids (text length a multiple of k, orders 2-3) a changed window is one read of
+    a per-(ciphertext, k) table of window sums by column ranks; window_tables=False walks the
+    window's column instead (identical results)."""
     flat, off = _lib.ragged(ciphers)
     cof = np.ascontiguousarray(cipher_of, dtype=np.int32).reshape(-1)
     keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, 2)
@@ -333,7 +336,8 @@ def sct_fast_climb(ciphers, cipher_of, keys, table, key_length, climbings, *, p1
         a.tries_done = _lib.ptr(out.tries_done)
         a.group_size, a.group_best = int(group_size), _lib.ptr(out.group_best)
         a.key_lengths, a.lookups = _lib.ptr(kl), _lib.ptr(out.lookups)
-        a.flags = _lib.FLAG_SCT_TABLE_L2 if table_l2 else 0
+        a.flags = ((_lib.FLAG_SCT_TABLE_L2 if table_l2 else 0)
+                   | (0 if window_tables else _lib.FLAG_SCT_NO_WINDOW_TABLES))
         ctx = _lib.context(dev)
         with ctx.lock:
             before = ctx.launches()

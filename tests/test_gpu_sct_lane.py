@@ -163,6 +163,46 @@ def test_fast_mode_vs_its_oracle(order):
 
 
 @pytest.mark.parametrize("order", [2, 3])
+def test_fast_mode_window_tables_on_regular_grids(order):
+    """Regular grids (text length a multiple of k) read the changed windows from the
+    per-(ciphertext, k) window-sum tables (ccg_sct_lane.cu sct_ftab_kernel): identical to the
+    fast mode's oracle and to the column walk, with one table read per changed window."""
+    rng = np.random.default_rng(720 + order)
+    lt = cc.LogNgramTable(order, -rng.random(26**order) * 20 - 1, -24.0) if order > 2 else \
+        cc.LogBigramTable(-rng.random(676) * 20 - 1, -24.0)
+    q = cc.quantize_sct_table(lt, text_len=600)
+    ciphers = [rng.integers(0, 26, L) for L in (400, 120, 600, 45)]
+    pairs = [(0, k) for k in (order, 4, 5, 8, 10, 16, 20, 25, 40)] + \
+            [(1, k) for k in (order, 6, 12, 15, 24, 30)] + [(2, k) for k in (12, 25, 30)] + \
+            [(3, k) for k in (order, 5, 9, 15)] + [(0, 7), (1, 7)]  # (+ two irregular grids)
+    pairs = [(c, k) for c, k in pairs if k >= order]
+    cof = np.array([c for c, _ in pairs for _ in range(3)], np.int32)
+    klens = np.array([k for _, k in pairs for _ in range(3)], np.int32)
+    m = cof.size
+    streams = list(range(m))
+    keys = philox_keys([77], streams)
+    for climb in (0, 300):
+        res = engine.sct_fast_climb(ciphers, cof, keys, q, klens, climb, draws_used=True)
+        walk = engine.sct_fast_climb(ciphers, cof, keys, q, klens, climb, draws_used=True,
+                                     window_tables=False)
+        want_s, want_k = _fast_oracle(ciphers, cof, klens, 77, streams, q.table, order, climb)
+        assert res.scores.tolist() == want_s.tolist() == walk.scores.tolist(), climb
+        for i in range(m):
+            assert np.array_equal(res.keys[i, :klens[i]].astype(np.int64), want_k[i]), (climb, i)
+        assert np.array_equal(res.draws_used, walk.draws_used)
+        if climb:
+            # tabulated: regular grid and order * k**order <= 2**17 entries (kSctFTabMaxEntries)
+            regular = np.array([len(ciphers[c]) % k == 0 and order * int(k)**order <= 2**17
+                                for c, k in zip(cof, klens)])
+            assert (res.lookups[regular] <= walk.lookups[regular]).all()
+            assert res.lookups[regular].sum() * 5 < walk.lookups[regular].sum()
+            assert (res.lookups[~regular] == walk.lookups[~regular]).all()
+            bad = [(int(c), int(k), int(v)) for c, k, v, r in zip(cof, klens, res.lookups, regular)
+                   if r and v > k * climb]
+            assert not bad, bad
+
+
+@pytest.mark.parametrize("order", [2, 3])
 def test_fast_mode_reduces_to_reference_climb_on_a_dyadic_table(order):
     """With log-probabilities that are multiples of 2^-10 (>= -24), quantising at shift 10 is
     exact and every float64 partial sum is exact, so the fast mode's integer fitness is the
