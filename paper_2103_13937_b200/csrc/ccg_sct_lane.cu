@@ -529,68 +529,58 @@ __global__ void __launch_bounds__(kSctLaneWarps * 32, MODE == 1 ? 3 : CCG_LANE_M
       // position events, and a step consumes exactly one draw in every lane.  Rejection loops
       // (apply_block_swaps redraws whole pairs while |p - q| < len, sct.py:100-104) then cost
       // one step per draw in the lane that needs them instead of stalling the warp.
-      enum { S_OP, S_H1, S_A1, S_B1, S_H2, S_L2, S_A2, S_B2, S_L3, S_P3, S_D3 };
-      int st = S_OP, hops = 0, pa = 0, plen = 0, pm = 2, nev = 0, pop = 0;
+      // State stt = 4 * phase + op, as in ccg_sct.cu ChainStep: phase 0 = operator draw
+      // (select_operator), 1 = hop count, 2 = block length, 3 = first position of a pair, 4 =
+      // second position (redrawn while equal; block swaps redraw the whole pair while
+      // |p - q| < len); op 1 = element swaps, 2 = block swaps, 3 = block shift.  Written with
+      // selects: the lanes of a warp are in different states, and a switch would serialise
+      // them.  A proposal's events collect in registers and go to the queue when it completes.
+      int stt = 0, hops = 1, pa = 0, plen = 1, pm = 2, nev = 0;
+      uint32_t e0 = 0u, e1 = 0u, e2 = 0u;
       int q_head = 0, q_cnt = 0;
       int64_t parsed = 0, done_t = 0, last = -1;
       auto qword = [&](int slot, int word) -> uint32_t& { return qp[32 * (kQWords * slot + word)]; };
-      auto emit = [&](int x, int y, int l) {
-        qword((q_head + q_cnt) % kQSlots, 1 + nev) = (uint32_t)x | ((uint32_t)y << 8) | ((uint32_t)l << 16);
-        ++nev;
-      };
-      auto finish = [&]() {
-        qword((q_head + q_cnt) % kQSlots, 0) = (uint32_t)pop | ((uint32_t)nev << 4);
-        ++q_cnt;
-        ++parsed;
-        st = S_OP;
-      };
+      const uint32_t kh = (uint32_t)(k / 2), km1 = (uint32_t)(k - 1);
+      const uint32_t h1 = (uint32_t)p.op1_hop, h2 = (uint32_t)p.op2_hop;
       auto step = [&]() {
-        uint32_t bound;
-        switch (st) {
-          case S_OP: bound = 100u; break;
-          case S_H1: bound = (uint32_t)p.op1_hop; break;
-          case S_H2: bound = (uint32_t)p.op2_hop; break;
-          case S_A1: case S_B1: bound = (uint32_t)k; break;
-          case S_L2: bound = (uint32_t)(k / 2); break;
-          case S_L3: bound = (uint32_t)(k - 1); break;
-          default: bound = (uint32_t)pm; break;  // pairs / positions within k - len + 1
-        }
+        const int ph = stt >> 2, op = stt & 3;
+        uint32_t bound = op == 1 ? (uint32_t)k : (uint32_t)pm;  // pairs / positions within k - len + 1
+        bound = ph == 2 ? (op == 2 ? kh : km1) : bound;
+        bound = ph == 1 ? (op == 1 ? h1 : h2) : bound;
+        bound = ph == 0 ? 100u : bound;
         const int v = d.below_buffered(bound);
-        switch (st) {
-          case S_OP:  // sct.py:69-79 select_operator
-            nev = 0;
-            pop = v < p.p1 ? 1 : v < p.p2 ? 2 : 3;
-            st = pop == 1 ? S_H1 : pop == 2 ? S_H2 : S_L3;
-            break;
-          case S_H1: hops = 1 + v; st = S_A1; break;  // sct.py:82-89
-          case S_A1: pa = v; st = S_B1; break;
-          case S_B1:
-            if (v != pa) {
-              emit(pa, v, 0);
-              if (--hops == 0) finish(); else st = S_A1;
-            }
-            break;
-          case S_H2: hops = 1 + v; st = S_L2; break;  // sct.py:92-112
-          case S_L2: plen = 1 + v; pm = k - plen + 1; st = S_A2; break;
-          case S_A2: pa = v; st = S_B2; break;
-          case S_B2:
-            if (v != pa) {
-              if (abs(pa - v) >= plen) {
-                emit(min(pa, v), max(pa, v), plen);
-                if (--hops == 0) finish(); else st = S_L2;
-              } else {
-                st = S_A2;  // the whole pair is redrawn
-              }
-            }
-            break;
-          case S_L3: plen = 1 + v; pm = k - plen + 1; st = S_P3; break;  // sct.py:115-135
-          case S_P3: pa = v; st = S_D3; break;
-          default:  // S_D3
-            if (v != pa) {
-              emit(pa, v, plen);
-              finish();
-            }
-            break;
+        const bool same = v == pa;
+        const bool pb = ph == 4 && !same;
+        const bool rej = pb && op == 2 && abs(pa - v) < plen;
+        const bool pair_done = pb && !rej;
+        const uint32_t lo = (uint32_t)min(pa, v), hi = (uint32_t)max(pa, v);
+        const uint32_t x = op == 2 ? lo | (hi << 8) | ((uint32_t)plen << 16)
+                                   : (uint32_t)pa | ((uint32_t)v << 8) | (op == 3 ? (uint32_t)plen << 16 : 0u);
+        e0 = pair_done && nev == 0 ? x : e0;
+        e1 = pair_done && nev == 1 ? x : e1;
+        e2 = pair_done && nev == 2 ? x : e2;
+        nev += pair_done ? 1 : 0;
+        const int nop = v < p.p1 ? 1 : v < p.p2 ? 2 : 3;
+        int ns = same ? stt : rej ? 14 : (op == 1 ? 13 : 10);  // phase 4
+        ns = ph == 3 ? 16 + op : ns;
+        ns = ph == 2 ? 12 + op : ns;
+        ns = ph == 1 ? (op == 1 ? 13 : 10) : ns;
+        ns = ph == 0 ? (nop == 3 ? 11 : 4 + nop) : ns;
+        hops = ph == 0 ? 1 : ph == 1 ? 1 + v : hops - (pair_done ? 1 : 0);
+        plen = ph == 2 ? 1 + v : plen;
+        pm = ph == 2 ? k - v : pm;
+        pa = ph == 3 ? v : pa;
+        stt = ns;
+        if (pair_done && hops == 0) {  // the proposal is complete: queue it
+          const int slot = (q_head + q_cnt) % kQSlots;
+          qword(slot, 0) = (uint32_t)op | ((uint32_t)nev << 4);
+          qword(slot, 1) = e0;
+          qword(slot, 2) = e1;
+          qword(slot, 3) = e2;
+          ++q_cnt;
+          ++parsed;
+          stt = 0;
+          nev = 0;
         }
       };
 
