@@ -10,6 +10,14 @@ namespace ccg {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// full-warp shfl.sync.idx with clamp 0x1f: the source lane is bits [4:0] of `src_lane`
+// (callers pass unmasked indices; __shfl_sync would mask them again)
+__device__ __forceinline__ uint32_t shfl_idx_raw(uint32_t v, uint32_t src_lane) {
+  uint32_t r;
+  asm volatile("shfl.sync.idx.b32 %0, %1, %2, 0x1f, 0xffffffff;" : "=r"(r) : "r"(v), "r"(src_lane));
+  return r;
+}
+
 // 128 draws of one stream as letters int(u*26), 5 bits each.  Lane L holds the letters of
 // draws base+4L .. base+4L+7 (its own Philox block plus lane L+1's), so the next FOUR
 // letters -- two tries' pairs in the common no-redraw case -- come out of one 64-bit
@@ -158,9 +166,11 @@ struct ByteWindow2 {
   __device__ __forceinline__ uint32_t round_letters(int lane) const {
     const uint32_t src = (uint32_t)lane >= (o >> 2) ? A : B;
     const uint32_t pos = o + 2u * (uint32_t)lane;
-    const int w = (int)(pos >> 2);
-    const uint32_t x0 = __shfl_sync(kFull, src, w & 31), x1 = __shfl_sync(kFull, src, (w + 1) & 31);
-    return __funnelshift_r(x0, x1, (pos & 3u) * 8u);
+    const uint32_t w = pos >> 2;
+    // shfl.idx takes the source lane from bits [4:0] of the index (clamp 0x1f), and the
+    // funnel shift's amount is taken mod 32: no masking needed
+    const uint32_t x0 = shfl_idx_raw(src, w), x1 = shfl_idx_raw(src, w + 1u);
+    return __funnelshift_r(x0, x1, pos * 8u);
   }
   __device__ __forceinline__ int next(int lane) {
     if (o > 255u) advance(lane);

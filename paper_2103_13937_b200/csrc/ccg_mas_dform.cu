@@ -39,13 +39,17 @@ namespace ccg {
 namespace {
 
 constexpr int kDWarps = 8;
-constexpr int kTS = 34;  // T row stride (int16): column walks are conflict-free (17 words/row)
+// T row stride (int16) = N's row stride (kNT): T[a][b] and NT[a][b] (= N[b][a]) share the index
+// a * 36 + b, so an on-demand delta computes two indices for its four T/N reads (and KS uses
+// the same stride for the fifth)
+constexpr int kTS = 36;
 constexpr int kNS = 33;  // S row stride (int32)
 // N is stored TRANSPOSED: lane y's column N[.][y] is the contiguous row NT[y][.], stride 36
 // words (16-byte aligned), so the accept's rank-2 update streams it with 128-bit loads and
 // stores (each 8-lane phase of an LDS.128 hits distinct banks: 4y + x mod 32)
 constexpr int kNT = 36;
 constexpr int kDS = 32;  // D row stride (int32): D[a][b] sits in bank b
+constexpr int kKS = 36;  // KS row stride (int32), = kTS
 
 // TABLE = true keeps D in shared memory (rebuilt on every accept); TABLE = false computes
 // each looked-up delta from T, N and ks on demand (no rebuild, 3.3 KB less per warp).
@@ -53,14 +57,14 @@ template <bool TABLE>
 struct alignas(16) DWarp {
   uint64_t rk[22];  // Philox round keys of the current worker's stream (+ M0*k0)
   int2 uv[28];      // accept: the (u_x, v_x) row factors of the N update (x < 26; 26, 27 pad)
-  int16_t T[kAlpha * kTS + 4];  // (+4: N starts 16-byte aligned)
-  int N[kAlpha * kNT];          // N[x][y] at N[y * kNT + x]
+  int16_t T[kAlpha * kTS];  // (936 int16: N starts 16-byte aligned)
+  int N[kAlpha * kNT];      // N[x][y] at N[y * kNT + x]
   int D[TABLE ? kAlpha * kDS : 4];
 };
 template <bool TABLE>
 struct DBlock {
   int S[kAlpha * kNS];
-  int KS[kAlpha * kDS];
+  int KS[kAlpha * kKS];
   DWarp<TABLE> w[kDWarps];
 };
 
@@ -68,7 +72,7 @@ struct DBlock {
 // ciphertext), computed once per ciphertext by dform_init_kernel when several workers share
 // a ciphertext: T and N in the shared-memory layout, and the score.
 struct alignas(16) CipherInit {
-  int16_t T[kAlpha * kTS + 4];
+  int16_t T[kAlpha * kTS];
   int N[kAlpha * kNT];
   int score;
   int pad_[3];
@@ -98,21 +102,25 @@ __device__ __forceinline__ void rebuild_D(const BT& B, WT& W, int lane) {
   for (int x = 0; x < kAlpha; ++x) {
     const int txx = __shfl_sync(kFull, tyy, x), nxx = __shfl_sync(kFull, nyy, x);
     const int kt = txx + tyy - t_at(W, x, y) - t_at(W, y, x);
-    const int dv = kt * B.KS[x * kDS + y] - nxx - nyy + W.N[y * kNT + x] + W.N[x * kNT + y];
+    const int dv = kt * B.KS[x * kKS + y] - nxx - nyy + W.N[y * kNT + x] + W.N[x * kNT + y];
     if (lane < kAlpha) W.D[x * kDS + y] = dv;
   }
   __syncwarp();
 }
 
-// D[a][b] from T, N and ks; tdg / ndg hold T[lane][lane] / N[lane][lane] (all lanes call)
+// D[a][b] from T, N and ks; tdg / ndg hold T[lane][lane] / N[lane][lane] (all lanes call).
+// ks_s: 32-bit shared address of B.KS.  With i1 = a*36 + b, i2 = b*36 + a:
+// T[a][b] = T[i1], T[b][a] = T[i2], N[b][a] = NT[i1], N[a][b] = NT[i2], ks = KS[i1].
 template <class WT>
 __device__ __forceinline__ int delta_at(uint32_t ks_s, const WT& W, int tdg, int ndg, int a, int b) {
+  static_assert(kTS == kNT && kKS == kNT, "delta_at shares one index across T, N and KS");
   const int ta = __shfl_sync(kFull, tdg, a), tb = __shfl_sync(kFull, tdg, b);
   const int na = __shfl_sync(kFull, ndg, a), nb = __shfl_sync(kFull, ndg, b);
-  const int kt = ta + tb - t_at(W, a, b) - t_at(W, b, a);
+  const uint32_t i1 = (uint32_t)(a * kTS + b), i2 = (uint32_t)(b * kTS + a);
+  const int kt = ta + tb - W.T[i1] - W.T[i2];
   // ks through a 32-bit shared address (a generic B.KS access recomputes the window base)
-  const int ks = (int)lds_u32(ks_s + 4u * (uint32_t)(a * kDS + b));
-  return kt * ks - na - nb + W.N[b * kNT + a] + W.N[a * kNT + b];
+  const int ks = (int)lds_u32(ks_s + 4u * i1);
+  return kt * ks - na - nb + W.N[i2] + W.N[i1];
 }
 
 // max over the 325 on-demand deltas; lane y scans column y
@@ -170,7 +178,7 @@ __device__ __forceinline__ void stage_block_tables(DBlock<TABLE>& B, const int64
   __syncthreads();
   for (int i = threadIdx.x; i < kAlpha * kAlpha; i += blockDim.x) {
     const int x = i / kAlpha, y = i - x * kAlpha;
-    B.KS[x * kDS + y] =
+    B.KS[x * kKS + y] =
         B.S[x * kNS + x] + B.S[y * kNS + y] - B.S[x * kNS + y] - B.S[y * kNS + x];
   }
   __syncthreads();

@@ -70,7 +70,14 @@ for order in (2, 3, 4):
     for i in (0, 21, 44):
         _, s, _ = O.sct_fast_worker(lane_c[lane_cof[i]], q.table, order, int(lane_k[i]), 40, 6, i)
         assert int(r.scores[i]) == s, (order, i)
-t4 = rng.integers(0, 60000, 26**4)
+    # regular grids (every k divides 200): the window-sum tables (sct_ftab_kernel)
+    reg_cof = np.zeros(40, np.int32)
+    reg_k = np.array([(4, 5, 8, 10)[i % 4] for i in range(40)], np.int32)
+    r = engine.sct_fast_climb(lane_c, reg_cof, lane_keys[:40], q, reg_k, 40)
+    for i in (0, 1, 2, 3):
+        _, s, _ = O.sct_fast_worker(lane_c[0], q.table, order, int(reg_k[i]), 40, 6, i)
+        assert int(r.scores[i]) == s, ("regular", order, i)
+t4 =rng.integers(0, 60000, 26**4)
 engine.mas_climb(cs, cof, keys, t4, 200, order=4, computed=True, lookups=True)
 engine.bench_l2_gather(26**4)
 # scoring / delta / test-set kernels
