@@ -334,18 +334,19 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
       // c2 of lane r0 unless that equals c0 too; the pairs after it are shifted by one draw
       // (c1, c2) up to the next redraw.  rng.py:81-89 exactly.
       const uint32_t wd = win.round_letters(lane);
-      const int c0 = (int)(wd & 0xffu), c1 = (int)((wd >> 8) & 0xffu), c2 = (int)((wd >> 16) & 0xffu);
+      // (one PRMT per byte: __byte_perm(x, 0, 0x444k) = byte k of x, zero-extended)
+      const int c0 = (int)(wd & 0xffu), c1 = (int)__byte_perm(wd, 0u, 0x4441u), c2 = (int)__byte_perm(wd, 0u, 0x4442u);
       // (o <= 128, so all 32 pairs and their redraw partners lie in the 256-draw window)
       // Lane j + 1's first two letters: after a second redraw the pairs realign on even
       // draws again, one lane further on (lane 31 has no successor: R <= 31 then).
       const uint32_t wn = __shfl_down_sync(kFull, wd, 1);
-      const int n0 = (int)(wn & 0xffu), n1 = (int)((wn >> 8) & 0xffu);
+      const int n0 = (int)(wn & 0xffu), n1 = (int)__byte_perm(wn, 0u, 0x4441u);
       const uint32_t eqA = __ballot_sync(kFull, c0 == c1);
-      const uint32_t r0 = eqA ? (uint32_t)(__ffs(eqA) - 1) : 32u;
+      const uint32_t r0 = eqA ? (uint32_t)(__ffs(eqA) - 1) : 32u;  // (< 32 iff eqA != 0)
       uint32_t R = 32u;    // pairs in this round
       uint32_t r1 = 32u;   // the second redraw pair (shifted alignment), if handled
       bool seq = false;    // the round stopped at a pair that needs the sequential path
-      if (r0 < 32u) {
+      if (eqA != 0u) {
         const int c2r = __shfl_sync(kFull, c2, (int)r0), c0r = __shfl_sync(kFull, c0, (int)r0);
         if (c2r == c0r) {
           R = r0;
@@ -386,7 +387,9 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
       const uint32_t acc = __ballot_sync(kFull, d > 0);
       if (acc == 0) {  // the common case: R rejections
         t += R;
-        win.o += 2u * R + (R > r0 ? 1u : 0u) + (R > r1 ? 1u : 0u);
+        // + (R > r0) + (R > r1), the redraws consumed (all values <= 32: the sign bit of the
+        // difference is the comparison, one LEA.HI each)
+        win.o += 2u * R + ((r0 - R) >> 31) + ((r1 - R) >> 31);
         if (seq && t < climbings) {  // one try through the sequential redraw path
           int a2, b2;
           win.pair(lane, a2, b2);
@@ -405,7 +408,7 @@ __global__ void __launch_bounds__(kDWarps * 32, TABLE ? 3 : 4) mas_climb_dform_k
       const int ak = __shfl_sync(kFull, pa, (int)k), bk = __shfl_sync(kFull, pb, (int)k);
       const int dk = __shfl_sync(kFull, d, (int)k);
       t += k;
-      win.o += 2u * (k + 1u) + (k + 1u > r0 ? 1u : 0u) + (k + 1u > r1 ? 1u : 0u);
+      win.o += 2u * (k + 1u) + ((r0 - (k + 1u)) >> 31) + ((r1 - (k + 1u)) >> 31);
       accept(ak, bk, dk);
       last = (int)t;
       ++nacc;
