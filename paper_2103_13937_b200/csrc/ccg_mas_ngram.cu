@@ -372,18 +372,18 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
       // first miss -- proposals never read the state, so computing ahead is exact.
       const uint32_t o = win.o;
       const uint32_t wd = win.round_letters(lane);
-      const uint32_t c0 = wd & 0xffu, c1 = (wd >> 8) & 0xffu, c2 = (wd >> 16) & 0xffu;
+      const uint32_t c0 = wd & 0xffu, c1 = __byte_perm(wd, 0u, 0x4441u), c2 = __byte_perm(wd, 0u, 0x4442u);
       // (o <= 128, so all 32 pairs and their redraw partners lie in the 256-draw window)
       // lane j + 1's first two letters: after a second redraw the pairs realign on even draws
       // one lane further on (three segments, as in ccg_mas_dform.cu)
       const uint32_t wn = __shfl_down_sync(kFull, wd, 1);
-      const uint32_t n0 = wn & 0xffu, n1 = (wn >> 8) & 0xffu;
+      const uint32_t n0 = wn & 0xffu, n1 = __byte_perm(wn, 0u, 0x4441u);
       const uint32_t eqA = __ballot_sync(kFull, c0 == c1);
       const uint32_t r0 = eqA ? (uint32_t)(__ffs(eqA) - 1) : 32u;
       uint32_t R = 32u;    // pairs in this round
       uint32_t r1 = 32u;   // the second redraw pair, if handled
       bool seq = false;    // the round stopped at a pair that needs the sequential path
-      if (r0 < 32u) {
+      if (eqA != 0u) {  // (r0 < 32)
         const uint32_t c2r = __shfl_sync(kFull, c2, (int)r0), c0r = __shfl_sync(kFull, c0, (int)r0);
         if (c2r == c0r) {
           R = r0;
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
         const int ak = __shfl_sync(kFull, (int)pa, (int)k), bk = __shfl_sync(kFull, (int)pb, (int)k);
         const int dk = __shfl_sync(kFull, d, (int)k);
         t += k;
-        win.o += 2u * (k + 1u) + (k + 1u > r0 ? 1u : 0u) + (k + 1u > r1 ? 1u : 0u);
+        win.o += 2u * (k + 1u) + ((r0 - (k + 1u)) >> 31) + ((r1 - (k + 1u)) >> 31);  // + redraws
         accept(ak, bk, dk);
         last = (int)t;
         since = 0;
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(kNgWarps * 32, 512 / (kNgWarps * 16)) mas_ngra
       }
       t += f;
       since += f;
-      win.o += 2u * f + (f > r0 ? 1u : 0u) + (f > r1 ? 1u : 0u);
+      win.o += 2u * f + ((r0 - f) >> 31) + ((r1 - f) >> 31);  // + (f > r0) + (f > r1)
       if (f < R) {
         // lane g < kMissBatch takes the g-th miss of the round
         uint32_t m = miss, mg = 32u;

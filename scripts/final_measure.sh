@@ -5,6 +5,8 @@
 TAG=${1:-final}; mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_gpu_$TAG.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke_$TAG.log
+# the reference's own test-suite against the aliased engine (staged by run_reference_suite.py --stage)
+if [ -d oracle/_ref/pkg/tests ]; then timeout 600 python tests/tools/run_reference_suite.py --run > /dev/null 2>&1; echo "refsuite rc=$?"; cp gpurun_out/reference_suite.txt gpurun_out/reference_suite_$TAG.txt; tail -1 gpurun_out/reference_suite_$TAG.txt; fi
 timeout 900 python bench.py --steps 20 --warmup 3 > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo "bench rc=$?"
 timeout 900 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/ref_$TAG.json 2> gpurun_out/ref_$TAG.err; echo "ref rc=$?"
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --profile > /dev/null 2>&1
