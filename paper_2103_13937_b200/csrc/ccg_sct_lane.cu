@@ -35,7 +35,7 @@
 //              up warp-collectively once per round, so the lanes' Philox blocks are
 //              generated together instead of diverging at every draw
 //   queue      parsed proposals: a header word + up to kSctLaneMaxHops events each
-//   key, cand  u8[KMAX][32];  colstart u16[KMAX][32];  window sums i32[KMAX][32] (FAST)
+//   key, cand  u8[KMAX][32];  colstart u16[KMAX + 8][32] (+8: next-row copies);  window sums i32[KMAX][32] (FAST)
 //   plan       the numpy pairwise recursion of this pass's text length (PARITY)
 //   text       the pass's ciphertext
 // The log table is staged per block: bigram directly (676 f64 / i32); trigram as a byte index
@@ -78,9 +78,15 @@ constexpr int pow26(int o) { return o == 2 ? 676 : o == 3 ? 17576 : 456976; }
 
 __host__ __device__ constexpr size_t round16(size_t b) { return (b + 15) & ~(size_t)15; }
 
+// colstart has kCsExt extra entries per lane: cs[k + i] = cs[i] + 1 (column i one row down),
+// so the letter of any of the next kCsExt positions -- in this row or, past the row's end,
+// the next -- is txt[cs[c + j] + r] with no per-position row select (ParityTerms::letters)
+constexpr int kCsExt = 8;
+constexpr int cs_ext_of(int mode) { return mode == 0 ? kCsExt : 0; }  // (parity mode only)
+
 template <int MODE, int KMAX>
 __host__ __device__ constexpr size_t lane_fixed_bytes() {
-  return (size_t)ring_of(MODE) * 128 + kQueueBytes + 2 * KMAX * 32 + KMAX * 64 +
+  return (size_t)ring_of(MODE) * 128 + kQueueBytes + 2 * KMAX * 32 + (KMAX + cs_ext_of(MODE)) * 64 +
          (MODE == 1 ? KMAX * 128 : 256);
 }
 template <int MODE, int ORDER, bool TSMEM, bool CIDX>
@@ -244,20 +250,19 @@ struct ParityTerms {
     }
   }
   // the letters of the next G positions, loaded before any is used.  For G >= 4 and k >= G
-  // the block spans at most one row boundary, so the column starts come from two base
-  // pointers with immediate offsets instead of a per-position walk.
+  // the block spans at most one row boundary: positions past the row's end read the
+  // extended colstart (cs[k + i] = cs[i] + 1), so every letter is txt[cs[c + j] + r] -- one
+  // base pointer with immediate offsets, no per-position select.
   template <int G>
   __device__ __forceinline__ void letters(int (&L)[ORDER - 1 + G]) {
+    static_assert(G <= kCsExt, "the extended colstart covers one row wrap of G positions");
     if (G >= 4 && wk.k >= G) {
       const int k = wk.k, c = wk.c, r = wk.r;
       const int split = k - c;  // positions j < split stay in row r
       const uint16_t* cb = wk.cs + 32 * c;
-      const uint16_t* cb2 = wk.cs - 32 * split;  // cb2[32 j] = colstart[j - split]
+      const uint8_t* tr = wk.txt + r;
 #pragma unroll
-      for (int j = 0; j < G; ++j) {
-        const bool same = j < split;
-        L[ORDER - 1 + j] = wk.txt[(same ? cb[32 * j] : cb2[32 * j]) + (same ? r : r + 1)];
-      }
+      for (int j = 0; j < G; ++j) L[ORDER - 1 + j] = tr[cb[32 * j]];
       if (split > G) {
         wk.c = c + G;
       } else {
@@ -417,7 +422,7 @@ __global__ void __launch_bounds__(kSctLaneWarps * 32, MODE == 1 ? 3 : CCG_LANE_M
   uint8_t* keyp = kb + lane;                                  // key[q] at keyp[32 q]
   uint8_t* candp = keyp + 32 * KMAX;                          // cand[q] at candp[32 q]
   uint16_t* csp = reinterpret_cast<uint16_t*>(kb + 64 * KMAX) + lane;  // colstart[c] at [32 c]
-  unsigned char* aux = kb + 128 * KMAX;
+  unsigned char* aux = kb + 128 * KMAX + 64 * cs_ext_of(MODE);
   int32_t* gp = reinterpret_cast<int32_t*>(aux) + lane;       // FAST: G[w] at gp[32 w]
   int32_t* plan = reinterpret_cast<int32_t*>(aux);            // PARITY
   uint8_t* txt = aux + (MODE == 1 ? 128 * KMAX : 256);
@@ -510,6 +515,7 @@ __global__ void __launch_bounds__(kSctLaneWarps * 32, MODE == 1 ? 3 : CCG_LANE_M
           const int c = keyp[32 * q];
           candp[32 * q] = (uint8_t)c;
           csp[32 * c] = (uint16_t)s;
+          if (MODE == 0 && c < kCsExt) csp[32 * (k + c)] = (uint16_t)(s + 1);
           s += seglen(c);
         }
         if (MODE == 0) {
@@ -637,6 +643,7 @@ __global__ void __launch_bounds__(kSctLaneWarps * 32, MODE == 1 ? 3 : CCG_LANE_M
             const int c = candp[32 * q];
             if (MODE == 1 && csp[32 * c] != s) dirty |= 1ULL << c;
             csp[32 * c] = (uint16_t)s;
+            if (MODE == 0 && c < kCsExt) csp[32 * (k + c)] = (uint16_t)(s + 1);
             s += seglen(c);
           }
         }
@@ -685,6 +692,7 @@ __global__ void __launch_bounds__(kSctLaneWarps * 32, MODE == 1 ? 3 : CCG_LANE_M
             const int c = keyp[32 * q];
             candp[32 * q] = (uint8_t)c;
             csp[32 * c] = (uint16_t)s;
+            if (MODE == 0 && c < kCsExt) csp[32 * (k + c)] = (uint16_t)(s + 1);
             s += seglen(c);
           }
         }
