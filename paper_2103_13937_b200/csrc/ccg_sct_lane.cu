@@ -78,11 +78,16 @@ constexpr int pow26(int o) { return o == 2 ? 676 : o == 3 ? 17576 : 456976; }
 
 __host__ __device__ constexpr size_t round16(size_t b) { return (b + 15) & ~(size_t)15; }
 
-// colstart has kCsExt extra entries per lane: cs[k + i] = cs[i] + 1 (column i one row down),
-// so the letter of any of the next kCsExt positions -- in this row or, past the row's end,
-// the next -- is txt[cs[c + j] + r] with no per-position row select (ParityTerms::letters)
+// colstart has kCsExt extra entries per lane: cs[m] = cs[m mod k] + m div k for
+// k <= m < k + kCsExt (the columns of the following rows), so the letter of any of the next
+// kCsExt positions -- in this row or past its end -- is txt[cs[c + j] + r] with no
+// per-position row select (ParityTerms::letters)
 constexpr int kCsExt = 8;
 constexpr int cs_ext_of(int mode) { return mode == 0 ? kCsExt : 0; }  // (parity mode only)
+// the extended entries of column c (segment start s): cs[c + q k] = s + q, q >= 1
+__device__ __forceinline__ void set_cs_ext(uint16_t* csp, int k, int c, int s) {
+  for (int m = c + k, q = 1; m < k + kCsExt; m += k, ++q) csp[32 * m] = (uint16_t)(s + q);
+}
 
 template <int MODE, int KMAX>
 __host__ __device__ constexpr size_t lane_fixed_bytes() {
@@ -249,26 +254,26 @@ struct ParityTerms {
       h[i] = wk.at(cc, rr);
     }
   }
-  // the letters of the next G positions, loaded before any is used.  For G >= 4 and k >= G
-  // the block spans at most one row boundary: positions past the row's end read the
-  // extended colstart (cs[k + i] = cs[i] + 1), so every letter is txt[cs[c + j] + r] -- one
-  // base pointer with immediate offsets, no per-position select.
+  // the letters of the next G positions, loaded before any is used.  For G >= 4, positions
+  // past the row's end read the extended colstart (cs[m] = cs[m mod k] + m div k, m < k + 8),
+  // so every letter is txt[cs[c + j] + r] -- one base pointer with immediate offsets, no
+  // per-position select, for any key length.
   template <int G>
   __device__ __forceinline__ void letters(int (&L)[ORDER - 1 + G]) {
     static_assert(G <= kCsExt, "the extended colstart covers one row wrap of G positions");
-    if (G >= 4 && wk.k >= G) {
+    if (G >= 4) {
       const int k = wk.k, c = wk.c, r = wk.r;
-      const int split = k - c;  // positions j < split stay in row r
       const uint16_t* cb = wk.cs + 32 * c;
       const uint8_t* tr = wk.txt + r;
 #pragma unroll
       for (int j = 0; j < G; ++j) L[ORDER - 1 + j] = tr[cb[32 * j]];
-      if (split > G) {
-        wk.c = c + G;
-      } else {
-        wk.c = G - split;
-        wk.r = r + 1;
+      int nc = c + G, nr = r;
+      while (nc >= k) {  // once for k >= G
+        nc -= k;
+        ++nr;
       }
+      wk.c = nc;
+      wk.r = nr;
       return;
     }
     int cc[G], rr[G];
@@ -515,7 +520,7 @@ __global__ void __launch_bounds__(kSctLaneWarps * 32, MODE == 1 ? 3 : CCG_LANE_M
           const int c = keyp[32 * q];
           candp[32 * q] = (uint8_t)c;
           csp[32 * c] = (uint16_t)s;
-          if (MODE == 0 && c < kCsExt) csp[32 * (k + c)] = (uint16_t)(s + 1);
+          if (MODE == 0) set_cs_ext(csp, k, c, s);
           s += seglen(c);
         }
         if (MODE == 0) {
@@ -643,7 +648,7 @@ __global__ void __launch_bounds__(kSctLaneWarps * 32, MODE == 1 ? 3 : CCG_LANE_M
             const int c = candp[32 * q];
             if (MODE == 1 && csp[32 * c] != s) dirty |= 1ULL << c;
             csp[32 * c] = (uint16_t)s;
-            if (MODE == 0 && c < kCsExt) csp[32 * (k + c)] = (uint16_t)(s + 1);
+            if (MODE == 0) set_cs_ext(csp, k, c, s);
             s += seglen(c);
           }
         }
@@ -692,7 +697,7 @@ __global__ void __launch_bounds__(kSctLaneWarps * 32, MODE == 1 ? 3 : CCG_LANE_M
             const int c = keyp[32 * q];
             candp[32 * q] = (uint8_t)c;
             csp[32 * c] = (uint16_t)s;
-            if (MODE == 0 && c < kCsExt) csp[32 * (k + c)] = (uint16_t)(s + 1);
+            if (MODE == 0) set_cs_ext(csp, k, c, s);
             s += seglen(c);
           }
         }
