@@ -338,7 +338,7 @@ def config_block(args, world):
 
 # ------------------------------------------------------------------ GPU leg
 # The committed ncu --set full capture of the headline kernel (update with the kernel):
-DFORM_PROFILE = "profiles/r2g_dform_ncu.txt"
+DFORM_PROFILE = "profiles/r2h_dform_ncu.txt"
 
 
 def read_ncu_summary(rel: str) -> dict | None:
