@@ -42,6 +42,26 @@ def _oracle_parity(ciphers, cof, klens, seed, streams, logs, climbings, order, *
     return scores, keys, last
 
 
+@pytest.mark.parametrize("order", [2, 3])
+def test_lane_kernel_every_short_key_length(order):
+    """Every key length 2..20 (and 31, 32) on short texts: an 8-position letter block wraps
+    several rows when k < 8 and exactly one row end for k >= 8 -- the extended colstart
+    (cs[m] = cs[m mod k] + m div k) must give the same letters as the per-position walk."""
+    rng = np.random.default_rng(900 + order)
+    logs = -rng.random(26**order) * 20 - 1
+    ks = list(range(2, 21)) + [31, 32]
+    ciphers = [rng.integers(0, 26, L) for L in (41, 64, 97)]
+    cof = np.array([i % 3 for i in range(len(ks) * 4)], np.int32)
+    klens = np.array([ks[i // 4] for i in range(len(cof))], np.int32)
+    streams = [int(s) for s in rng.integers(0, 2**40, len(cof))]
+    keys = philox_keys([77], streams)
+    res = engine.sct_climb(ciphers, cof, keys, logs, klens, 300, order=order, kernel="lane")
+    want_s, want_k, _ = _oracle_parity(ciphers, cof, klens, 77, streams, logs, 300, order)
+    assert res.scores.tolist() == want_s.tolist()
+    for i in range(len(cof)):
+        assert np.array_equal(res.keys[i, :klens[i]].astype(np.int64), want_k[i]), i
+
+
 @pytest.mark.parametrize("order", [2, 3, 4])
 def test_lane_kernel_vs_oracle(order):
     """Ragged text lengths AND key lengths in one launch, chunks of 32 workers spanning
