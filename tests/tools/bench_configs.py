@@ -50,6 +50,22 @@ KEYGEN = 2**32 - 2
 THREADS = os.cpu_count() or 1
 
 
+
+C3_PROFILE = "profiles/r2h_c3_lane_ncu.txt"
+
+
+def _ncu_counter(rel, pat):
+    """One counter from a committed profiles/*_ncu.txt summary (None if absent)."""
+    import re
+
+    try:
+        txt = (Path(__file__).resolve().parents[2] / rel).read_text()
+    except OSError:
+        return None
+    m = re.search(pat + r"\s+([0-9.eE+]+)", txt)
+    return float(m.group(1)) if m else None
+
+
 def timed(fn, reps=1):
     fn()  # warm-up (also loads tables / allocates scratch)
     t0 = time.perf_counter()
@@ -204,9 +220,25 @@ def c3(bounded=False, quick=False):
             "achieved": total_evals / total_s * lpe, "peak": peak, "unit": "lookups/s",
             "frac": total_evals / total_s * lpe / peak,
             "peak_source": "148 SMs x 32 lane lookups per clock x 1965 MHz (SURVEY 8d formula)"}
+    # the counter-based bound: shared-memory wavefronts per evaluation from the committed ncu
+    # capture of the same launch shape (1,000 climbings) x this run's rate, against one
+    # wavefront per SM per clock -- the random text / table gathers replay on bank conflicts,
+    # so this, not the lane-lookup peak, is the pipe the kernel fills
+    wf = _ncu_counter(C3_PROFILE, r"l1tex__data_pipe_lsu_wavefronts_mem_shared\.sum")
+    tr = _ncu_counter(C3_PROFILE, r"tries in the captured launch:")
+    pipe = None
+    if wf and tr:
+        wpe = wf / tr
+        wpeak = 148 * 1.965e9
+        pipe = {"bound": "smem-pipe", "wavefronts_per_eval": wpe,
+                "achieved": total_evals / total_s * wpe, "peak": wpeak, "unit": "wavefronts/s",
+                "frac": total_evals / total_s * wpe / wpeak,
+                "ncu_pct_of_peak": _ncu_counter(C3_PROFILE, r"l1tex__data_pipe_lsu_wavefronts_mem_shared\.sum\.pct_of_peak_sustained_elapsed"),
+                "source": f"ncu wavefronts / tries ({C3_PROFILE}) x this run's evals/s; peak = 1 "
+                          "wavefront per SM per clock at 1965 MHz"}
     out = [{"config": "C3", "what": "SCT k=5..20, 1000 ciphertexts x 400 letters, trigram log "
                                     "table, parity mode (float64, numpy pairwise order)",
-            "roofline": roof,
+            "roofline": roof, "smem_pipe_roofline": pipe,
             "workers_per_cipher": W, "climbings": K, "launches": "one (ragged key lengths)",
             "evals": total_evals, "seconds": total_s, "evals_per_s": total_evals / total_s,
             "recovered": int(sum(rec)), "of": n_c,
